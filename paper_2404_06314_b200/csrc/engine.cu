@@ -1,0 +1,869 @@
+// libvqc.so: kernels, launch orchestration and the C ABI declared in
+// include/vqc.h. See kernels.cuh for the execution model and DESIGN.md for the
+// roofline accounting.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/vqc.h"
+#include "kernels.cuh"
+#include "scheduler.h"
+
+namespace vqc {
+
+// ------------------------------------------------------------------ kernels
+
+template <bool DUAL>
+__device__ void observe(const DevProgram& D, const RunArgs& A, const PassDesc* pd, double2* s_psi,
+                        double2* s_phi, const double* s_u_row, const Group& grp, double* s_red,
+                        int& red_buf, uint32_t tile_base, int k, int64_t bl0, bool do_expect,
+                        int seed_mode, int bra, int tile, int n_tiles) {
+  const int Nt = 1 << k;
+  if (do_expect) {
+    const int red_stride = A.red_slots * grp.S * grp.W;
+    double* redbuf = s_red + red_buf * red_stride;
+    for (int m = 0; m < D.M; ++m) {
+      const int lo = D.term_offs[m], hi = D.term_offs[m + 1];
+      double acc = 0.0;
+      for (int l = grp.gi; l < Nt; l += grp.TPS) {
+        const uint32_t j = tile_base | (pd ? local_to_global(*pd, (uint32_t)l, k) : (uint32_t)l);
+        const double2 x = s_psi[swz((uint32_t)l)];
+        acc += zweight(D, j, lo, hi) * (x.x * x.x + x.y * x.y);
+      }
+      acc = grp.reduce(acc);
+      if (grp.leader()) redbuf[grp.red_index(m)] = acc;
+    }
+    __syncthreads();
+    const int total = D.M * grp.S;
+    for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+      const int m = idx / grp.S, s_ = idx - m * grp.S;
+      double v = 0.0;
+      for (int w = 0; w < grp.W; ++w) v += redbuf[(m * grp.S + s_) * grp.W + w];
+      const int64_t bl = bl0 + s_;
+      if (bl < A.nb) A.expect[(bl * D.M + m) * n_tiles + tile] = v;
+    }
+    red_buf ^= 1;
+  }
+  if constexpr (DUAL) {
+    if (seed_mode != 0) {
+      for (int l = grp.gi; l < Nt; l += grp.TPS) {
+        const uint32_t j = tile_base | (pd ? local_to_global(*pd, (uint32_t)l, k) : (uint32_t)l);
+        double w = 0.0;
+        if (seed_mode == 1) {
+          for (int m = 0; m < D.M; ++m) {
+            const double u = s_u_row[m];
+            if (u != 0.0) w += u * zweight(D, j, D.term_offs[m], D.term_offs[m + 1]);
+          }
+        } else {
+          w = zweight(D, j, D.term_offs[bra], D.term_offs[bra + 1]);
+        }
+        const uint32_t p = swz((uint32_t)l);
+        const double2 x = s_psi[p];
+        s_phi[p] = make_double2(w * x.x, w * x.y);
+      }
+    }
+  }
+}
+
+// Whole state on chip: one CTA owns S samples of n <= 12 qubits and runs
+// forward, expectations, seed and the adjoint sweep without touching HBM.
+template <int R, bool DUAL>
+__global__ void __launch_bounds__(256) k_smem(DevProgram D, RunArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* smem = reinterpret_cast<double2*>(smem_raw);
+  const int n = D.n, N = 1 << n;
+  Group grp;
+  grp.tid = threadIdx.x;
+  grp.TPS = 1 << (n - R);
+  grp.S = A.S;
+  grp.gi = threadIdx.x & (grp.TPS - 1);
+  grp.sl = threadIdx.x >> (n - R);
+  grp.W = grp.TPS >= 32 ? grp.TPS >> 5 : 1;
+  const int64_t bl0 = (int64_t)blockIdx.x * A.S;
+  const int64_t bl = bl0 + grp.sl;
+  const bool valid = bl < A.nb;
+  const int64_t b = A.b0 + (valid ? bl : 0);
+  double2* s_psi = smem + (size_t)grp.sl * N;
+  double2* s_phi = smem + (size_t)(A.S + grp.sl) * N;
+  double2* s_cs_all = smem + (size_t)(DUAL ? 2 : 1) * A.S * N;
+  double2* s_cs = s_cs_all + (size_t)grp.sl * D.n_rot;
+  double* s_red = reinterpret_cast<double*>(s_cs_all + (size_t)A.S * D.n_rot);
+  double* s_u = s_red + 2 * A.red_slots * A.S * grp.W;
+
+  for (int r = grp.gi; r < D.n_rot; r += grp.TPS)
+    s_cs[r] = valid ? rot_cs(D, A, b, r) : make_double2(1.0, 0.0);
+  for (int l = grp.gi; l < N; l += grp.TPS) s_psi[swz((uint32_t)l)] = make_double2(l == 0 ? 1.0 : 0.0, 0.0);
+  if (DUAL && A.upstream != nullptr)
+    for (int m = grp.gi; m < D.M; m += grp.TPS) s_u[grp.sl * D.M + m] = valid ? A.upstream[b * D.M + m] : 0.0;
+  __syncthreads();
+
+  int red_buf = 0;
+  const PassDesc* pd = D.passes;
+  run_segments<R, false>(D, A, pd->seg_begin, pd->seg_end, s_psi, s_psi, s_cs, 0, s_red, red_buf, grp,
+                         0u, bl0, A.nb, 0, 0, 1);
+  if constexpr (!DUAL) {
+    observe<false>(D, A, nullptr, s_psi, s_psi, nullptr, grp, s_red, red_buf, 0u, n, bl0, true, 0, 0, 0, 1);
+  } else {
+    if (!A.jacobian) {
+      observe<true>(D, A, nullptr, s_psi, s_phi, s_u + grp.sl * D.M, grp, s_red, red_buf, 0u, n, bl0,
+                    A.expect != nullptr, 1, 0, 0, 1);
+      __syncthreads();
+      run_segments<R, true>(D, A, pd->bseg_begin, pd->bseg_end, s_psi, s_phi, s_cs, 0, s_red, red_buf,
+                            grp, 0u, bl0, A.nb, 0, 0, 1);
+    } else {
+      observe<true>(D, A, nullptr, s_psi, s_phi, nullptr, grp, s_red, red_buf, 0u, n, bl0,
+                    A.expect != nullptr, 0, 0, 0, 1);
+      double2* fin = A.psi_fin + (size_t)bl * N;
+      if (D.M > 1 && valid)
+        for (int l = grp.gi; l < N; l += grp.TPS) fin[l] = s_psi[swz((uint32_t)l)];
+      for (int m = 0; m < D.M; ++m) {
+        if (m > 0) {
+          __syncthreads();
+          if (valid)
+            for (int l = grp.gi; l < N; l += grp.TPS) s_psi[swz((uint32_t)l)] = fin[l];
+        }
+        observe<true>(D, A, nullptr, s_psi, s_phi, nullptr, grp, s_red, red_buf, 0u, n, bl0, false, 2, m,
+                      0, 1);
+        __syncthreads();
+        run_segments<R, true>(D, A, pd->bseg_begin, pd->bseg_end, s_psi, s_phi, s_cs, 0, s_red, red_buf,
+                              grp, 0u, bl0, A.nb, m, 0, 1);
+      }
+    }
+  }
+}
+
+// One pass over HBM-resident states: CTA (tile, row) stages 2^k amplitudes.
+template <int R, bool DUAL>
+__global__ void __launch_bounds__(256) k_pass(DevProgram D, RunArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* smem = reinterpret_cast<double2*>(smem_raw);
+  const PassDesc* pd = D.passes + A.pass;
+  const int k = pd->k, Nt = 1 << k;
+  const uint32_t flags = A.flags;
+  Group grp;
+  grp.tid = threadIdx.x;
+  grp.TPS = blockDim.x;
+  grp.S = 1;
+  grp.gi = threadIdx.x;
+  grp.sl = 0;
+  grp.W = grp.TPS >= 32 ? grp.TPS >> 5 : 1;
+  const int tile = blockIdx.x, n_tiles = gridDim.x;
+  const int64_t bl = blockIdx.y;
+  const int64_t b = A.b0 + bl;
+  const size_t N = (size_t)1 << D.n;
+  uint32_t tile_base = 0;
+  {
+    const uint32_t lm = pd->local_mask;
+    int c = 0;
+    for (int q = 0; q < D.n; ++q)
+      if (!((lm >> q) & 1u)) tile_base |= (((uint32_t)tile >> c++) & 1u) << q;
+  }
+  double2* s_psi = smem;
+  double2* s_phi = smem + Nt;
+  double2* s_cs = smem + (size_t)(DUAL ? 2 : 1) * Nt;
+  const int nrot = pd->rot_end - pd->rot_begin;
+  double* s_red = reinterpret_cast<double*>(s_cs + (nrot > 0 ? nrot : 0));
+  double* s_u = s_red + 2 * A.red_slots * grp.W;
+
+  for (int r = threadIdx.x; r < nrot; r += blockDim.x) s_cs[r] = rot_cs(D, A, b, pd->rot_begin + r);
+  if (DUAL && (flags & F_SEED) && A.bra < 0)
+    for (int m = threadIdx.x; m < D.M; m += blockDim.x) s_u[m] = A.upstream[b * D.M + m];
+  if (flags & F_INIT) {
+    for (int l = threadIdx.x; l < Nt; l += blockDim.x)
+      s_psi[swz((uint32_t)l)] = make_double2((tile_base == 0 && l == 0) ? 1.0 : 0.0, 0.0);
+  } else {
+    const double2* src = ((flags & F_LOAD_FIN) ? A.psi_fin : A.psi) + (size_t)bl * N;
+    for (int l = threadIdx.x; l < Nt; l += blockDim.x)
+      s_psi[swz((uint32_t)l)] = src[tile_base | local_to_global(*pd, (uint32_t)l, k)];
+  }
+  if (DUAL && (flags & F_LOAD_PHI)) {
+    const double2* src = A.phi + (size_t)bl * N;
+    for (int l = threadIdx.x; l < Nt; l += blockDim.x)
+      s_phi[swz((uint32_t)l)] = src[tile_base | local_to_global(*pd, (uint32_t)l, k)];
+  }
+  __syncthreads();
+  int red_buf = 0;
+  if (flags & F_FWD)
+    run_segments<R, false>(D, A, pd->seg_begin, pd->seg_end, s_psi, s_psi, s_cs, pd->rot_begin, s_red,
+                           red_buf, grp, tile_base, bl, A.nb, 0, tile, n_tiles);
+  if (flags & F_STORE_FIN) {
+    double2* dst = A.psi_fin + (size_t)bl * N;
+    for (int l = threadIdx.x; l < Nt; l += blockDim.x)
+      dst[tile_base | local_to_global(*pd, (uint32_t)l, k)] = s_psi[swz((uint32_t)l)];
+  }
+  if (flags & (F_OBSERVE | F_SEED)) {
+    observe<DUAL>(D, A, pd, s_psi, s_phi, s_u, grp, s_red, red_buf, tile_base, k, bl,
+                  (flags & F_OBSERVE) != 0, (flags & F_SEED) ? (A.bra < 0 ? 1 : 2) : 0, A.bra, tile,
+                  n_tiles);
+    __syncthreads();
+  }
+  if constexpr (DUAL) {
+    if (flags & F_BWD)
+      run_segments<R, true>(D, A, pd->bseg_begin, pd->bseg_end, s_psi, s_phi, s_cs, pd->rot_begin, s_red,
+                            red_buf, grp, tile_base, bl, A.nb, A.bra < 0 ? 0 : A.bra, tile, n_tiles);
+  }
+  if (flags & F_STORE_PSI) {
+    double2* dst = A.psi + (size_t)bl * N;
+    for (int l = threadIdx.x; l < Nt; l += blockDim.x)
+      dst[tile_base | local_to_global(*pd, (uint32_t)l, k)] = s_psi[swz((uint32_t)l)];
+  }
+  if (DUAL && (flags & F_STORE_PHI)) {
+    double2* dst = A.phi + (size_t)bl * N;
+    for (int l = threadIdx.x; l < Nt; l += blockDim.x)
+      dst[tile_base | local_to_global(*pd, (uint32_t)l, k)] = s_phi[swz((uint32_t)l)];
+  }
+}
+
+// out[i] = sum_t in[i * n_tiles + t], fixed order (one warp per output)
+__global__ void k_tile_reduce(const double* __restrict__ in, double* __restrict__ out, int64_t count,
+                              int n_tiles) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= count) return;
+  double v = 0.0;
+  for (int t = lane; t < n_tiles; t += 32) v += in[w * n_tiles + t];
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  if (lane == 0) out[w] = v;
+}
+
+// chain rule (_kernels.py:269-278): out[b,k,col] = sum_e ip[b,k,gslot_e] * dangle/dp
+__global__ void k_chain(DevProgram D, RunArgs A, const double* __restrict__ ip, int64_t nb, int K,
+                        const int32_t* __restrict__ col_offs, const ChainEntry* __restrict__ chain,
+                        int ncols, double* __restrict__ out) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= nb * K * ncols) return;
+  const int col = (int)(idx % ncols);
+  const int64_t bk = idx / ncols;
+  const int64_t b = A.b0 + bk / K;
+  double acc = 0.0;
+  for (int e = col_offs[col]; e < col_offs[col + 1]; ++e) {
+    const ChainEntry ce = chain[e];
+    double partial = ce.coeff;
+    for (int u = 0; u < ce.nother; ++u) partial *= flat_val(D, A, b, ce.other[u]);
+    acc += ip[bk * D.NG + ce.gslot] * partial;
+  }
+  out[idx] = acc;
+}
+
+// out[col] = sum_b rows[b, col] in fixed order (model.py:661 einsum over rows)
+__global__ void k_batch_sum(const double* __restrict__ rows, int64_t nb, int ncols,
+                            double* __restrict__ out) {
+  __shared__ double part[8][33];
+  const int col = blockIdx.x * 32 + threadIdx.x;
+  double v = 0.0;
+  if (col < ncols)
+    for (int64_t b = threadIdx.y; b < nb; b += 8) v += rows[b * ncols + col];
+  part[threadIdx.y][threadIdx.x] = v;
+  __syncthreads();
+  if (threadIdx.y == 0 && col < ncols) {
+    double s = 0.0;
+    for (int w = 0; w < 8; ++w) s += part[w][threadIdx.x];
+    out[col] = s;
+  }
+}
+
+using KFn = void (*)(DevProgram, RunArgs);
+
+KFn smem_kernel(int R, bool dual) {
+  switch (R) {
+    case 1: return dual ? k_smem<1, true> : k_smem<1, false>;
+    case 2: return dual ? k_smem<2, true> : k_smem<2, false>;
+    case 3: return dual ? k_smem<3, true> : k_smem<3, false>;
+    default: return dual ? k_smem<4, true> : k_smem<4, false>;
+  }
+}
+KFn pass_kernel(bool dual) { return dual ? k_pass<kMaxR, true> : k_pass<kMaxR, false>; }
+
+}  // namespace vqc
+
+// ------------------------------------------------------------------ host side
+
+using namespace vqc;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int64_t g_launches = 0;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(VQC_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+constexpr int kMaxSmemBytes = 232448;  // 227 KiB opt-in per CTA on sm_100
+
+template <class T>
+cudaError_t upload(const std::vector<T>& v, T** d) {
+  *d = nullptr;
+  if (v.empty()) return cudaSuccess;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(d), v.size() * sizeof(T));
+  if (e != cudaSuccess) return e;
+  return cudaMemcpy(*d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+}
+
+size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+int env_int(const char* name, int dflt) {
+  const char* s = std::getenv(name);
+  return (s && *s) ? std::atoi(s) : dflt;
+}
+
+}  // namespace
+
+struct VqcPlan {
+  int device = 0;
+  int sms = 148;
+  HostProgram prog;
+  int64_t total_params = 0, enc_off = 0, enc_size = 0;
+  int M = 0;
+  std::vector<int32_t> term_offs;
+  std::vector<uint32_t> smask;
+  std::vector<double> tcoeff;
+  // device tables
+  Op* d_ops = nullptr;
+  SegDesc* d_segs = nullptr;
+  int32_t* d_seg_ip = nullptr;
+  PassDesc* d_passes = nullptr;
+  RotDesc* d_rots = nullptr;
+  int32_t* d_term_offs = nullptr;
+  uint32_t* d_smask = nullptr;
+  double* d_tcoeff = nullptr;
+  int32_t* d_col_offs = nullptr;
+  ChainEntry* d_chain = nullptr;
+  DevProgram D{};
+  size_t state_budget = 0;
+  // host-call cache
+  std::mutex mu;
+  cudaStream_t stream = nullptr;
+  void* h_dev = nullptr;
+  size_t h_dev_bytes = 0;
+};
+
+namespace {
+
+struct Layout {
+  size_t ip = 0, rows = 0, psi = 0, phi = 0, fin = 0, ipart = 0, epart = 0, total = 0;
+  int64_t chunk = 0;
+  int n_tiles = 1;
+  int K = 1;
+};
+
+Layout make_layout(const VqcPlan* p, int64_t B, int mode) {
+  Layout L;
+  const HostProgram& P = p->prog;
+  const int64_t N = (int64_t)1 << P.n;
+  const int M = p->M;
+  L.K = mode == VQC_MODE_JACOBIAN ? std::max(M, 1) : 1;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off = align_up(off + bytes);
+    return o;
+  };
+  const bool adj = mode != VQC_MODE_FORWARD;
+  L.ip = take(adj ? (size_t)B * L.K * P.NG * sizeof(double) : 0);
+  L.rows = take(mode == VQC_MODE_VJP ? (size_t)B * P.n_cols * sizeof(double) : 0);
+  if (!P.hbm) {
+    L.chunk = B;
+    L.fin = take(mode == VQC_MODE_JACOBIAN && M > 1 ? (size_t)B * N * 16 : 0);
+  } else {
+    L.n_tiles = 1 << (P.n - P.k);
+    const int nstates = mode == VQC_MODE_FORWARD ? 1 : (mode == VQC_MODE_VJP ? 2 : 3);
+    const size_t per = (size_t)nstates * N * 16 + (size_t)L.K * P.NG * L.n_tiles * 8 +
+                       (size_t)M * L.n_tiles * 8;
+    int64_t chunk = (int64_t)(p->state_budget / std::max<size_t>(per, 1));
+    chunk = std::max<int64_t>(1, std::min<int64_t>(chunk, B));
+    L.chunk = chunk;
+    L.psi = take((size_t)chunk * N * 16);
+    L.phi = take(adj ? (size_t)chunk * N * 16 : 0);
+    L.fin = take(mode == VQC_MODE_JACOBIAN ? (size_t)chunk * N * 16 : 0);
+    L.ipart = take(adj ? (size_t)chunk * L.K * P.NG * L.n_tiles * 8 : 0);
+    L.epart = take((size_t)chunk * M * L.n_tiles * 8);
+  }
+  L.total = off + 256;
+  return L;
+}
+
+int red_slots(const VqcPlan* p) { return std::max(1, std::max(p->M, p->prog.max_ip_per_seg)); }
+
+// samples per CTA in smem mode
+int smem_samples(const VqcPlan* p, int64_t B, bool dual, size_t* smem_bytes) {
+  const HostProgram& P = p->prog;
+  const int TPS = 1 << (P.n - P.R);
+  const int W = TPS >= 32 ? TPS / 32 : 1;
+  auto bytes_for = [&](int S) {
+    return (size_t)S * (dual ? 2 : 1) * ((size_t)16 << P.n) + (size_t)S * P.n_rot * 16 +
+           (size_t)2 * red_slots(p) * S * W * 8 + (size_t)S * p->M * 8;
+  };
+  int smax = std::max(1, 256 / TPS);
+  const int64_t want = std::max<int64_t>(1, (B + 2 * p->sms - 1) / (2 * p->sms));
+  int S = 1;
+  while (S * 2 <= smax && S * 2 <= want && bytes_for(S * 2) <= (size_t)kMaxSmemBytes) S *= 2;
+  *smem_bytes = bytes_for(S);
+  return S;
+}
+
+size_t pass_smem(const VqcPlan* p, bool dual) {
+  const HostProgram& P = p->prog;
+  const int TPS = 1 << (P.k - P.R);
+  const int W = TPS >= 32 ? TPS / 32 : 1;
+  return (size_t)(dual ? 2 : 1) * ((size_t)16 << P.k) + (size_t)P.max_rot_per_pass * 16 +
+         (size_t)2 * red_slots(p) * W * 8 + (size_t)p->M * 8 + 16;
+}
+
+int launch(KFn fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st, const DevProgram& D,
+           const RunArgs& A) {
+  static std::mutex attr_mu;
+  static std::vector<KFn> configured;
+  {
+    std::lock_guard<std::mutex> lk(attr_mu);
+    if (std::find(configured.begin(), configured.end(), fn) == configured.end()) {
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes);
+      configured.push_back(fn);
+    }
+  }
+  if (smem > (size_t)kMaxSmemBytes) return fail(VQC_E_UNSUPPORTED, "shared-memory footprint too large");
+  fn<<<grid, block, smem, st>>>(D, A);
+  ++g_launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  return VQC_OK;
+}
+
+int run_tile_reduce(const double* in, double* out, int64_t count, int n_tiles, cudaStream_t st) {
+  if (count <= 0) return VQC_OK;
+  const int threads = 256;
+  const int64_t blocks = (count * 32 + threads - 1) / threads;
+  k_tile_reduce<<<(unsigned)blocks, threads, 0, st>>>(in, out, count, n_tiles);
+  ++g_launches;
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? VQC_OK : cuda_fail(e, "tile reduce");
+}
+
+// run forward (+ adjoint) for all rows; fills ip (B,K,NG) and d_expect
+int run_core(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, const double* d_up,
+             double* d_expect, int mode, char* ws, const Layout& L, cudaStream_t st) {
+  const HostProgram& P = p->prog;
+  const DevProgram& D = p->D;
+  RunArgs A{};
+  A.inputs = d_in;
+  A.weights = d_w;
+  A.upstream = d_up;
+  A.K = L.K;
+  A.red_slots = red_slots(p);
+  double* ip = reinterpret_cast<double*>(ws + L.ip);
+  const bool adj = mode != VQC_MODE_FORWARD;
+  if (!P.hbm) {
+    size_t smem = 0;
+    const int S = smem_samples(p, B, adj, &smem);
+    A.b0 = 0;
+    A.nb = B;
+    A.S = S;
+    A.bra = -1;
+    A.expect = d_expect;
+    A.ip = ip;
+    A.psi_fin = reinterpret_cast<double2*>(ws + L.fin);
+    A.jacobian = mode == VQC_MODE_JACOBIAN;
+    const int TPS = 1 << (P.n - P.R);
+    const dim3 grid((unsigned)((B + S - 1) / S)), block((unsigned)(S * TPS));
+    return launch(smem_kernel(P.R, adj), grid, block, smem, st, D, A);
+  }
+  // HBM passes, chunked over rows
+  double2* psi = reinterpret_cast<double2*>(ws + L.psi);
+  double2* phi = reinterpret_cast<double2*>(ws + L.phi);
+  double2* fin = reinterpret_cast<double2*>(ws + L.fin);
+  double* ipart = reinterpret_cast<double*>(ws + L.ipart);
+  double* epart = reinterpret_cast<double*>(ws + L.epart);
+  const int TPS = 1 << (P.k - P.R);
+  const int NP = (int)P.passes.size();
+  const size_t sm1 = pass_smem(p, false), sm2 = pass_smem(p, true);
+  for (int64_t b0 = 0; b0 < B; b0 += L.chunk) {
+    const int64_t nb = std::min<int64_t>(L.chunk, B - b0);
+    A.b0 = b0;
+    A.nb = nb;
+    A.S = 1;
+    A.psi = psi;
+    A.phi = phi;
+    A.psi_fin = fin;
+    A.expect = epart;
+    A.ip = ipart;
+    A.bra = -1;
+    const dim3 grid((unsigned)L.n_tiles, (unsigned)nb), block((unsigned)TPS);
+    int rc;
+    for (int pi = 0; pi < NP - 1; ++pi) {
+      A.pass = pi;
+      A.flags = (pi == 0 ? F_INIT : F_LOAD_PSI) | F_FWD | F_STORE_PSI;
+      if ((rc = launch(pass_kernel(false), grid, block, sm1, st, D, A))) return rc;
+    }
+    const uint32_t first = NP == 1 ? F_INIT : F_LOAD_PSI;
+    A.pass = NP - 1;
+    if (mode == VQC_MODE_FORWARD) {
+      A.flags = first | F_FWD | F_OBSERVE;
+      if ((rc = launch(pass_kernel(false), grid, block, sm1, st, D, A))) return rc;
+    } else if (mode == VQC_MODE_VJP) {
+      A.flags = first | F_FWD | F_OBSERVE | F_SEED | F_BWD | (NP > 1 ? (F_STORE_PSI | F_STORE_PHI) : 0);
+      if ((rc = launch(pass_kernel(true), grid, block, sm2, st, D, A))) return rc;
+      for (int pi = NP - 2; pi >= 0; --pi) {
+        A.pass = pi;
+        A.flags = F_LOAD_PSI | F_LOAD_PHI | F_BWD | (pi > 0 ? (F_STORE_PSI | F_STORE_PHI) : 0);
+        if ((rc = launch(pass_kernel(true), grid, block, sm2, st, D, A))) return rc;
+      }
+    } else {
+      A.flags = first | F_FWD | F_OBSERVE | F_STORE_FIN;
+      if ((rc = launch(pass_kernel(false), grid, block, sm1, st, D, A))) return rc;
+      for (int m = 0; m < p->M; ++m) {
+        A.bra = m;
+        A.pass = NP - 1;
+        A.flags = F_LOAD_FIN | F_SEED | F_BWD | (NP > 1 ? (F_STORE_PSI | F_STORE_PHI) : 0);
+        if ((rc = launch(pass_kernel(true), grid, block, sm2, st, D, A))) return rc;
+        for (int pi = NP - 2; pi >= 0; --pi) {
+          A.pass = pi;
+          A.flags = F_LOAD_PSI | F_LOAD_PHI | F_BWD | (pi > 0 ? (F_STORE_PSI | F_STORE_PHI) : 0);
+          if ((rc = launch(pass_kernel(true), grid, block, sm2, st, D, A))) return rc;
+        }
+      }
+    }
+    if (adj && (rc = run_tile_reduce(ipart, ip + (size_t)b0 * L.K * P.NG, nb * L.K * P.NG, L.n_tiles, st)))
+      return rc;
+    if (d_expect && (rc = run_tile_reduce(epart, d_expect + (size_t)b0 * p->M, nb * p->M, L.n_tiles, st)))
+      return rc;
+  }
+  return VQC_OK;
+}
+
+int run_chain(VqcPlan* p, const double* d_in, const double* d_w, const double* ip, int64_t B, int K,
+              double* out, cudaStream_t st) {
+  const HostProgram& P = p->prog;
+  const int64_t total = B * K * P.n_cols;
+  if (total <= 0) return VQC_OK;
+  RunArgs A{};
+  A.inputs = d_in;
+  A.weights = d_w;
+  A.b0 = 0;
+  const int threads = 256;
+  k_chain<<<(unsigned)((total + threads - 1) / threads), threads, 0, st>>>(
+      p->D, A, ip, B, K, p->d_col_offs, p->d_chain, P.n_cols, out);
+  ++g_launches;
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? VQC_OK : cuda_fail(e, "chain rule");
+}
+
+int check_common(const VqcPlan* p, const double* d_in, const double* d_w, int64_t B) {
+  if (!p) return fail(VQC_E_INVALID, "plan is NULL");
+  if (B < 0) return fail(VQC_E_INVALID, "batch size must be >= 0");
+  if (B > 0 && p->enc_size > 0 && !d_in) return fail(VQC_E_INVALID, "inputs pointer is NULL");
+  if (p->total_params > 0 && !d_w) return fail(VQC_E_INVALID, "weights pointer is NULL");
+  if (B > (int64_t)65535 * 65535) return fail(VQC_E_INVALID, "batch too large");
+  return VQC_OK;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ C ABI
+
+extern "C" {
+
+int vqc_abi_version(void) { return VQC_ABI_VERSION; }
+
+const char* vqc_last_error(void) { return g_err.c_str(); }
+
+int64_t vqc_last_launch_count(void) { return g_launches; }
+
+int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_t* wrt_col, int precision,
+                    VqcPlan** out) {
+  g_err.clear();
+  if (!c || !obs || !out) return fail(VQC_E_INVALID, "NULL argument");
+  *out = nullptr;
+  if (precision != 0) return fail(VQC_E_UNSUPPORTED, "only complex128 precision (0) is implemented");
+  if (c->n_qubits < 1 || c->n_qubits > kMaxQubits)
+    return fail(VQC_E_INVALID, "num_qubits must be in [1, 24], got " + std::to_string(c->n_qubits));
+  if (c->n_gates < 0 || c->total_params < 0) return fail(VQC_E_INVALID, "negative sizes");
+  if (c->n_gates > 0 && (!c->kinds || !c->q0 || !c->q1 || !c->coeff || !c->f_offs))
+    return fail(VQC_E_INVALID, "NULL gate table");
+  if (c->enc_offset < 0 || c->enc_size < 0 || c->enc_offset + c->enc_size > c->total_params)
+    return fail(VQC_E_INVALID, "encoding slot out of range");
+  if (obs->n_obs < 0 || (obs->n_obs > 0 && (!obs->term_offs)))
+    return fail(VQC_E_INVALID, "bad observable table");
+  if (c->total_params > 0 && !wrt_col) return fail(VQC_E_INVALID, "wrt_col is NULL");
+
+  std::vector<GateIn> gates((size_t)c->n_gates);
+  for (int64_t g = 0; g < c->n_gates; ++g) {
+    GateIn& gi = gates[g];
+    gi.kind = (int)c->kinds[g];
+    gi.q0 = (int)c->q0[g];
+    gi.q1 = (int)c->q1[g];
+    gi.coeff = c->coeff[g];
+    if (gi.kind >= G_RX && gi.kind <= G_RZ) {
+      const int64_t lo = c->f_offs[g], hi = c->f_offs[g + 1];
+      if (lo < 0 || hi < lo || (hi > lo && !c->f_idx)) return fail(VQC_E_INVALID, "bad f_offs");
+      for (int64_t t = lo; t < hi; ++t) gi.fidx.push_back((int32_t)c->f_idx[t]);
+      if ((int)gi.fidx.size() > kMaxFactors)
+        return fail(VQC_E_UNSUPPORTED, "gate " + std::to_string(g) + ": more than 4 angle factors");
+    }
+  }
+  std::vector<int64_t> wcol((size_t)c->total_params, -1);
+  for (int64_t i = 0; i < c->total_params; ++i) wcol[i] = wrt_col[i];
+
+  VqcPlan* p = new VqcPlan();
+  ScheduleOptions opt;
+  opt.tile_qubits = env_int("VQC_TILE_QUBITS", 11);
+  std::string err = build_program(gates, c->n_qubits, c->total_params, wcol, opt, &p->prog);
+  if (!err.empty()) {
+    delete p;
+    return fail(err.find("out of range") != std::string::npos || err.find("duplicate") != std::string::npos
+                    ? VQC_E_INVALID
+                    : VQC_E_UNSUPPORTED,
+                err);
+  }
+  p->total_params = c->total_params;
+  p->enc_off = c->enc_offset;
+  p->enc_size = c->enc_size;
+  p->M = (int)obs->n_obs;
+  p->term_offs.assign((size_t)p->M + 1, 0);
+  const uint32_t nmask = c->n_qubits >= 32 ? 0xffffffffu : ((1u << c->n_qubits) - 1u);
+  for (int m = 0; m < p->M; ++m) {
+    const int64_t lo = obs->term_offs[m], hi = obs->term_offs[m + 1];
+    if (lo < 0 || hi < lo) { delete p; return fail(VQC_E_INVALID, "bad term_offs"); }
+    for (int64_t t = lo; t < hi; ++t) {
+      if (obs->x_masks[t] != 0) {
+        delete p;
+        return fail(VQC_E_UNSUPPORTED,
+                    "observable " + std::to_string(m) + ": X/Y Pauli strings are not supported on the GPU path "
+                    "(Z strings only)");
+      }
+      if (obs->sign_masks[t] < 0 || ((uint64_t)obs->sign_masks[t] & ~(uint64_t)nmask)) {
+        delete p;
+        return fail(VQC_E_INVALID, "observable sign mask out of range");
+      }
+      const double pr = obs->phases ? obs->phases[2 * t] : 1.0, pim = obs->phases ? obs->phases[2 * t + 1] : 0.0;
+      if (pr != 1.0 || pim != 0.0) { delete p; return fail(VQC_E_UNSUPPORTED, "non-unit phase on a Z string"); }
+      p->smask.push_back((uint32_t)obs->sign_masks[t]);
+      p->tcoeff.push_back(obs->coeffs[t]);
+    }
+    p->term_offs[m + 1] = (int32_t)p->smask.size();
+  }
+  cudaError_t e = cudaGetDevice(&p->device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, p->device);
+  const HostProgram& P = p->prog;
+  if (e == cudaSuccess) e = upload(P.ops, &p->d_ops);
+  if (e == cudaSuccess) e = upload(P.segs, &p->d_segs);
+  if (e == cudaSuccess) e = upload(P.seg_ip, &p->d_seg_ip);
+  if (e == cudaSuccess) e = upload(P.passes, &p->d_passes);
+  if (e == cudaSuccess) e = upload(P.rots, &p->d_rots);
+  if (e == cudaSuccess) e = upload(p->term_offs, &p->d_term_offs);
+  if (e == cudaSuccess) e = upload(p->smask, &p->d_smask);
+  if (e == cudaSuccess) e = upload(p->tcoeff, &p->d_tcoeff);
+  if (e == cudaSuccess) e = upload(P.col_offs, &p->d_col_offs);
+  if (e == cudaSuccess) e = upload(P.chain, &p->d_chain);
+  if (e != cudaSuccess) {
+    vqc_plan_destroy(p);
+    return cuda_fail(e, "plan upload");
+  }
+  DevProgram& D = p->D;
+  D.ops = p->d_ops;
+  D.segs = p->d_segs;
+  D.seg_ip = p->d_seg_ip;
+  D.passes = p->d_passes;
+  D.rots = p->d_rots;
+  D.term_offs = p->d_term_offs;
+  D.t_smask = p->d_smask;
+  D.t_coeff = p->d_tcoeff;
+  D.n = P.n;
+  D.k = P.k;
+  D.R = P.R;
+  D.NG = P.NG;
+  D.n_rot = P.n_rot;
+  D.M = p->M;
+  D.n_pass = (int)P.passes.size();
+  D.enc_off = p->enc_off;
+  D.enc_size = p->enc_size;
+  p->state_budget = (size_t)env_int("VQC_STATE_BUDGET_MB", 16384) << 20;
+  *out = p;
+  return VQC_OK;
+}
+
+void vqc_plan_destroy(VqcPlan* p) {
+  if (!p) return;
+  cudaFree(p->d_ops);
+  cudaFree(p->d_segs);
+  cudaFree(p->d_seg_ip);
+  cudaFree(p->d_passes);
+  cudaFree(p->d_rots);
+  cudaFree(p->d_term_offs);
+  cudaFree(p->d_smask);
+  cudaFree(p->d_tcoeff);
+  cudaFree(p->d_col_offs);
+  cudaFree(p->d_chain);
+  if (p->h_dev) cudaFree(p->h_dev);
+  if (p->stream) cudaStreamDestroy(p->stream);
+  delete p;
+}
+
+int64_t vqc_plan_num_cols(const VqcPlan* p) { return p ? p->prog.n_cols : -1; }
+int64_t vqc_plan_num_obs(const VqcPlan* p) { return p ? p->M : -1; }
+int vqc_plan_mode(const VqcPlan* p) { return p ? (p->prog.hbm ? 1 : 0) : -1; }
+
+int64_t vqc_plan_describe(const VqcPlan* p, char* buf, int64_t cap) {
+  if (!p) return -1;
+  const HostProgram& P = p->prog;
+  int nseg = 0;
+  for (const PassDesc& pd : P.passes) nseg += pd.seg_end - pd.seg_begin;
+  char tmp[512];
+  const int len = snprintf(tmp, sizeof tmp,
+                           "{\"n\": %d, \"mode\": \"%s\", \"tile_qubits\": %d, \"reg_slots\": %d, "
+                           "\"passes\": %d, \"segments\": %d, \"rotations\": %d, \"grad_slots\": %d, "
+                           "\"fwd_ops\": %d, \"bwd_ops\": %d, \"cols\": %d, \"obs\": %d}",
+                           P.n, P.hbm ? "hbm" : "smem", P.k, P.R, (int)P.passes.size(), nseg, P.n_rot,
+                           P.NG, P.n_fwd_ops, P.n_bwd_ops, P.n_cols, p->M);
+  if (buf && cap > 0) {
+    const int64_t c = std::min<int64_t>(cap - 1, len);
+    memcpy(buf, tmp, (size_t)c);
+    buf[c] = 0;
+  }
+  return len;
+}
+
+size_t vqc_workspace_bytes(const VqcPlan* p, int64_t B, int mode) {
+  if (!p || B < 0 || mode < 0 || mode > 2) return 0;
+  return make_layout(p, B, mode).total;
+}
+
+int vqc_forward(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, double* d_expect, void* ws,
+                size_t ws_bytes, void* stream) {
+  g_err.clear();
+  g_launches = 0;
+  int rc = check_common(p, d_in, d_w, B);
+  if (rc) return rc;
+  if (B == 0 || p->M == 0) return VQC_OK;
+  if (!d_expect) return fail(VQC_E_INVALID, "expect pointer is NULL");
+  const Layout L = make_layout(p, B, VQC_MODE_FORWARD);
+  if (ws_bytes < L.total || (!ws && L.total > 0)) return fail(VQC_E_WORKSPACE, "workspace too small");
+  char* w = reinterpret_cast<char*>(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  return run_core(p, d_in, d_w, B, nullptr, d_expect, VQC_MODE_FORWARD, w, L, (cudaStream_t)stream);
+}
+
+int vqc_adjoint(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, const double* d_up,
+                double* d_expect, double* d_jac, double* d_rows, double* d_sum, void* ws, size_t ws_bytes,
+                void* stream) {
+  g_err.clear();
+  g_launches = 0;
+  int rc = check_common(p, d_in, d_w, B);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const HostProgram& P = p->prog;
+  const int mode = d_up ? VQC_MODE_VJP : VQC_MODE_JACOBIAN;
+  if (mode == VQC_MODE_JACOBIAN && !d_jac && P.n_cols > 0 && p->M > 0)
+    return fail(VQC_E_INVALID, "Jacobian mode needs d_jac");
+  // degenerate shapes (batch.py:464-468)
+  if (B == 0) {
+    if (d_sum && P.n_cols > 0) {
+      cudaError_t e = cudaMemsetAsync(d_sum, 0, (size_t)P.n_cols * 8, st);
+      if (e != cudaSuccess) return cuda_fail(e, "memset");
+    }
+    return VQC_OK;
+  }
+  if (p->M == 0 || P.n_cols == 0 || P.NG == 0) {
+    cudaError_t e = cudaSuccess;
+    if (d_jac && P.n_cols > 0 && p->M > 0) e = cudaMemsetAsync(d_jac, 0, (size_t)B * p->M * P.n_cols * 8, st);
+    if (e == cudaSuccess && d_rows && P.n_cols > 0) e = cudaMemsetAsync(d_rows, 0, (size_t)B * P.n_cols * 8, st);
+    if (e == cudaSuccess && d_sum && P.n_cols > 0) e = cudaMemsetAsync(d_sum, 0, (size_t)P.n_cols * 8, st);
+    if (e != cudaSuccess) return cuda_fail(e, "memset");
+    if (p->M == 0 || !d_expect) return VQC_OK;
+    const Layout L = make_layout(p, B, VQC_MODE_FORWARD);
+    if (ws_bytes < L.total || !ws) return fail(VQC_E_WORKSPACE, "workspace too small");
+    char* w = reinterpret_cast<char*>(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+    return run_core(p, d_in, d_w, B, nullptr, d_expect, VQC_MODE_FORWARD, w, L, st);
+  }
+  const Layout L = make_layout(p, B, mode);
+  if (ws_bytes < L.total || !ws) return fail(VQC_E_WORKSPACE, "workspace too small");
+  char* w = reinterpret_cast<char*>(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  if ((rc = run_core(p, d_in, d_w, B, d_up, d_expect, mode, w, L, st))) return rc;
+  const double* ip = reinterpret_cast<const double*>(w + L.ip);
+  if (mode == VQC_MODE_JACOBIAN) return run_chain(p, d_in, d_w, ip, B, L.K, d_jac, st);
+  double* rows = d_rows ? d_rows : reinterpret_cast<double*>(w + L.rows);
+  if ((rc = run_chain(p, d_in, d_w, ip, B, 1, rows, st))) return rc;
+  if (d_sum) {
+    const dim3 block(32, 8), grid((unsigned)((P.n_cols + 31) / 32));
+    k_batch_sum<<<grid, block, 0, st>>>(rows, B, P.n_cols, d_sum);
+    ++g_launches;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "batch sum");
+  }
+  return VQC_OK;
+}
+
+int vqc_run_batch_host(VqcPlan* p, const double* h_in, const double* h_w, int64_t B, const double* h_up,
+                       double* h_expect, double* h_jac, double* h_rows, double* h_sum) {
+  g_err.clear();
+  if (!p) return fail(VQC_E_INVALID, "plan is NULL");
+  std::lock_guard<std::mutex> lk(p->mu);
+  int rc = check_common(p, h_in, h_w, B);
+  if (rc) return rc;
+  cudaError_t e = cudaSetDevice(p->device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  if (!p->stream && (e = cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking)) != cudaSuccess)
+    return cuda_fail(e, "stream");
+  const HostProgram& P = p->prog;
+  const int M = p->M, C = P.n_cols;
+  const bool fwd_only = !h_up && !h_jac;
+  const int mode = fwd_only ? VQC_MODE_FORWARD : (h_up ? VQC_MODE_VJP : VQC_MODE_JACOBIAN);
+  const size_t in_b = (size_t)B * p->enc_size * 8, w_b = (size_t)p->total_params * 8,
+               up_b = h_up ? (size_t)B * M * 8 : 0, ex_b = (size_t)B * M * 8,
+               jac_b = (mode == VQC_MODE_JACOBIAN) ? (size_t)B * M * C * 8 : 0,
+               rows_b = (mode == VQC_MODE_VJP) ? (size_t)B * C * 8 : 0, sum_b = (size_t)C * 8;
+  const size_t ws_b = vqc_workspace_bytes(p, B, mode);
+  size_t off = 0;
+  auto take = [&](size_t b) { const size_t o = off; off = align_up(off + b); return o; };
+  const size_t o_in = take(in_b), o_w = take(w_b), o_up = take(up_b), o_ex = take(ex_b), o_jac = take(jac_b),
+               o_rows = take(rows_b), o_sum = take(sum_b), o_ws = take(ws_b);
+  if (off > p->h_dev_bytes) {
+    if (p->h_dev) cudaFree(p->h_dev);
+    p->h_dev = nullptr;
+    p->h_dev_bytes = 0;
+    if ((e = cudaMalloc(&p->h_dev, off)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    p->h_dev_bytes = off;
+  }
+  char* d = reinterpret_cast<char*>(p->h_dev);
+  cudaStream_t st = p->stream;
+  if (in_b && (e = cudaMemcpyAsync(d + o_in, h_in, in_b, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+    return cuda_fail(e, "H2D inputs");
+  if (w_b && (e = cudaMemcpyAsync(d + o_w, h_w, w_b, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+    return cuda_fail(e, "H2D weights");
+  if (up_b && (e = cudaMemcpyAsync(d + o_up, h_up, up_b, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+    return cuda_fail(e, "H2D upstream");
+  double* dex = reinterpret_cast<double*>(d + o_ex);
+  if (fwd_only) {
+    rc = vqc_forward(p, reinterpret_cast<double*>(d + o_in), reinterpret_cast<double*>(d + o_w), B, dex,
+                     d + o_ws, ws_b, st);
+  } else {
+    rc = vqc_adjoint(p, reinterpret_cast<double*>(d + o_in), reinterpret_cast<double*>(d + o_w), B,
+                     h_up ? reinterpret_cast<double*>(d + o_up) : nullptr, dex,
+                     jac_b ? reinterpret_cast<double*>(d + o_jac) : nullptr,
+                     rows_b ? reinterpret_cast<double*>(d + o_rows) : nullptr,
+                     mode == VQC_MODE_VJP ? reinterpret_cast<double*>(d + o_sum) : nullptr, d + o_ws, ws_b, st);
+  }
+  if (rc) return rc;
+  if (h_expect && ex_b && (e = cudaMemcpyAsync(h_expect, dex, ex_b, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+    return cuda_fail(e, "D2H expect");
+  if (h_jac && jac_b && (e = cudaMemcpyAsync(h_jac, d + o_jac, jac_b, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+    return cuda_fail(e, "D2H jac");
+  if (h_rows && rows_b && (e = cudaMemcpyAsync(h_rows, d + o_rows, rows_b, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+    return cuda_fail(e, "D2H rows");
+  if (h_sum && mode == VQC_MODE_VJP && sum_b &&
+      (e = cudaMemcpyAsync(h_sum, d + o_sum, sum_b, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+    return cuda_fail(e, "D2H sum");
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e, "synchronize");
+  return VQC_OK;
+}
+
+}  // extern "C"

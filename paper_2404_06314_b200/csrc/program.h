@@ -1,0 +1,93 @@
+// Device program format: what the host scheduler (scheduler.cpp) emits and
+// the sm_100a kernels (kernels.cu) interpret.
+//
+// A state of n qubits is processed in PASSES. A pass owns a set of k "local"
+// qubits: one CTA stages a tile of 2^k amplitudes (all other index bits fixed)
+// in shared memory. n <= kSmemMaxQubits runs as a single pass whose tile is the
+// whole state, kept on chip for the entire forward + adjoint sweep. Larger n
+// stream tiles between HBM and shared memory, one kernel launch per pass.
+//
+// Inside a tile, work is split into SEGMENTS: each thread holds 2^R amplitudes
+// in registers (R "register slots" = R local qubits) and applies every gate of
+// the segment to them; a segment boundary is a shared-memory transpose. Gates
+// whose mixing qubit (rotation/H/X target, CNOT target) is a register slot run
+// in registers; diagonal gates (RZ, CZ) and CNOT controls may sit on any qubit
+// (their effect on non-register bits is a per-thread constant).
+#pragma once
+#include <stdint.h>
+
+#ifdef __CUDACC__
+#define VQC_HD __host__ __device__
+#else
+#define VQC_HD
+#endif
+
+namespace vqc {
+
+constexpr int kMaxR = 4;            // register slots per thread
+constexpr int kMaxQubits = 24;      // statevector.py:21
+constexpr int kSmemMaxQubits = 12;  // on-chip (single pass) limit
+constexpr int kMaxFactors = 4;      // factors per angle expression on this path
+
+// gate codes (_kernels.py:16-22, CZ new)
+enum GateKind : int { G_RX = 0, G_RY = 1, G_RZ = 2, G_CNOT = 3, G_H = 4, G_X = 5, G_CZ = 6 };
+
+// op codes of the device program
+enum OpCode : uint32_t {
+  OP_RX = 0, OP_RY = 1, OP_RZ = 2, OP_CNOT = 3, OP_H = 4, OP_X = 5, OP_CZ = 6,
+  OP_IPX = 7, OP_IPY = 8, OP_IPZ = 9,
+};
+
+// operand field (6 bits): bit 5 set -> register slot (low 3 bits), else a
+// global qubit number whose bit is constant per thread.
+constexpr uint32_t kSlotFlag = 32u;
+
+// w0: [0,5) opcode | [5,11) operand a | [11,17) operand b | [17,27) local ip
+//     index | bit 31 adjoint (rotations: negate the angle)
+struct Op {
+  uint32_t w0;
+  uint32_t param;  // rotation id (rotations) or grad slot (IP ops)
+};
+
+VQC_HD inline uint32_t op_code(uint32_t w0) { return w0 & 31u; }
+VQC_HD inline uint32_t op_a(uint32_t w0) { return (w0 >> 5) & 63u; }
+VQC_HD inline uint32_t op_b(uint32_t w0) { return (w0 >> 11) & 63u; }
+VQC_HD inline uint32_t op_ip(uint32_t w0) { return (w0 >> 17) & 1023u; }
+VQC_HD inline bool op_adj(uint32_t w0) { return (w0 >> 31) & 1u; }
+
+struct SegDesc {
+  int32_t op_begin, op_end;
+  int32_t ip_begin, ip_count;  // seg_ip[ip_begin + i] = grad slot of local ip i
+  int8_t nreg, nthr, pad0, pad1;
+  int8_t reg_l[kMaxR];         // tile-local bit position of each register slot
+  int8_t reg_g[kMaxR];         // global qubit of each register slot
+  int8_t thr_l[kMaxQubits];    // tile-local bit position of thread-index bit i
+  int8_t thr_g[kMaxQubits];    // global qubit of thread-index bit i
+};
+
+struct PassDesc {
+  int32_t seg_begin, seg_end;    // forward segments
+  int32_t bseg_begin, bseg_end;  // adjoint segments (executed in order)
+  int32_t rot_begin, rot_end;    // rotation ids used by this pass (contiguous)
+  int32_t k;                     // local qubits (tile = 2^k amplitudes)
+  uint32_t local_mask;           // global qubits local to the tile
+  int8_t local_q[kMaxQubits];    // tile-local position -> global qubit
+};
+
+// angle_r = coeff * prod flat[fidx[0..nf)]   (_kernels.py:128-134)
+struct RotDesc {
+  double coeff;
+  int32_t nf;
+  int32_t fidx[kMaxFactors];
+};
+
+// chain rule (_kernels.py:269-278): column col accumulates
+//   ip[gslot] * coeff * prod_{u} flat[other[u]]
+struct ChainEntry {
+  int32_t gslot;
+  int32_t nother;
+  int32_t other[kMaxFactors - 1];
+  double coeff;
+};
+
+}  // namespace vqc

@@ -1,0 +1,378 @@
+// Circuit -> device program lowering (see program.h for the execution model).
+//
+// The reference applies gates strictly one after another, one full state
+// sweep each (_kernels.py:137-141, 257-281). Here gates are grouped so that a
+// tile/register-resident chunk of the state receives many gates per memory
+// round trip. Gates are only reordered when they commute, using the Pauli
+// structure of the gate set: on a shared qubit, two gates commute iff both act
+// diagonally there (RZ, CZ, CNOT control: "Z"), or both act like X (RX, X,
+// CNOT target), or both like Y (RY). H commutes with nothing. Reordering
+// commuting gates is exact in real arithmetic; in floating point it moves
+// results by ~1e-16 (SURVEY §8c noise floor).
+#include "scheduler.h"
+
+#include <algorithm>
+#include <cstdio>
+
+namespace vqc {
+namespace {
+
+enum Act { A_Z = 0, A_X = 1, A_Y = 2, A_G = 3 };
+
+struct GateInfo {
+  int nq = 1;
+  int q[2] = {0, 0};
+  int act[2] = {0, 0};
+  uint32_t mix = 0;  // qubits that must be local (tile) / a register slot (segment)
+  bool rot = false;
+  bool need_grad = false;
+  std::vector<int> preds;
+};
+
+struct Group {
+  uint32_t mask = 0;
+  std::vector<int> gates;
+};
+
+int popc(uint32_t x) { return __builtin_popcount(x); }
+
+std::string analyze(const std::vector<GateIn>& gates, int n, int64_t total_params,
+                    const std::vector<int64_t>& wrt_col, std::vector<GateInfo>* out) {
+  const int G = (int)gates.size();
+  out->assign(G, GateInfo());
+  struct QubitBlocks {
+    int cur_type = -1;
+    std::vector<int> cur, prev;
+  };
+  std::vector<QubitBlocks> blocks(n);
+  char buf[256];
+  for (int g = 0; g < G; ++g) {
+    const GateIn& gi = gates[g];
+    GateInfo& inf = (*out)[g];
+    auto qcheck = [&](int q) -> bool { return q >= 0 && q < n; };
+    switch (gi.kind) {
+      case G_RX: case G_RY: case G_RZ: case G_H: case G_X:
+        if (!qcheck(gi.q0)) { snprintf(buf, sizeof buf, "gate %d: qubit %d out of range", g, gi.q0); return buf; }
+        inf.nq = 1; inf.q[0] = gi.q0;
+        inf.act[0] = gi.kind == G_RX || gi.kind == G_X ? A_X
+                   : gi.kind == G_RY ? A_Y : gi.kind == G_RZ ? A_Z : A_G;
+        inf.mix = gi.kind == G_RZ ? 0u : (1u << gi.q0);
+        inf.rot = gi.kind <= G_RZ;
+        break;
+      case G_CNOT: case G_CZ:
+        if (!qcheck(gi.q0) || !qcheck(gi.q1)) {
+          snprintf(buf, sizeof buf, "gate %d: qubit out of range", g); return buf;
+        }
+        if (gi.q0 == gi.q1) { snprintf(buf, sizeof buf, "gate %d: duplicate qubit indices", g); return buf; }
+        inf.nq = 2; inf.q[0] = gi.q0; inf.q[1] = gi.q1;
+        inf.act[0] = A_Z; inf.act[1] = gi.kind == G_CNOT ? A_X : A_Z;
+        inf.mix = gi.kind == G_CNOT ? (1u << gi.q1) : 0u;
+        break;
+      default:
+        snprintf(buf, sizeof buf, "gate %d: unknown gate kind %d", g, gi.kind); return buf;
+    }
+    if (inf.rot) {
+      if ((int)gi.fidx.size() > kMaxFactors) {
+        snprintf(buf, sizeof buf, "gate %d: %d angle factors (this path supports <= %d)", g,
+                 (int)gi.fidx.size(), kMaxFactors);
+        return buf;
+      }
+      for (int32_t f : gi.fidx) {
+        if (f < 0 || f >= total_params) { snprintf(buf, sizeof buf, "gate %d: factor index %d out of range", g, f); return buf; }
+        if (wrt_col[f] >= 0) inf.need_grad = true;
+      }
+    }
+    // Per qubit, consecutive gates of one commuting type form a block. A gate
+    // joining the current block depends on every member of the previous
+    // block (a different type); a gate of a new type closes the current
+    // block and depends on all of it. H (A_G) always starts its own block.
+    for (int i = 0; i < inf.nq; ++i) {
+      QubitBlocks& qb = blocks[inf.q[i]];
+      const int t = inf.act[i];
+      if (t == qb.cur_type && t != A_G) {
+        qb.cur.push_back(g);
+      } else {
+        qb.prev.swap(qb.cur);
+        qb.cur.assign(1, g);
+        qb.cur_type = t;
+      }
+      inf.preds.insert(inf.preds.end(), qb.prev.begin(), qb.prev.end());
+    }
+    std::sort(inf.preds.begin(), inf.preds.end());
+    inf.preds.erase(std::unique(inf.preds.begin(), inf.preds.end()), inf.preds.end());
+  }
+  return "";
+}
+
+// Greedy partition of `todo` (a topological order) into groups whose mixing
+// qubits fit `cap` local qubits (always including `forced`). status: 0 pending,
+// 1 done; gates outside `todo` must be marked done.
+std::vector<Group> greedy_groups(const std::vector<int>& todo, const std::vector<GateInfo>& info,
+                                 int cap, uint32_t forced, std::vector<uint8_t>& status) {
+  std::vector<Group> groups;
+  std::vector<int> remaining = todo;
+  while (!remaining.empty()) {
+    Group grp;
+    grp.mask = forced;
+    for (int g : remaining) {
+      bool ok = true;
+      for (int p : info[g].preds)
+        if (status[p] != 1 && status[p] != 2) { ok = false; break; }
+      if (ok) {
+        const uint32_t m = grp.mask | info[g].mix;
+        if (popc(m) <= cap) {
+          grp.mask = m;
+          status[g] = 2;
+          grp.gates.push_back(g);
+        } else {
+          ok = false;
+        }
+      }
+      if (!ok) status[g] = 3;
+    }
+    std::vector<int> next;
+    for (int g : remaining) {
+      if (status[g] == 2) status[g] = 1;
+      else { status[g] = 0; next.push_back(g); }
+    }
+    if (grp.gates.empty()) return {};  // cannot happen when cap >= popc(forced) + 1
+    groups.push_back(std::move(grp));
+    remaining.swap(next);
+  }
+  return groups;
+}
+
+uint32_t enc(uint32_t code, uint32_t a, uint32_t b, uint32_t ipl, bool adj) {
+  return code | (a << 5) | (b << 11) | (ipl << 17) | (adj ? (1u << 31) : 0u);
+}
+
+}  // namespace
+
+std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total_params,
+                          const std::vector<int64_t>& wrt_col, const ScheduleOptions& opt,
+                          HostProgram* P) {
+  if (n < 1 || n > kMaxQubits) return "num_qubits must be in [1, 24]";
+  std::vector<GateInfo> info;
+  std::string err = analyze(gates, n, total_params, wrt_col, &info);
+  if (!err.empty()) return err;
+  const int G = (int)gates.size();
+
+  *P = HostProgram();
+  P->n = n;
+  P->hbm = n > opt.smem_max_qubits;
+  P->k = P->hbm ? std::min(opt.tile_qubits, n) : n;
+  P->R = std::min(opt.reg_slots, P->k);
+  if (P->hbm && P->k < opt.forced_low + 1) return "tile too small";
+  const int k = P->k, R = P->R;
+  const uint32_t all_mask = n == 32 ? 0xffffffffu : ((1u << n) - 1u);
+
+  // ---- level 1: passes (tiles of k local qubits) ----
+  std::vector<uint8_t> status(G, 0);
+  std::vector<int> todo(G);
+  for (int g = 0; g < G; ++g) todo[g] = g;
+  std::vector<Group> passes;
+  if (P->hbm) {
+    const uint32_t forced = (1u << opt.forced_low) - 1u;
+    passes = greedy_groups(todo, info, k, forced, status);
+    if (G > 0 && passes.empty()) return "pass scheduling failed";
+  } else {
+    Group all;
+    all.mask = all_mask;
+    all.gates = todo;
+    passes.push_back(all);
+    for (int g = 0; g < G; ++g) status[g] = 1;
+  }
+  if (passes.empty()) {  // no gates: one empty pass still observes the state
+    Group g0;
+    g0.mask = P->hbm ? ((1u << k) - 1u) : all_mask;
+    passes.push_back(g0);
+  }
+
+  std::vector<int> rot_id(G, -1), gslot(G, -1);
+  int next_rot = 0, next_g = 0;
+
+  for (size_t pi = 0; pi < passes.size(); ++pi) {
+    Group& pg = passes[pi];
+    // pad the local set to exactly k qubits (lowest unused first)
+    for (int q = 0; q < n && popc(pg.mask) < k; ++q) pg.mask |= 1u << q;
+    PassDesc pd{};
+    pd.k = k;
+    pd.local_mask = pg.mask;
+    int pos_of[kMaxQubits];
+    for (int q = 0, p = 0; q < n; ++q) {
+      pos_of[q] = -1;
+      if (pg.mask >> q & 1u) { pd.local_q[p] = (int8_t)q; pos_of[q] = p++; }
+    }
+    pd.rot_begin = next_rot;
+
+    // ---- level 2: register segments inside the tile ----
+    std::vector<uint8_t> st2(G, 1);
+    for (int g : pg.gates) st2[g] = 0;
+    std::vector<Group> segs = greedy_groups(pg.gates, info, R, 0u, st2);
+    if (!pg.gates.empty() && segs.empty()) return "segment scheduling failed";
+
+    pd.seg_begin = (int)P->segs.size();
+    std::vector<SegDesc> fwd_descs;
+    std::vector<std::vector<int>> fwd_gates;
+    for (Group& sgp : segs) {
+      // pad register set to exactly R local qubits
+      for (int q = 0; q < n && popc(sgp.mask) < R; ++q)
+        if ((pg.mask >> q & 1u) && !(sgp.mask >> q & 1u)) sgp.mask |= 1u << q;
+      SegDesc sd{};
+      int slot_of[kMaxQubits];
+      for (int q = 0; q < kMaxQubits; ++q) slot_of[q] = -1;
+      int ns = 0;
+      for (int q = 0; q < n; ++q)
+        if (sgp.mask >> q & 1u) {
+          sd.reg_g[ns] = (int8_t)q;
+          sd.reg_l[ns] = (int8_t)pos_of[q];
+          slot_of[q] = ns++;
+        }
+      sd.nreg = (int8_t)ns;
+      // thread bits: remaining local positions; the first three cover distinct
+      // residues mod 3 so each quarter-warp's 16-byte smem accesses hit 8
+      // distinct bank groups under the mod-3 fold swizzle (kernels.cu swz()).
+      std::vector<int> rest;
+      for (int p = 0; p < k; ++p)
+        if (!(sgp.mask >> pd.local_q[p] & 1u)) rest.push_back(p);
+      std::vector<int> order;
+      for (int r = 0; r < 3; ++r)
+        for (size_t i = 0; i < rest.size(); ++i)
+          if (rest[i] >= 0 && rest[i] % 3 == r) { order.push_back(rest[i]); rest[i] = -1; break; }
+      for (int p : rest)
+        if (p >= 0) order.push_back(p);
+      sd.nthr = (int8_t)order.size();
+      for (size_t i = 0; i < order.size(); ++i) {
+        sd.thr_l[i] = (int8_t)order[i];
+        sd.thr_g[i] = pd.local_q[order[i]];
+      }
+      auto operand = [&](int q) -> uint32_t {
+        return slot_of[q] >= 0 ? (kSlotFlag | (uint32_t)slot_of[q]) : (uint32_t)q;
+      };
+      sd.op_begin = (int)P->ops.size();
+      for (int g : sgp.gates) {
+        const GateIn& gi = gates[g];
+        Op op{};
+        switch (gi.kind) {
+          case G_RX: case G_RY: case G_RZ:
+            rot_id[g] = next_rot++;
+            if (info[g].need_grad) gslot[g] = next_g++;
+            op.w0 = enc(gi.kind, operand(gi.q0), 0, 0, false);
+            op.param = (uint32_t)rot_id[g];
+            break;
+          case G_H: case G_X:
+            op.w0 = enc(gi.kind, operand(gi.q0), 0, 0, false);
+            break;
+          case G_CNOT: case G_CZ:
+            op.w0 = enc(gi.kind, operand(gi.q0), operand(gi.q1), 0, false);
+            break;
+        }
+        if ((info[g].mix & sgp.mask) != info[g].mix) return "internal: mixing qubit not in registers";
+        P->ops.push_back(op);
+      }
+      sd.op_end = (int)P->ops.size();
+      sd.ip_begin = 0;
+      sd.ip_count = 0;
+      P->segs.push_back(sd);
+      fwd_descs.push_back(sd);
+      fwd_gates.push_back(sgp.gates);
+    }
+    pd.seg_end = (int)P->segs.size();
+    pd.rot_end = next_rot;
+    P->max_rot_per_pass = std::max(P->max_rot_per_pass, pd.rot_end - pd.rot_begin);
+
+    // adjoint segments: forward segments reversed, ops reversed, IP before un-apply
+    pd.bseg_begin = (int)P->segs.size();
+    for (int si = (int)fwd_descs.size() - 1; si >= 0; --si) {
+      SegDesc sd = fwd_descs[si];
+      int slot_of[kMaxQubits];
+      for (int q = 0; q < kMaxQubits; ++q) slot_of[q] = -1;
+      for (int s = 0; s < sd.nreg; ++s) slot_of[(int)sd.reg_g[s]] = s;
+      auto operand = [&](int q) -> uint32_t {
+        return slot_of[q] >= 0 ? (kSlotFlag | (uint32_t)slot_of[q]) : (uint32_t)q;
+      };
+      sd.op_begin = (int)P->ops.size();
+      sd.ip_begin = (int)P->seg_ip.size();
+      int nip = 0;
+      const std::vector<int>& gl = fwd_gates[si];
+      for (int gi_ = (int)gl.size() - 1; gi_ >= 0; --gi_) {
+        const int g = gl[gi_];
+        const GateIn& gi = gates[g];
+        if (info[g].rot && info[g].need_grad) {
+          Op ip{};
+          ip.w0 = enc(OP_IPX + gi.kind, operand(gi.q0), 0, (uint32_t)nip, false);
+          ip.param = (uint32_t)gslot[g];
+          P->ops.push_back(ip);
+          P->seg_ip.push_back(gslot[g]);
+          ++nip;
+        }
+        Op op{};
+        if (info[g].rot) {
+          op.w0 = enc(gi.kind, operand(gi.q0), 0, 0, true);
+          op.param = (uint32_t)rot_id[g];
+        } else if (gi.kind == G_H || gi.kind == G_X) {
+          op.w0 = enc(gi.kind, operand(gi.q0), 0, 0, false);
+        } else {
+          op.w0 = enc(gi.kind, operand(gi.q0), operand(gi.q1), 0, false);
+        }
+        P->ops.push_back(op);
+      }
+      if (nip > 1023) return "too many gradient rotations in one segment";
+      sd.op_end = (int)P->ops.size();
+      sd.ip_count = nip;
+      P->max_ip_per_seg = std::max(P->max_ip_per_seg, nip);
+      P->segs.push_back(sd);
+    }
+    pd.bseg_end = (int)P->segs.size();
+    P->passes.push_back(pd);
+  }
+  P->n_rot = next_rot;
+  P->NG = next_g;
+  for (const SegDesc& s : P->segs) (void)s;
+  P->n_fwd_ops = 0;
+  P->n_bwd_ops = 0;
+  for (const PassDesc& pd : P->passes) {
+    for (int s = pd.seg_begin; s < pd.seg_end; ++s) P->n_fwd_ops += P->segs[s].op_end - P->segs[s].op_begin;
+    for (int s = pd.bseg_begin; s < pd.bseg_end; ++s) P->n_bwd_ops += P->segs[s].op_end - P->segs[s].op_begin;
+  }
+
+  // rotation angle descriptors, indexed by rotation id
+  P->rots.assign(P->n_rot, RotDesc{});
+  for (int g = 0; g < G; ++g)
+    if (rot_id[g] >= 0) {
+      RotDesc& rd = P->rots[rot_id[g]];
+      rd.coeff = gates[g].coeff;
+      rd.nf = (int32_t)gates[g].fidx.size();
+      for (int i = 0; i < rd.nf; ++i) rd.fidx[i] = gates[g].fidx[i];
+    }
+
+  // chain rule table (_kernels.py:269-278), reference accumulation order:
+  // gates from last to first, factors in expression order
+  int64_t max_col = -1;
+  for (int64_t c : wrt_col) max_col = std::max(max_col, c);
+  P->n_cols = (int)(max_col + 1);
+  std::vector<std::vector<ChainEntry>> per_col(P->n_cols);
+  for (int g = G - 1; g >= 0; --g) {
+    if (gslot[g] < 0) continue;
+    const std::vector<int32_t>& fx = gates[g].fidx;
+    for (size_t t = 0; t < fx.size(); ++t) {
+      const int64_t col = wrt_col[fx[t]];
+      if (col < 0) continue;
+      ChainEntry ce{};
+      ce.gslot = gslot[g];
+      ce.coeff = gates[g].coeff;
+      ce.nother = 0;
+      for (size_t u = 0; u < fx.size(); ++u)
+        if (u != t) ce.other[ce.nother++] = fx[u];
+      per_col[col].push_back(ce);
+    }
+  }
+  P->col_offs.assign(P->n_cols + 1, 0);
+  for (int c = 0; c < P->n_cols; ++c) {
+    P->col_offs[c + 1] = P->col_offs[c] + (int32_t)per_col[c].size();
+    P->chain.insert(P->chain.end(), per_col[c].begin(), per_col[c].end());
+  }
+  return "";
+}
+
+}  // namespace vqc

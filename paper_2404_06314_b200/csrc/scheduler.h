@@ -1,0 +1,51 @@
+// Host-side lowering of the reference's flat gate list (CompiledCircuit,
+// circuit.py:168-216) into the pass/segment device program of program.h.
+#pragma once
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "program.h"
+
+namespace vqc {
+
+struct GateIn {
+  int kind = 0;
+  int q0 = 0, q1 = 0;
+  double coeff = 1.0;
+  std::vector<int32_t> fidx;  // flat parameter indices (product factors)
+};
+
+struct ScheduleOptions {
+  int tile_qubits = 11;      // k for HBM passes
+  int reg_slots = kMaxR;     // R
+  int forced_low = 3;        // qubits 0..forced_low-1 always local in HBM passes
+  int smem_max_qubits = kSmemMaxQubits;  // n above this streams tiles through HBM
+};
+
+struct HostProgram {
+  int n = 0, k = 0, R = 0;
+  bool hbm = false;
+  int n_rot = 0;   // rotations (angle table entries)
+  int NG = 0;      // grad slots (rotations with a requested factor)
+  int max_ip_per_seg = 0;
+  int max_rot_per_pass = 0;
+  std::vector<PassDesc> passes;
+  std::vector<SegDesc> segs;
+  std::vector<Op> ops;
+  std::vector<int32_t> seg_ip;
+  std::vector<RotDesc> rots;
+  int n_cols = 0;
+  std::vector<int32_t> col_offs;  // n_cols + 1
+  std::vector<ChainEntry> chain;
+  // stats
+  int n_fwd_ops = 0, n_bwd_ops = 0;
+};
+
+// Returns "" on success, else an error message. wrt_col: flat index -> column or -1.
+std::string build_program(const std::vector<GateIn>& gates, int n_qubits, int64_t total_params,
+                          const std::vector<int64_t>& wrt_col, const ScheduleOptions& opt,
+                          HostProgram* out);
+
+}  // namespace vqc

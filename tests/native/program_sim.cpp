@@ -1,0 +1,273 @@
+// TEST INFRASTRUCTURE: semantic CPU interpreter of the device program that
+// scheduler.cpp emits (program.h), used to check the scheduler on CPU.
+//
+// It executes passes / segments / ops exactly in the order the kernels do,
+// resolving register slots to qubits through the segment descriptors, on a
+// full complex128 state — so a wrong reordering, operand encoding, IP
+// placement, gradient-slot map or chain-rule table shows up as a mismatch
+// against the oracle. It also asserts the structural invariants the kernels
+// rely on (tile sizes, slot/thread-bit partitions, mixing operands in
+// registers). It does not model the kernels' tiling arithmetic (swizzle,
+// pdep); the GPU parity tests cover that.
+#include <cmath>
+#include <cstdio>
+#include <complex>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../paper_2404_06314_b200/csrc/scheduler.h"
+
+using namespace vqc;
+using cd = std::complex<double>;
+
+namespace {
+
+struct Sim {
+  int n;
+  std::vector<cd> psi, phi;
+  bool dual = false;
+
+  void rot(std::vector<cd>& s, int kind, int q, double c, double sn) {
+    const size_t step = (size_t)1 << q;
+    for (size_t j = 0; j < s.size(); ++j) {
+      if (j & step) continue;
+      cd a0 = s[j], a1 = s[j | step];
+      if (kind == G_RX) {
+        s[j] = c * a0 - cd(0, sn) * a1;
+        s[j | step] = -cd(0, sn) * a0 + c * a1;
+      } else if (kind == G_RY) {
+        s[j] = c * a0 - sn * a1;
+        s[j | step] = sn * a0 + c * a1;
+      } else {
+        s[j] = cd(c, -sn) * a0;
+        s[j | step] = cd(c, sn) * a1;
+      }
+    }
+  }
+  void fixed(std::vector<cd>& s, int kind, int a, int b) {
+    const size_t ma = (size_t)1 << a, mb = (size_t)1 << b;
+    for (size_t j = 0; j < s.size(); ++j) {
+      if (kind == G_H && !(j & ma)) {
+        cd x = s[j], y = s[j | ma];
+        const double inv = 1.0 / std::sqrt(2.0);
+        s[j] = (x + y) * inv;
+        s[j | ma] = (x - y) * inv;
+      } else if (kind == G_X && !(j & ma)) {
+        std::swap(s[j], s[j | ma]);
+      } else if (kind == G_CNOT && (j & ma) && !(j & mb)) {
+        std::swap(s[j], s[j | mb]);
+      } else if (kind == G_CZ && (j & ma) && (j & mb)) {
+        s[j] = -s[j];
+      }
+    }
+  }
+  double ip(int axis, int q) {
+    const size_t m = (size_t)1 << q;
+    cd acc = 0;
+    for (size_t j = 0; j < psi.size(); ++j) {
+      cd pj;
+      if (axis == 0) pj = psi[j ^ m];
+      else if (axis == 1) pj = (j & m) ? cd(0, 1) * psi[j ^ m] : cd(0, -1) * psi[j ^ m];
+      else pj = (j & m) ? -psi[j] : psi[j];
+      acc += std::conj(phi[j]) * pj;
+    }
+    return acc.imag();
+  }
+};
+
+std::string check_program(const HostProgram& P, const ScheduleOptions& opt) {
+  for (size_t pi = 0; pi < P.passes.size(); ++pi) {
+    const PassDesc& pd = P.passes[pi];
+    if (__builtin_popcount(pd.local_mask) != P.k) return "pass local set size != k";
+    if (P.hbm && (pd.local_mask & ((1u << opt.forced_low) - 1u)) != ((1u << opt.forced_low) - 1u))
+      return "pass misses forced low qubits";
+    for (int p = 0; p < P.k; ++p)
+      if (!((pd.local_mask >> pd.local_q[p]) & 1u) || (p > 0 && pd.local_q[p] <= pd.local_q[p - 1]))
+        return "local_q not the ascending local set";
+    auto check_seg = [&](const SegDesc& sd) -> std::string {
+      if (sd.nreg != P.R || sd.nthr != P.k - P.R) return "segment slot/thread counts";
+      uint32_t seen = 0;
+      for (int s = 0; s < sd.nreg; ++s) {
+        if (pd.local_q[(int)sd.reg_l[s]] != sd.reg_g[s]) return "reg_l/reg_g mismatch";
+        seen |= 1u << sd.reg_g[s];
+      }
+      for (int i = 0; i < sd.nthr; ++i) {
+        if (pd.local_q[(int)sd.thr_l[i]] != sd.thr_g[i]) return "thr_l/thr_g mismatch";
+        if (seen >> sd.thr_g[i] & 1u) return "thread bit overlaps a slot";
+        seen |= 1u << sd.thr_g[i];
+      }
+      if (seen != pd.local_mask) return "slots + thread bits != local set";
+      for (int o = sd.op_begin; o < sd.op_end; ++o) {
+        const Op& op = P.ops[o];
+        const uint32_t code = op_code(op.w0), a = op_a(op.w0), b = op_b(op.w0);
+        auto in_regs = [&](uint32_t x) { return (x & kSlotFlag) && (int)(x & 7u) < sd.nreg; };
+        auto ok_const = [&](uint32_t x) {
+          if (x & kSlotFlag) return (int)(x & 7u) < sd.nreg;
+          if ((int)x >= P.n) return false;
+          for (int s = 0; s < sd.nreg; ++s)
+            if ((uint32_t)sd.reg_g[s] == x) return false;  // register qubits must use slots
+          return true;
+        };
+        switch (code) {
+          case OP_RX: case OP_RY: case OP_H: case OP_X: case OP_IPX: case OP_IPY:
+            if (!in_regs(a)) return "mixing operand not a register slot";
+            break;
+          case OP_RZ: case OP_IPZ:
+            if (!ok_const(a)) return "bad RZ operand";
+            break;
+          case OP_CNOT:
+            if (!in_regs(b)) return "CNOT target not in registers";
+            if (!ok_const(a)) return "bad CNOT control";
+            break;
+          case OP_CZ:
+            if (!ok_const(a) || !ok_const(b)) return "bad CZ operand";
+            break;
+          default:
+            return "unknown opcode";
+        }
+      }
+      return "";
+    };
+    for (int s = pd.seg_begin; s < pd.seg_end; ++s) {
+      std::string e = check_seg(P.segs[s]);
+      if (!e.empty()) return e;
+    }
+    for (int s = pd.bseg_begin; s < pd.bseg_end; ++s) {
+      std::string e = check_seg(P.segs[s]);
+      if (!e.empty()) return e;
+    }
+  }
+  return "";
+}
+
+}  // namespace
+
+extern "C" {
+
+// One row: flat (total_params) with the encoding slice already set.
+// upstream (M) != NULL -> VJP (grad_out: n_cols); else Jacobian (M x n_cols).
+// stats: [passes, segments, rotations, grad_slots].
+int sim_run(int n, int64_t G, const int64_t* kinds, const int64_t* q0, const int64_t* q1,
+            const double* coeff, const int64_t* f_offs, const int64_t* f_idx, int64_t total_params,
+            const int64_t* wrt_col, int tile_qubits, int smem_max_qubits, int M, const int64_t* term_offs,
+            const double* t_coeff, const int64_t* t_smask, const double* flat, const double* upstream,
+            double* expect_out, double* grad_out, int64_t* stats, char* err, int errcap) {
+  std::vector<GateIn> gates((size_t)G);
+  for (int64_t g = 0; g < G; ++g) {
+    gates[g].kind = (int)kinds[g];
+    gates[g].q0 = (int)q0[g];
+    gates[g].q1 = (int)q1[g];
+    gates[g].coeff = coeff[g];
+    if (kinds[g] <= 2)
+      for (int64_t t = f_offs[g]; t < f_offs[g + 1]; ++t) gates[g].fidx.push_back((int32_t)f_idx[t]);
+  }
+  std::vector<int64_t> wc(wrt_col, wrt_col + total_params);
+  ScheduleOptions opt;
+  opt.tile_qubits = tile_qubits;
+  opt.smem_max_qubits = smem_max_qubits;
+  HostProgram P;
+  std::string e = build_program(gates, n, total_params, wc, opt, &P);
+  if (e.empty()) e = check_program(P, opt);
+  if (!e.empty()) {
+    snprintf(err, (size_t)errcap, "%s", e.c_str());
+    return -1;
+  }
+  int nseg = 0;
+  for (const PassDesc& pd : P.passes) nseg += pd.seg_end - pd.seg_begin;
+  stats[0] = (int64_t)P.passes.size();
+  stats[1] = nseg;
+  stats[2] = P.n_rot;
+  stats[3] = P.NG;
+
+  std::vector<double> c(P.n_rot), s(P.n_rot);
+  for (int r = 0; r < P.n_rot; ++r) {
+    double a = P.rots[r].coeff;
+    for (int t = 0; t < P.rots[r].nf; ++t) a *= flat[P.rots[r].fidx[t]];
+    c[r] = std::cos(0.5 * a);
+    s[r] = std::sin(0.5 * a);
+  }
+  Sim S;
+  S.n = n;
+  const size_t N = (size_t)1 << n;
+  S.psi.assign(N, 0);
+  S.psi[0] = 1;
+  auto qubit_of = [](const SegDesc& sd, uint32_t x) -> int {
+    return (x & kSlotFlag) ? sd.reg_g[x & 7u] : (int)x;
+  };
+  auto apply = [&](std::vector<cd>& st, const SegDesc& sd, const Op& op) {
+    const uint32_t code = op_code(op.w0);
+    const int qa = qubit_of(sd, op_a(op.w0)), qb = qubit_of(sd, op_b(op.w0));
+    if (code <= OP_RZ) {
+      const double sn = op_adj(op.w0) ? -s[op.param] : s[op.param];
+      S.rot(st, (int)code, qa, c[op.param], sn);
+    } else {
+      S.fixed(st, (int)code, qa, qb);
+    }
+  };
+  for (const PassDesc& pd : P.passes)
+    for (int sg = pd.seg_begin; sg < pd.seg_end; ++sg) {
+      const SegDesc& sd = P.segs[sg];
+      for (int o = sd.op_begin; o < sd.op_end; ++o) apply(S.psi, sd, P.ops[o]);
+    }
+  auto zw = [&](size_t j, int lo, int hi) {
+    double w = 0;
+    for (int t = lo; t < hi; ++t) w += (__builtin_popcountll(j & (size_t)t_smask[t]) & 1) ? -t_coeff[t] : t_coeff[t];
+    return w;
+  };
+  for (int m = 0; m < M; ++m) {
+    double acc = 0;
+    for (size_t j = 0; j < N; ++j) acc += zw(j, (int)term_offs[m], (int)term_offs[m + 1]) * std::norm(S.psi[j]);
+    expect_out[m] = acc;
+  }
+  const int K = upstream ? 1 : M;
+  const std::vector<cd> psi_fin = S.psi;
+  std::vector<double> ipv((size_t)P.NG);
+  for (int kb = 0; kb < K; ++kb) {
+    S.psi = psi_fin;
+    S.phi.assign(N, 0);
+    for (size_t j = 0; j < N; ++j) {
+      double w = 0;
+      if (upstream) {
+        for (int m = 0; m < M; ++m) w += upstream[m] * zw(j, (int)term_offs[m], (int)term_offs[m + 1]);
+      } else {
+        w = zw(j, (int)term_offs[kb], (int)term_offs[kb + 1]);
+      }
+      S.phi[j] = w * S.psi[j];
+    }
+    std::fill(ipv.begin(), ipv.end(), 0.0);
+    for (int pi = (int)P.passes.size() - 1; pi >= 0; --pi) {
+      const PassDesc& pd = P.passes[pi];
+      for (int sg = pd.bseg_begin; sg < pd.bseg_end; ++sg) {
+        const SegDesc& sd = P.segs[sg];
+        for (int o = sd.op_begin; o < sd.op_end; ++o) {
+          const Op& op = P.ops[o];
+          const uint32_t code = op_code(op.w0);
+          if (code >= OP_IPX) {
+            ipv[op.param] = S.ip((int)(code - OP_IPX), qubit_of(sd, op_a(op.w0)));
+            if (P.seg_ip[sd.ip_begin + op_ip(op.w0)] != (int32_t)op.param) {
+              snprintf(err, (size_t)errcap, "seg_ip table mismatch");
+              return -1;
+            }
+          } else {
+            apply(S.psi, sd, op);
+            apply(S.phi, sd, op);
+          }
+        }
+      }
+    }
+    for (int col = 0; col < P.n_cols; ++col) {
+      double acc = 0;
+      for (int e2 = P.col_offs[col]; e2 < P.col_offs[col + 1]; ++e2) {
+        const ChainEntry& ce = P.chain[e2];
+        double partial = ce.coeff;
+        for (int u = 0; u < ce.nother; ++u) partial *= flat[ce.other[u]];
+        acc += ipv[ce.gslot] * partial;
+      }
+      grad_out[(size_t)kb * P.n_cols + col] = acc;
+    }
+  }
+  return 0;
+}
+
+}  // extern "C"

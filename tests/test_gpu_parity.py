@@ -1,0 +1,267 @@
+"""GPU parity: libvqc.so (through the C ABI) vs the oracle / reference goldens.
+
+Tolerance (BASELINE north star, complex128): |gpu - ref| <= 1e-10 * max(1, |ref|).
+"""
+
+import ast
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, close, oracle_batch
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    from paper_2404_06314_b200 import build
+    build.build()
+    return torch
+
+
+def _engine():
+    from paper_2404_06314_b200 import BatchEngine
+    return BatchEngine()
+
+
+def _request(circ, obs, w, x, wrt):
+    from paper_2404_06314_b200 import BatchRequest
+    return BatchRequest(circ, obs, w, x, wrt=wrt)
+
+
+def _golden(name):
+    path = os.path.join(GOLDEN, name)
+    if not os.path.exists(path):
+        pytest.skip(f"{name} missing")
+    return np.load(path)
+
+
+@pytest.mark.parametrize("cfg_id", [1, 2, 3, 4, 5])
+def test_config_golden_jacobian(torch_cuda, cfg_id):
+    """Per-row expectations and Jacobians on the golden rows (reference run_batch)."""
+    from paper_2404_06314_b200 import configs
+    g = _golden(f"cfg{cfg_id}.npz")
+    spec = configs.CONFIGS[cfg_id]
+    circ, obs, wrt = configs.build(spec, configs.native_api())
+    res = _engine().run_batch(_request(circ, obs, {"w": g["w"]}, g["x_rows"], wrt))
+    assert close(res.expectations, g["expect"]) < TOL
+    assert close(res.gradients["w"], g["jac_w"]) < TOL
+    if "jac_x" in g:
+        assert close(res.gradients["x"], g["jac_x"]) < TOL
+    fwd = _engine().run_batch(_request(circ, obs, {"w": g["w"]}, g["x_rows"], ()))
+    assert close(fwd.expectations, g["expect_fwd"]) < TOL
+
+
+@pytest.mark.parametrize("cfg_id", [1, 2, 3, 4, 5])
+def test_config_golden_vjp(torch_cuda, cfg_id):
+    """VJP mode (upstream = ones) through vqc_adjoint vs the reference einsum."""
+    torch = torch_cuda
+    from paper_2404_06314_b200 import configs
+    g = _golden(f"cfg{cfg_id}.npz")
+    spec = configs.CONFIGS[cfg_id]
+    circ, obs, wrt = configs.build(spec, configs.native_api())
+    eng = _engine()
+    plan, layout = eng.plans.get(circ, obs, wrt, eng.device)
+    x = g["x_rows"]
+    B, M = len(x), len(obs)
+    dev = eng.device
+    flat = eng.base_flat(circ, {"w": g["w"]})
+    d_x = torch.from_numpy(x).to(dev)
+    d_w = torch.from_numpy(flat).to(dev)
+    up = torch.ones((B, M), dtype=torch.float64, device=dev)
+    rows = torch.empty((B, layout.n_cols), dtype=torch.float64, device=dev)
+    vsum = torch.empty((layout.n_cols,), dtype=torch.float64, device=dev)
+    expect = torch.empty((B, M), dtype=torch.float64, device=dev)
+    from paper_2404_06314_b200 import native
+    ws = torch.empty(plan.workspace_bytes(B, native.VQC_MODE_VJP), dtype=torch.uint8, device=dev)
+    plan.adjoint(d_x, d_w, up, expect, None, rows, vsum, ws, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert close(expect.cpu().numpy(), g["expect"]) < TOL
+    name_cols = {n: (lo, hi) for n, lo, hi in layout.slices}
+    lo, hi = name_cols["w"]
+    assert close(vsum.cpu().numpy()[lo:hi], g["vjp_w"]) < TOL
+    if "vjp_x_rows" in g:
+        lo, hi = name_cols["x"]
+        assert close(rows.cpu().numpy()[:, lo:hi], g["vjp_x_rows"]) < TOL
+
+
+def _random_cases():
+    path = os.path.join(GOLDEN, "random.npz")
+    if not os.path.exists(path):
+        return []
+    g = np.load(path)
+    return [i for i in range(int(g["count"])) if not bool(g[f"c{i}_general"])]
+
+
+@pytest.mark.parametrize("idx", _random_cases())
+def test_random_circuits_vs_reference(torch_cuda, idx):
+    """Random circuits over RX RY RZ CNOT H X, shared/product parameters, Z-string sums."""
+    from paper_2404_06314_b200 import ir
+    from paper_2404_06314_b200.observables import Observable
+    g = np.load(os.path.join(GOLDEN, "random.npz"))
+    p = f"c{idx}_"
+    circ = ir.circuit_from_dict(ast.literal_eval(str(g[p + "doc"])))
+    obs = [Observable(t) for t in ast.literal_eval(str(g[p + "obs"]))]
+    trainable = {"theta": g[p + "theta"], "lam": g[p + "lam"]}
+    res = _engine().run_batch(_request(circ, obs, trainable, g[p + "inputs"], ("theta", "lam", "s")))
+    assert close(res.expectations, g[p + "expect"]) < TOL
+    for name in ("theta", "lam", "s"):
+        assert close(res.gradients[name], g[p + "jac_" + name]) < TOL
+
+
+def _rand_circuit(rng, n, n_gates, with_cz=True):
+    from paper_2404_06314_b200.ir import AngleExpression, Circuit, Gate, GateKind, ParameterSet
+    sets = (ParameterSet("s", 4, "encoding"), ParameterSet("a", 5), ParameterSet("b", 3))
+    pool = [(s.name, i) for s in sets for i in range(s.size)]
+    kinds = list(GateKind) if with_cz else [k for k in GateKind if k != GateKind.CZ]
+    gates = []
+    for _ in range(n_gates):
+        kind = kinds[int(rng.integers(len(kinds)))]
+        if kind.num_qubits == 2 and n < 2:
+            kind = GateKind.H
+        if kind.num_qubits == 2:
+            a, b = rng.permutation(n)[:2]
+            gates.append(Gate(kind, (int(a), int(b))))
+        elif kind.is_rotation:
+            refs = []
+            for _ in range(int(rng.integers(0, 4))):
+                r = pool[int(rng.integers(len(pool)))]
+                if r not in refs:
+                    refs.append(r)
+            gates.append(Gate(kind, (int(rng.integers(n)),),
+                              AngleExpression(float(rng.uniform(-2, 2)), tuple(refs))))
+        else:
+            gates.append(Gate(kind, (int(rng.integers(n)),)))
+    circ = Circuit(n, tuple(gates), sets)
+    trainable = {"a": rng.uniform(-2, 2, 5), "b": rng.uniform(-2, 2, 3)}
+    return circ, trainable
+
+
+def _z_obs(rng, n, m):
+    from paper_2404_06314_b200.observables import Observable
+    out = []
+    for _ in range(m):
+        terms = []
+        for _ in range(int(rng.integers(1, 4))):
+            terms.append((float(rng.uniform(-2, 2)),
+                          "".join("Z" if rng.random() < 0.4 else "I" for _ in range(n))))
+        out.append(Observable(tuple(terms)))
+    return out
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 8, 11, 12, 13, 14, 15])
+def test_random_with_cz_vs_oracle(torch_cuda, n):
+    """All gate kinds incl. CZ; n spans the on-chip (<=12) and HBM-pass (>=13) paths."""
+    rng = np.random.default_rng(100 + n)
+    circ, trainable = _rand_circuit(rng, n, 30 + 4 * n)
+    obs = _z_obs(rng, n, 3)
+    x = rng.uniform(-2, 2, (5, 4))
+    wrt = ("a", "b", "s")
+    e_ref, j_ref = oracle_batch(circ, obs, trainable, x, wrt)
+    res = _engine().run_batch(_request(circ, obs, trainable, x, wrt))
+    assert close(res.expectations, e_ref) < TOL
+    for k in wrt:
+        assert close(res.gradients[k], j_ref[k]) < TOL
+
+
+def test_hbm_chunking_is_bitwise_invariant(torch_cuda, monkeypatch):
+    """Row chunking (state budget) must not change any per-row result."""
+    from paper_2404_06314_b200 import configs
+    spec = configs.CONFIGS[4]
+    circ, obs, wrt = configs.build(spec, configs.native_api())
+    x, w = configs.inputs_and_weights(spec, batch=6)
+    a = _engine().run_batch(_request(circ, obs, {"w": w}, x, wrt))
+    monkeypatch.setenv("VQC_STATE_BUDGET_MB", "4")   # forces 1-2 rows per chunk
+    b = _engine().run_batch(_request(circ, obs, {"w": w}, x, wrt))
+    np.testing.assert_array_equal(a.expectations, b.expectations)
+    for k in a.gradients:
+        np.testing.assert_array_equal(a.gradients[k], b.gradients[k])
+
+
+def test_determinism(torch_cuda):
+    from paper_2404_06314_b200 import configs
+    spec = configs.CONFIGS[3]
+    circ, obs, wrt = configs.build(spec, configs.native_api())
+    x, w = configs.inputs_and_weights(spec, batch=300)
+    eng = _engine()
+    a = eng.run_batch(_request(circ, obs, {"w": w}, x, wrt))
+    b = eng.run_batch(_request(circ, obs, {"w": w}, x, wrt))
+    np.testing.assert_array_equal(a.expectations, b.expectations)
+    np.testing.assert_array_equal(a.gradients["w"], b.gradients["w"])
+
+
+def test_degenerate_shapes(torch_cuda):
+    """Empty batch and M = 0 keep their dims (batch.py:464-468)."""
+    from paper_2404_06314_b200 import configs
+    spec = configs.CONFIGS[1]
+    circ, obs, wrt = configs.build(spec, configs.native_api())
+    x, w = configs.inputs_and_weights(spec)
+    eng = _engine()
+    r = eng.run_batch(_request(circ, obs, {"w": w}, x[:0], wrt))
+    assert r.expectations.shape == (0, 1) and r.gradients["w"].shape == (0, 1, 16)
+    r = eng.run_batch(_request(circ, [], {"w": w}, x[:3], wrt))
+    assert r.expectations.shape == (3, 0) and r.gradients["x"].shape == (3, 0, 4)
+
+
+def test_unsupported_observable_raises(torch_cuda):
+    from paper_2404_06314_b200 import configs, parse_observable
+    spec = configs.CONFIGS[1]
+    circ, _, wrt = configs.build(spec, configs.native_api())
+    x, w = configs.inputs_and_weights(spec)
+    with pytest.raises(NotImplementedError, match="Z strings only"):
+        _engine().run_batch(_request(circ, [parse_observable("XZZZ")], {"w": w}, x[:2], wrt))
+
+
+def test_no_gates_circuit(torch_cuda):
+    from paper_2404_06314_b200.ir import Circuit, ParameterSet
+    from paper_2404_06314_b200 import parse_observable
+    for n in (3, 14):
+        circ = Circuit(n, (), (ParameterSet("s", 1, "encoding"), ParameterSet("t", 1)))
+        obs = [parse_observable("Z" + "I" * (n - 1))]
+        res = _engine().run_batch(_request(circ, obs, {"t": np.zeros(1)}, np.zeros((2, 1)), ("t",)))
+        np.testing.assert_array_equal(res.expectations, np.ones((2, 1)))
+        np.testing.assert_array_equal(res.gradients["t"], np.zeros((2, 1, 1)))
+
+
+def test_max_qubits_24(torch_cuda):
+    """Largest register the reference allows (statevector.py:21)."""
+    from paper_2404_06314_b200.ir import AngleExpression, Circuit, Gate, GateKind, ParameterSet
+    from paper_2404_06314_b200.observables import z_observable
+    n = 24
+    gates = [Gate(GateKind.RY, (q,), AngleExpression(1.0, (("s", q % 2),))) for q in range(n)]
+    gates += [Gate(GateKind.CNOT, (q, q + 1)) for q in range(n - 1)]
+    gates += [Gate(GateKind.RX, (q,), AngleExpression(0.5, (("t", q % 3),))) for q in (0, 12, 23)]
+    circ = Circuit(n, tuple(gates), (ParameterSet("s", 2, "encoding"), ParameterSet("t", 3)))
+    obs = [z_observable(n, (0,)), z_observable(n, (23,)), z_observable(n, (5, 17))]
+    x = np.array([[0.3, -1.1]])
+    t = np.array([0.2, 0.9, -0.4])
+    e_ref, j_ref = oracle_batch(circ, obs, {"t": t}, x, ("t", "s"))
+    res = _engine().run_batch(_request(circ, obs, {"t": t}, x, ("t", "s")))
+    assert close(res.expectations, e_ref) < TOL
+    for k in ("t", "s"):
+        assert close(res.gradients[k], j_ref[k]) < TOL
+
+
+def test_host_abi_matches_device_abi(torch_cuda):
+    """vqc_run_batch_host (numpy in/out) == the device-pointer path."""
+    from paper_2404_06314_b200 import configs
+    g = _golden("cfg2.npz")
+    spec = configs.CONFIGS[2]
+    circ, obs, wrt = configs.build(spec, configs.native_api())
+    eng = _engine()
+    plan, layout = eng.plans.get(circ, obs, wrt, eng.device)
+    flat = eng.base_flat(circ, {"w": g["w"]})
+    x = g["x_rows"]
+    e, jac, _, _ = plan.run_batch_host(x, flat, jacobian=True)
+    assert close(e, g["expect"]) < TOL
+    lo, hi = [(a, b) for n, a, b in layout.slices if n == "w"][0]
+    assert close(jac[:, :, lo:hi], g["jac_w"]) < TOL
+    up = np.ones((len(x), len(obs)))
+    e2, _, rows, vsum = plan.run_batch_host(x, flat, upstream=up)
+    assert close(vsum[lo:hi], g["vjp_w"]) < TOL
