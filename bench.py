@@ -1,0 +1,420 @@
+#!/usr/bin/env python
+"""Benchmark: batched statevector forward + adjoint gradients on B200.
+
+Contract (driver): ``python bench.py --gpus N --steps K --warmup W`` prints ONE
+JSON line on rank 0. One step = one forward + adjoint-gradient pass (VJP,
+upstream = ones, the autograd semantics) over the whole batch of the
+headline workload, BASELINE.json config 4 (16 qubits, 10 layers, batch
+16384 sharded over the GPUs, 16 per-qubit <Z_i>, gradients w.r.t. weights and
+inputs), plus the one NCCL all-reduce of the weight gradients for N > 1.
+
+* ``value``: samples/s over the whole job, device-timed with CUDA events on
+  the launching stream (max over ranks), inputs resident in HBM, L2 flushed
+  between timed steps.
+* ``e2e``: the same metric through the host-buffer C ABI call
+  (``vqc_run_batch_host``: H2D inputs, run, D2H results, synchronise).
+* ``roofline``: FP64 bound; algorithmic flops per sample
+  F = 2^n [6R + 6R(1+K) + 4 Rn K] over the state-evolution kernels' measured
+  time; peak = measured DFMA throughput (profiles/peaks_fp64.json).
+* ``cpu_baseline``: the CPU oracle (C restatement of the reference kernels,
+  OpenMP over rows like the reference's thread pool) on a bounded row sample.
+* ``--impl reference``: that CPU path alone, as the reference arm.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "QNN fwd+adjoint-grad samples/sec vs qubits/layers; % of HBM/FP64 roofline"
+HEADLINE_CFG = 4
+FP64_PEAK_FALLBACK = 37.1  # TFLOP/s, tools/probe_peaks.cu on this pool (profiles/peaks_fp64.json)
+
+
+def fp64_peak() -> tuple[float, str]:
+    path = os.path.join(ROOT, "profiles", "peaks_fp64.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["fp64_fma_tflops"]), "measured (tools/probe_peaks.cu DFMA loop, profiles/peaks_fp64.json)"
+    except Exception:
+        return FP64_PEAK_FALLBACK, "measured earlier on this pool (tools/probe_peaks.cu)"
+
+
+def hbm_peak() -> float:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"])
+    except Exception:
+        return 6650.0
+
+
+def workload_desc(spec) -> str:
+    ent = {"cnot_ring": "CNOT ring", "cz_chain": "CZ chain", "cz_all": "CZ all-to-all"}[spec.entangler]
+    obs = {"zzzz": "<Z0Z1Z2Z3>", "per_qubit": f"{spec.n} per-qubit <Z_i>", "sum_z": "sum_i <Z_i>",
+           "z0z1": "<Z0 Z1>"}[spec.observables]
+    wrt = "weights and inputs" if spec.wrt_inputs else "weights"
+    return (f"cfg{spec.cfg_id}: {spec.n} qubits, {spec.layers} layers ({spec.enc} encoding, "
+            f"{'/'.join(spec.trainable)} trainable, {ent}), batch {spec.batch}, {obs}, "
+            f"forward + adjoint VJP grads w.r.t. {wrt}, complex128")
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+        self._t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self._t:
+            self._t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        loaded = [s for s in sm if s > 500] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ----------------------------------------------------------------------------- CPU arms
+
+def cpu_reference_rows(spec, rows: int, threads: int):
+    """Reference semantics on the CPU oracle: run_batch(method='adjoint', wrt)
+    (Jacobian, M+1 reverse sweeps per row; batch.py:478-480) + the backward
+    einsum (model.py:661). Returns wall seconds."""
+    from paper_2404_06314_b200 import configs
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from conftest import oracle_batch
+    circ, obs, wrt = configs.build(spec, configs.native_api())
+    x, w = configs.inputs_and_weights(spec)
+    xs = x[:rows]
+    t0 = time.perf_counter()
+    e, jac = oracle_batch(circ, obs, {"w": w}, xs, wrt, threads=threads)
+    up = np.ones((rows, len(obs)))
+    _ = {k: np.einsum("bm,bmp->p", up, v) for k, v in jac.items()}
+    return time.perf_counter() - t0
+
+
+def cpu_rows_for(spec, threads: int, target_s: float) -> int:
+    """Bounded sample: rows so one timed sample takes about target_s."""
+    t1 = cpu_reference_rows(spec, max(1, threads), threads)  # one row per thread
+    per_round = max(t1, 1e-4)
+    rounds = max(1, int(target_s / per_round))
+    return int(min(spec.batch, rounds * threads))
+
+
+def cpu_baseline(spec, target_s: float = 10.0) -> dict:
+    threads = os.cpu_count() or 1
+    rows = cpu_rows_for(spec, threads, target_s)
+    dt = cpu_reference_rows(spec, rows, threads)
+    return {"value": rows / dt, "unit": "samples/s", "cores": threads, "kind": "port",
+            "sample": f"{rows} of {spec.batch} rows of cfg{spec.cfg_id}, oracle (C port of vqckit "
+                      f"_kernels.py, Jacobian + einsum = reference backward semantics), "
+                      f"{threads} OpenMP threads, {dt:.1f} s"}
+
+
+def run_reference(args, spec):
+    world, rank, _ = dist_setup()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    rows = cpu_rows_for(spec, threads, target_s=args.ref_step_s)
+    for _ in range(args.warmup):
+        cpu_reference_rows(spec, threads, threads)
+    times = [cpu_reference_rows(spec, rows, threads) for _ in range(args.steps)]
+    per_step = statistics.mean(times)
+    value = rows / per_step
+    line = {
+        "metric": METRIC, "value": value, "unit": "samples/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_desc(spec), "batch": spec.batch, "qubits": spec.n,
+                   "layers": spec.layers, "step_sample_rows": rows},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads, "kind": "port",
+                         "sample": f"{rows} rows per step of cfg{spec.cfg_id} (bounded sample; "
+                                   "rows are independent so samples/s extrapolates linearly)"},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+
+class GpuWorkload:
+    def __init__(self, spec, rank: int, world: int, device):
+        import torch
+
+        from paper_2404_06314_b200 import configs, native
+        from paper_2404_06314_b200.engine import BatchEngine, split_workload
+        self.spec = spec
+        self.torch = torch
+        circ, obs, wrt = configs.build(spec, configs.native_api())
+        x, w = configs.inputs_and_weights(spec)
+        lo, hi = split_workload(spec.batch, world)[rank]
+        self.rows = hi - lo
+        self.engine = BatchEngine(device=device)
+        self.plan, self.layout = self.engine.plans.get(circ, obs, wrt, torch.device(device))
+        self.flat = self.engine.base_flat(circ, {"w": w})
+        self.x_host = np.ascontiguousarray(x[lo:hi])
+        self.M = len(obs)
+        dev = torch.device(device)
+        self.dev = dev
+        self.d_x = torch.from_numpy(self.x_host).to(dev)
+        self.d_w = torch.from_numpy(self.flat).to(dev)
+        self.d_up = torch.ones((self.rows, self.M), dtype=torch.float64, device=dev)
+        self.expect = torch.empty((self.rows, self.M), dtype=torch.float64, device=dev)
+        self.vsum = torch.empty((self.layout.n_cols,), dtype=torch.float64, device=dev)
+        self.rows_out = torch.empty((self.rows, self.layout.n_cols), dtype=torch.float64, device=dev)
+        self.ws = torch.empty(self.plan.workspace_bytes(self.rows, native.VQC_MODE_VJP),
+                              dtype=torch.uint8, device=dev)
+        self.native = native
+        self.up_host = np.ones((self.rows, self.M))
+
+    def step(self, world: int):
+        stream = self.torch.cuda.current_stream(self.dev).cuda_stream
+        self.plan.adjoint(self.d_x, self.d_w, self.d_up, self.expect, None, self.rows_out,
+                          self.vsum, self.ws, stream)
+        launches = self.native.last_launch_count()
+        if world > 1:
+            self.torch.distributed.all_reduce(self.vsum)
+        return launches
+
+    def step_host(self, world: int):
+        e, _, rows, vsum = self.plan.run_batch_host(self.x_host, self.flat, upstream=self.up_host)
+        if world > 1:
+            t = self.torch.from_numpy(vsum).to(self.dev)
+            self.torch.distributed.all_reduce(t)
+            vsum = t.cpu().numpy()
+        return e, rows, vsum
+
+    def e2e_bytes(self):
+        h2d = self.x_host.nbytes + self.flat.nbytes + self.up_host.nbytes
+        d2h = self.rows * self.M * 8 + self.rows * self.layout.n_cols * 8 + self.layout.n_cols * 8
+        return h2d, d2h
+
+
+def roofline_from_profile(spec, prof: dict, steps: int, rows_total: int) -> dict:
+    from paper_2404_06314_b200 import configs
+    peak, how = fp64_peak()
+    evo = {k: v for k, v in prof.items() if k.startswith("pass_") or k.startswith("smem_")}
+    evo_ms = sum(v[0] for v in evo.values()) / steps
+    evo_launches = sum(v[1] for v in evo.values()) / steps
+    flops = configs.flops_per_sample(spec, K=1) * rows_total
+    achieved = flops / (evo_ms * 1e-3) / 1e12 if evo_ms > 0 else 0.0
+    total_ms = sum(v[0] for v in prof.values()) / steps
+    out = {
+        "bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+        "frac": achieved / peak, "traffic": None,
+        "kernel": "+".join(sorted(evo)) if evo else None,
+        "kernel_share_of_step": evo_ms / total_ms if total_ms > 0 else None,
+        "launches_per_step": evo_launches,
+        "algorithmic_flops_per_sample": configs.flops_per_sample(spec, K=1),
+        "peak_source": how,
+    }
+    hb = configs.hbm_bytes_per_sample(spec, K=1)
+    if hb > 0 and evo_ms > 0:
+        gbs = hb * rows_total / (evo_ms * 1e-3) / 1e9
+        out["hbm_model"] = {"bytes_per_sample": hb, "achieved_gbs": gbs, "peak_gbs": hbm_peak(),
+                            "frac": gbs / hbm_peak()}
+    return out
+
+
+def measure_gpu(spec, args, rank, world, device, flush_buf, with_e2e: bool, steps: int, warmup: int):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2404_06314_b200 import native
+    wl = GpuWorkload(spec, rank, world, device)
+    for _ in range(warmup):
+        wl.step(world)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(torch.cuda.current_device()).start()
+    native.profile_enable(True)
+    launches = 0
+    for k in range(steps):
+        flush_buf.add_(1)               # L2 flush (256 MiB write), outside the events
+        ev[k][0].record()
+        launches += wl.step(world)
+        ev[k][1].record()
+    torch.cuda.synchronize()
+    prof = native.profile_report()
+    native.profile_enable(False)
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_per_step = float(t.item()) / steps
+    value = spec.batch / (ms_per_step * 1e-3)
+    res = {"value": value, "ms_per_step": ms_per_step, "gpu_launches": launches, "clocks": clk,
+           "kernels": {k: {"ms_per_step": v[0] / steps, "launches_per_step": v[1] / steps}
+                       for k, v in prof.items()},
+           "roofline": roofline_from_profile(spec, prof, steps, wl.rows)}
+    if with_e2e:
+        for _ in range(max(1, warmup)):
+            wl.step_host(world)
+        if world > 1:
+            dist.barrier()
+        times = []
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            wl.step_host(world)
+            times.append(time.perf_counter() - t0)
+        tt = torch.tensor([sum(times)], dtype=torch.float64, device=device)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item()) / steps
+        h2d, d2h = wl.e2e_bytes()
+        res["e2e"] = {"value": spec.batch / e2e_s, "unit": "samples/s", "h2d_bytes_per_step": h2d,
+                      "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
+                      "path": "vqc_run_batch_host (numpy in/out, pageable host buffers)"}
+    res["plan"] = json.loads(wl.plan.describe())
+    del wl
+    torch.cuda.empty_cache()
+    return res
+
+
+def run_ours(args, spec):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2404_06314_b200 import build, configs
+    world, rank, local = dist_setup()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    device = f"cuda:{local if world > 1 else 0}"
+    torch.cuda.set_device(device)
+    build.build()
+    flush = torch.zeros(256 << 20 >> 3, dtype=torch.float64, device=device)
+    res = measure_gpu(spec, args, rank, world, device, flush, True, args.steps, args.warmup)
+    sweep = []
+    if world == 1 and not args.no_sweep:
+        for cid in (1, 2, 3, 5):
+            s = configs.CONFIGS[cid]
+            r = measure_gpu(s, args, rank, world, device, flush, False, 3, 2)
+            sweep.append({"config": workload_desc(s), "value": r["value"], "unit": "samples/s",
+                          "ms_per_step": r["ms_per_step"],
+                          "roofline_frac_fp64": r["roofline"]["frac"],
+                          "achieved_tflops": r["roofline"]["achieved"],
+                          "kernels": r["kernels"], "plan": r["plan"]})
+    line = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            cpu = cpu_baseline(spec, target_s=args.cpu_target_s)
+        line = {
+            "metric": METRIC, "value": res["value"], "unit": "samples/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded: x ~ U(-pi,pi) (B,n), weights ~ U(0,2pi); BASELINE cfg4)",
+            "config": {"workload": workload_desc(spec), "batch": spec.batch, "qubits": spec.n,
+                       "layers": spec.layers, "observables": 16, "mode": "vjp (upstream = ones)",
+                       "parallelism": f"dp{world} (row shards, split_workload; 1 NCCL all-reduce "
+                                      "of the weight grads)" if world > 1 else "dp1",
+                       "l2": "flushed between timed steps (256 MiB write); states stream through "
+                             "a >1 GiB HBM workspace"},
+            "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": res["e2e"],
+            "gpu_launches": res["gpu_launches"], "clocks": res["clocks"], "kernels": res["kernels"],
+            "plan": res["plan"],
+        }
+        if sweep:
+            line["sweep"] = sweep
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", type=int, default=HEADLINE_CFG)
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-target-s", type=float, default=10.0)
+    ap.add_argument("--ref-step-s", type=float, default=4.0)
+    args = ap.parse_args()
+    from paper_2404_06314_b200 import configs
+    spec = configs.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, spec)
+    else:
+        run_ours(args, spec)
+
+
+if __name__ == "__main__":
+    main()

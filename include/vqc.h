@@ -131,6 +131,12 @@ int vqc_run_batch_host(VqcPlan* plan, const double* h_inputs, const double* h_we
 /* Number of kernels the last call on this thread launched (for bench claims). */
 int64_t vqc_last_launch_count(void);
 
+/* Per-kernel CUDA-event timing of this thread's launches (bench/profiling):
+ * enable resets the totals; report synchronises pending events and writes
+ * {"kernel": [total_ms, launches], ...} into buf, returning the JSON length. */
+void vqc_profile_enable(int on);
+int64_t vqc_profile_report(char* buf, int64_t cap);
+
 const char* vqc_last_error(void);
 int vqc_abi_version(void);
 

@@ -291,6 +291,52 @@ namespace {
 thread_local std::string g_err;
 thread_local int64_t g_launches = 0;
 
+// Optional per-kernel CUDA-event timing (vqc_profile_enable / _report): one
+// event pair around each launch on the launching stream.
+struct ProfPending {
+  const char* name;
+  cudaEvent_t e0, e1;
+};
+struct ProfAgg {
+  std::string name;
+  double ms;
+  int64_t count;
+};
+thread_local bool g_prof = false;
+thread_local std::vector<ProfPending> g_prof_pending;
+thread_local std::vector<cudaEvent_t> g_prof_pool;
+thread_local std::vector<ProfAgg> g_prof_agg;
+
+cudaEvent_t prof_event() {
+  if (!g_prof_pool.empty()) {
+    cudaEvent_t e = g_prof_pool.back();
+    g_prof_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct ProfScope {
+  const char* name;
+  cudaStream_t st;
+  cudaEvent_t e0 = nullptr;
+  ProfScope(const char* n, cudaStream_t s) : name(n), st(s) {
+    if (g_prof) {
+      e0 = prof_event();
+      cudaEventRecord(e0, st);
+    }
+  }
+  ~ProfScope() {
+    if (e0) {
+      cudaEvent_t e1 = prof_event();
+      cudaEventRecord(e1, st);
+      g_prof_pending.push_back({name, e0, e1});
+    }
+  }
+};
+
 int fail(int code, const std::string& msg) {
   g_err = msg;
   return code;
@@ -421,8 +467,8 @@ size_t pass_smem(const VqcPlan* p, bool dual) {
          (size_t)2 * red_slots(p) * W * 8 + (size_t)p->M * 8 + 16;
 }
 
-int launch(KFn fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st, const DevProgram& D,
-           const RunArgs& A) {
+int launch(const char* name, KFn fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+           const DevProgram& D, const RunArgs& A) {
   static std::mutex attr_mu;
   static std::vector<KFn> configured;
   {
@@ -433,6 +479,7 @@ int launch(KFn fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st, const De
     }
   }
   if (smem > (size_t)kMaxSmemBytes) return fail(VQC_E_UNSUPPORTED, "shared-memory footprint too large");
+  ProfScope ps(name, st);
   fn<<<grid, block, smem, st>>>(D, A);
   ++g_launches;
   cudaError_t e = cudaGetLastError();
@@ -444,6 +491,7 @@ int run_tile_reduce(const double* in, double* out, int64_t count, int n_tiles, c
   if (count <= 0) return VQC_OK;
   const int threads = 256;
   const int64_t blocks = (count * 32 + threads - 1) / threads;
+  ProfScope ps("tile_reduce", st);
   k_tile_reduce<<<(unsigned)blocks, threads, 0, st>>>(in, out, count, n_tiles);
   ++g_launches;
   cudaError_t e = cudaGetLastError();
@@ -476,7 +524,7 @@ int run_core(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, const
     A.jacobian = mode == VQC_MODE_JACOBIAN;
     const int TPS = 1 << (P.n - P.R);
     const dim3 grid((unsigned)((B + S - 1) / S)), block((unsigned)(S * TPS));
-    return launch(smem_kernel(P.R, adj), grid, block, smem, st, D, A);
+    return launch(adj ? "smem_fwd_adjoint" : "smem_forward", smem_kernel(P.R, adj), grid, block, smem, st, D, A);
   }
   // HBM passes, chunked over rows
   double2* psi = reinterpret_cast<double2*>(ws + L.psi);
@@ -503,33 +551,33 @@ int run_core(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, const
     for (int pi = 0; pi < NP - 1; ++pi) {
       A.pass = pi;
       A.flags = (pi == 0 ? F_INIT : F_LOAD_PSI) | F_FWD | F_STORE_PSI;
-      if ((rc = launch(pass_kernel(false), grid, block, sm1, st, D, A))) return rc;
+      if ((rc = launch("pass_forward", pass_kernel(false), grid, block, sm1, st, D, A))) return rc;
     }
     const uint32_t first = NP == 1 ? F_INIT : F_LOAD_PSI;
     A.pass = NP - 1;
     if (mode == VQC_MODE_FORWARD) {
       A.flags = first | F_FWD | F_OBSERVE;
-      if ((rc = launch(pass_kernel(false), grid, block, sm1, st, D, A))) return rc;
+      if ((rc = launch("pass_forward", pass_kernel(false), grid, block, sm1, st, D, A))) return rc;
     } else if (mode == VQC_MODE_VJP) {
       A.flags = first | F_FWD | F_OBSERVE | F_SEED | F_BWD | (NP > 1 ? (F_STORE_PSI | F_STORE_PHI) : 0);
-      if ((rc = launch(pass_kernel(true), grid, block, sm2, st, D, A))) return rc;
+      if ((rc = launch("pass_adjoint", pass_kernel(true), grid, block, sm2, st, D, A))) return rc;
       for (int pi = NP - 2; pi >= 0; --pi) {
         A.pass = pi;
         A.flags = F_LOAD_PSI | F_LOAD_PHI | F_BWD | (pi > 0 ? (F_STORE_PSI | F_STORE_PHI) : 0);
-        if ((rc = launch(pass_kernel(true), grid, block, sm2, st, D, A))) return rc;
+        if ((rc = launch("pass_adjoint", pass_kernel(true), grid, block, sm2, st, D, A))) return rc;
       }
     } else {
       A.flags = first | F_FWD | F_OBSERVE | F_STORE_FIN;
-      if ((rc = launch(pass_kernel(false), grid, block, sm1, st, D, A))) return rc;
+      if ((rc = launch("pass_forward", pass_kernel(false), grid, block, sm1, st, D, A))) return rc;
       for (int m = 0; m < p->M; ++m) {
         A.bra = m;
         A.pass = NP - 1;
         A.flags = F_LOAD_FIN | F_SEED | F_BWD | (NP > 1 ? (F_STORE_PSI | F_STORE_PHI) : 0);
-        if ((rc = launch(pass_kernel(true), grid, block, sm2, st, D, A))) return rc;
+        if ((rc = launch("pass_adjoint", pass_kernel(true), grid, block, sm2, st, D, A))) return rc;
         for (int pi = NP - 2; pi >= 0; --pi) {
           A.pass = pi;
           A.flags = F_LOAD_PSI | F_LOAD_PHI | F_BWD | (pi > 0 ? (F_STORE_PSI | F_STORE_PHI) : 0);
-          if ((rc = launch(pass_kernel(true), grid, block, sm2, st, D, A))) return rc;
+          if ((rc = launch("pass_adjoint", pass_kernel(true), grid, block, sm2, st, D, A))) return rc;
         }
       }
     }
@@ -551,6 +599,7 @@ int run_chain(VqcPlan* p, const double* d_in, const double* d_w, const double* i
   A.weights = d_w;
   A.b0 = 0;
   const int threads = 256;
+  ProfScope ps("chain_rule", st);
   k_chain<<<(unsigned)((total + threads - 1) / threads), threads, 0, st>>>(
       p->D, A, ip, B, K, p->d_col_offs, p->d_chain, P.n_cols, out);
   ++g_launches;
@@ -578,6 +627,39 @@ int vqc_abi_version(void) { return VQC_ABI_VERSION; }
 const char* vqc_last_error(void) { return g_err.c_str(); }
 
 int64_t vqc_last_launch_count(void) { return g_launches; }
+
+void vqc_profile_enable(int on) {
+  g_prof = on != 0;
+  if (g_prof) g_prof_agg.clear();
+}
+
+int64_t vqc_profile_report(char* buf, int64_t cap) {
+  for (ProfPending& p : g_prof_pending) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(p.e1) == cudaSuccess) cudaEventElapsedTime(&ms, p.e0, p.e1);
+    bool found = false;
+    for (ProfAgg& a : g_prof_agg)
+      if (a.name == p.name) { a.ms += ms; a.count += 1; found = true; break; }
+    if (!found) g_prof_agg.push_back({p.name, (double)ms, 1});
+    g_prof_pool.push_back(p.e0);
+    g_prof_pool.push_back(p.e1);
+  }
+  g_prof_pending.clear();
+  std::string js = "{";
+  for (size_t i = 0; i < g_prof_agg.size(); ++i) {
+    char tmp[160];
+    snprintf(tmp, sizeof tmp, "%s\"%s\": [%.6f, %lld]", i ? ", " : "", g_prof_agg[i].name.c_str(),
+             g_prof_agg[i].ms, (long long)g_prof_agg[i].count);
+    js += tmp;
+  }
+  js += "}";
+  if (buf && cap > 0) {
+    const int64_t c = std::min<int64_t>(cap - 1, (int64_t)js.size());
+    memcpy(buf, js.data(), (size_t)c);
+    buf[c] = 0;
+  }
+  return (int64_t)js.size();
+}
 
 int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_t* wrt_col, int precision,
                     VqcPlan** out) {
@@ -794,6 +876,7 @@ int vqc_adjoint(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, co
   if ((rc = run_chain(p, d_in, d_w, ip, B, 1, rows, st))) return rc;
   if (d_sum) {
     const dim3 block(32, 8), grid((unsigned)((P.n_cols + 31) / 32));
+    ProfScope ps("batch_sum", st);
     k_batch_sum<<<grid, block, 0, st>>>(rows, B, P.n_cols, d_sum);
     ++g_launches;
     cudaError_t e = cudaGetLastError();

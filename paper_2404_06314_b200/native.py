@@ -28,7 +28,8 @@ _ERRORS = {-1: ValueError, -2: NotImplementedError, -3: RuntimeError, -4: Runtim
 EXPORTED_SYMBOLS = (
     "vqc_plan_create", "vqc_plan_destroy", "vqc_plan_num_cols", "vqc_plan_num_obs",
     "vqc_plan_mode", "vqc_plan_describe", "vqc_workspace_bytes", "vqc_forward", "vqc_adjoint",
-    "vqc_run_batch_host", "vqc_last_launch_count", "vqc_last_error", "vqc_abi_version",
+    "vqc_run_batch_host", "vqc_last_launch_count", "vqc_profile_enable", "vqc_profile_report",
+    "vqc_last_error", "vqc_abi_version",
 )
 
 
@@ -83,6 +84,10 @@ def load_library(path: str | None = None):
                                            _F64P, _F64P]
         lib.vqc_last_launch_count.restype = ctypes.c_int64
         lib.vqc_last_launch_count.argtypes = []
+        lib.vqc_profile_enable.restype = None
+        lib.vqc_profile_enable.argtypes = [ctypes.c_int]
+        lib.vqc_profile_report.restype = ctypes.c_int64
+        lib.vqc_profile_report.argtypes = [ctypes.c_char_p, ctypes.c_int64]
         lib.vqc_last_error.restype = ctypes.c_char_p
         lib.vqc_last_error.argtypes = []
         lib.vqc_abi_version.restype = ctypes.c_int
@@ -205,3 +210,18 @@ class Plan:
 
 def last_launch_count() -> int:
     return int(load_library().vqc_last_launch_count())
+
+
+def profile_enable(on: bool = True) -> None:
+    """Per-kernel CUDA-event timing of this thread's launches (resets totals)."""
+    load_library().vqc_profile_enable(1 if on else 0)
+
+
+def profile_report() -> dict:
+    """{kernel: (total_ms, launches)} for launches since profile_enable."""
+    import json
+    lib = load_library()
+    n = int(lib.vqc_profile_report(None, 0))
+    buf = ctypes.create_string_buffer(n + 1)
+    lib.vqc_profile_report(buf, n + 1)
+    return {k: (float(v[0]), int(v[1])) for k, v in json.loads(buf.value.decode()).items()}
