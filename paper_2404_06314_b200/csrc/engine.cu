@@ -28,14 +28,14 @@ __device__ void observe(const DevProgram& D, const RunArgs& A, const PassDesc* p
   if (do_expect) {
     const int red_stride = A.red_slots * grp.S * grp.W;
     double* redbuf = s_red + red_buf * red_stride;
+    const TileWalk tw = tile_walk(pd, tile_base, k, grp.gi, grp.TPS);
     for (int m = 0; m < D.M; ++m) {
       const int lo = D.term_offs[m], hi = D.term_offs[m + 1];
       double acc = 0.0;
-      for (int l = grp.gi; l < Nt; l += grp.TPS) {
-        const uint32_t j = tile_base | (pd ? local_to_global(*pd, (uint32_t)l, k) : (uint32_t)l);
-        const double2 x = s_psi[swz((uint32_t)l)];
+      for_tile(tw, grp.gi, grp.TPS, [&](uint32_t l, uint32_t j) {
+        const double2 x = s_psi[swz(l)];
         acc += zweight(D, j, lo, hi) * (x.x * x.x + x.y * x.y);
-      }
+      });
       acc = grp.reduce(acc);
       if (grp.leader()) redbuf[grp.red_index(m)] = acc;
     }
@@ -52,8 +52,8 @@ __device__ void observe(const DevProgram& D, const RunArgs& A, const PassDesc* p
   }
   if constexpr (DUAL) {
     if (seed_mode != 0) {
-      for (int l = grp.gi; l < Nt; l += grp.TPS) {
-        const uint32_t j = tile_base | (pd ? local_to_global(*pd, (uint32_t)l, k) : (uint32_t)l);
+      const TileWalk tw = tile_walk(pd, tile_base, k, grp.gi, grp.TPS);
+      for_tile(tw, grp.gi, grp.TPS, [&](uint32_t l, uint32_t j) {
         double w = 0.0;
         if (seed_mode == 1) {
           for (int m = 0; m < D.M; ++m) {
@@ -63,20 +63,36 @@ __device__ void observe(const DevProgram& D, const RunArgs& A, const PassDesc* p
         } else {
           w = zweight(D, j, D.term_offs[bra], D.term_offs[bra + 1]);
         }
-        const uint32_t p = swz((uint32_t)l);
+        const uint32_t p = swz(l);
         const double2 x = s_psi[p];
         s_phi[p] = make_double2(w * x.x, w * x.y);
-      }
+      });
     }
   }
 }
 
+// Shared-memory carve-up (kernels and host sizing must agree).
+struct SmemLayout {
+  size_t psi, phi, cs, u, av, red, up, total;  // byte offsets
+  __host__ __device__ SmemLayout(int S, int n_amp, bool dual, int nrot, int nblk, int nav, int red_slots,
+                                 int W, int M) {
+    size_t o = 0;
+    psi = o; o += (size_t)S * n_amp * 16;
+    phi = o; o += dual ? (size_t)S * n_amp * 16 : 0;
+    cs = o; o += (size_t)S * nrot * 16;
+    u = o; o += (size_t)S * nblk * 64;
+    av = o; o += (size_t)S * nav * 32;
+    red = o; o += (size_t)2 * red_slots * S * W * 8;
+    up = o; o += (size_t)S * M * 8;
+    total = o + 16;
+  }
+};
+
 // Whole state on chip: one CTA owns S samples of n <= 12 qubits and runs
 // forward, expectations, seed and the adjoint sweep without touching HBM.
 template <int R, bool DUAL>
-__global__ void __launch_bounds__(256) k_smem(DevProgram D, RunArgs A) {
+__global__ void __launch_bounds__(R >= 4 ? 256 : 512) k_smem(DevProgram D, RunArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* smem = reinterpret_cast<double2*>(smem_raw);
   const int n = D.n, N = 1 << n;
   Group grp;
   grp.tid = threadIdx.x;
@@ -89,33 +105,35 @@ __global__ void __launch_bounds__(256) k_smem(DevProgram D, RunArgs A) {
   const int64_t bl = bl0 + grp.sl;
   const bool valid = bl < A.nb;
   const int64_t b = A.b0 + (valid ? bl : 0);
-  double2* s_psi = smem + (size_t)grp.sl * N;
-  double2* s_phi = smem + (size_t)(A.S + grp.sl) * N;
-  double2* s_cs_all = smem + (size_t)(DUAL ? 2 : 1) * A.S * N;
-  double2* s_cs = s_cs_all + (size_t)grp.sl * D.n_rot;
-  double* s_red = reinterpret_cast<double*>(s_cs_all + (size_t)A.S * D.n_rot);
-  double* s_u = s_red + 2 * A.red_slots * A.S * grp.W;
+  const PassDesc* pd = D.passes;
+  const int nrot = D.n_rot, nblk = D.n_blk, nav = D.n_av;
+  const SmemLayout L(A.S, N, DUAL, nrot, nblk, nav, A.red_slots, grp.W, D.M);
+  double2* s_psi = reinterpret_cast<double2*>(smem_raw + L.psi) + (size_t)grp.sl * N;
+  double2* s_phi = reinterpret_cast<double2*>(smem_raw + L.phi) + (size_t)grp.sl * N;
+  double2* s_cs = reinterpret_cast<double2*>(smem_raw + L.cs) + (size_t)grp.sl * nrot;
+  double2* s_u = reinterpret_cast<double2*>(smem_raw + L.u) + (size_t)grp.sl * nblk * 4;
+  double* s_av_all = reinterpret_cast<double*>(smem_raw + L.av);
+  double* s_red = reinterpret_cast<double*>(smem_raw + L.red);
+  double* s_up = reinterpret_cast<double*>(smem_raw + L.up);
 
-  for (int r = grp.gi; r < D.n_rot; r += grp.TPS)
-    s_cs[r] = valid ? rot_cs(D, A, b, r) : make_double2(1.0, 0.0);
   for (int l = grp.gi; l < N; l += grp.TPS) s_psi[swz((uint32_t)l)] = make_double2(l == 0 ? 1.0 : 0.0, 0.0);
   if (DUAL && A.upstream != nullptr)
-    for (int m = grp.gi; m < D.M; m += grp.TPS) s_u[grp.sl * D.M + m] = valid ? A.upstream[b * D.M + m] : 0.0;
-  __syncthreads();
+    for (int m = grp.gi; m < D.M; m += grp.TPS) s_up[grp.sl * D.M + m] = valid ? A.upstream[b * D.M + m] : 0.0;
+  build_tables(D, A, pd, b, valid, s_cs, s_u, s_av_all + (size_t)grp.sl * nav * 4, grp.gi, grp.TPS);
+  const SampleTables T{s_cs, s_u, 0, 0};
 
   int red_buf = 0;
-  const PassDesc* pd = D.passes;
-  run_segments<R, false>(D, A, pd->seg_begin, pd->seg_end, s_psi, s_psi, s_cs, 0, s_red, red_buf, grp,
-                         0u, bl0, A.nb, 0, 0, 1);
+  run_segments<R, false>(D, A, pd->seg_begin, pd->seg_end, s_psi, s_psi, T, s_av_all, nav * 4, 0, s_red,
+                         red_buf, grp, 0u, bl0, 0, 0, 1);
   if constexpr (!DUAL) {
     observe<false>(D, A, nullptr, s_psi, s_psi, nullptr, grp, s_red, red_buf, 0u, n, bl0, true, 0, 0, 0, 1);
   } else {
     if (!A.jacobian) {
-      observe<true>(D, A, nullptr, s_psi, s_phi, s_u + grp.sl * D.M, grp, s_red, red_buf, 0u, n, bl0,
+      observe<true>(D, A, nullptr, s_psi, s_phi, s_up + grp.sl * D.M, grp, s_red, red_buf, 0u, n, bl0,
                     A.expect != nullptr, 1, 0, 0, 1);
       __syncthreads();
-      run_segments<R, true>(D, A, pd->bseg_begin, pd->bseg_end, s_psi, s_phi, s_cs, 0, s_red, red_buf,
-                            grp, 0u, bl0, A.nb, 0, 0, 1);
+      run_segments<R, true>(D, A, pd->bseg_begin, pd->bseg_end, s_psi, s_phi, T, s_av_all, nav * 4, 0, s_red,
+                            red_buf, grp, 0u, bl0, 0, 0, 1);
     } else {
       observe<true>(D, A, nullptr, s_psi, s_phi, nullptr, grp, s_red, red_buf, 0u, n, bl0,
                     A.expect != nullptr, 0, 0, 0, 1);
@@ -131,8 +149,8 @@ __global__ void __launch_bounds__(256) k_smem(DevProgram D, RunArgs A) {
         observe<true>(D, A, nullptr, s_psi, s_phi, nullptr, grp, s_red, red_buf, 0u, n, bl0, false, 2, m,
                       0, 1);
         __syncthreads();
-        run_segments<R, true>(D, A, pd->bseg_begin, pd->bseg_end, s_psi, s_phi, s_cs, 0, s_red, red_buf,
-                              grp, 0u, bl0, A.nb, m, 0, 1);
+        run_segments<R, true>(D, A, pd->bseg_begin, pd->bseg_end, s_psi, s_phi, T, s_av_all, nav * 4, 0,
+                              s_red, red_buf, grp, 0u, bl0, m, 0, 1);
       }
     }
   }
@@ -140,9 +158,8 @@ __global__ void __launch_bounds__(256) k_smem(DevProgram D, RunArgs A) {
 
 // One pass over HBM-resident states: CTA (tile, row) stages 2^k amplitudes.
 template <int R, bool DUAL>
-__global__ void __launch_bounds__(256) k_pass(DevProgram D, RunArgs A) {
+__global__ void __launch_bounds__(R >= 4 ? 256 : 512) k_pass(DevProgram D, RunArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* smem = reinterpret_cast<double2*>(smem_raw);
   const PassDesc* pd = D.passes + A.pass;
   const int k = pd->k, Nt = 1 << k;
   const uint32_t flags = A.flags;
@@ -164,59 +181,60 @@ __global__ void __launch_bounds__(256) k_pass(DevProgram D, RunArgs A) {
     for (int q = 0; q < D.n; ++q)
       if (!((lm >> q) & 1u)) tile_base |= (((uint32_t)tile >> c++) & 1u) << q;
   }
-  double2* s_psi = smem;
-  double2* s_phi = smem + Nt;
-  double2* s_cs = smem + (size_t)(DUAL ? 2 : 1) * Nt;
-  const int nrot = pd->rot_end - pd->rot_begin;
-  double* s_red = reinterpret_cast<double*>(s_cs + (nrot > 0 ? nrot : 0));
-  double* s_u = s_red + 2 * A.red_slots * grp.W;
+  const SmemLayout L(1, Nt, DUAL, D.max_rot_pass, D.max_blk_pass, D.max_av_pass, A.red_slots, grp.W, D.M);
+  double2* s_psi = reinterpret_cast<double2*>(smem_raw + L.psi);
+  double2* s_phi = reinterpret_cast<double2*>(smem_raw + L.phi);
+  double2* s_cs = reinterpret_cast<double2*>(smem_raw + L.cs);
+  double2* s_u = reinterpret_cast<double2*>(smem_raw + L.u);
+  double* s_av = reinterpret_cast<double*>(smem_raw + L.av);
+  double* s_red = reinterpret_cast<double*>(smem_raw + L.red);
+  double* s_up = reinterpret_cast<double*>(smem_raw + L.up);
 
-  for (int r = threadIdx.x; r < nrot; r += blockDim.x) s_cs[r] = rot_cs(D, A, b, pd->rot_begin + r);
   if (DUAL && (flags & F_SEED) && A.bra < 0)
-    for (int m = threadIdx.x; m < D.M; m += blockDim.x) s_u[m] = A.upstream[b * D.M + m];
+    for (int m = threadIdx.x; m < D.M; m += blockDim.x) s_up[m] = A.upstream[b * D.M + m];
+  const TileWalk tw = tile_walk(pd, tile_base, k, threadIdx.x, blockDim.x);
   if (flags & F_INIT) {
     for (int l = threadIdx.x; l < Nt; l += blockDim.x)
       s_psi[swz((uint32_t)l)] = make_double2((tile_base == 0 && l == 0) ? 1.0 : 0.0, 0.0);
   } else {
     const double2* src = ((flags & F_LOAD_FIN) ? A.psi_fin : A.psi) + (size_t)bl * N;
-    for (int l = threadIdx.x; l < Nt; l += blockDim.x)
-      s_psi[swz((uint32_t)l)] = src[tile_base | local_to_global(*pd, (uint32_t)l, k)];
+    const double2* srcf = A.phi + (size_t)bl * N;
+    const bool lphi = DUAL && (flags & F_LOAD_PHI);
+    for_tile(tw, threadIdx.x, blockDim.x, [&](uint32_t l, uint32_t j) {
+      s_psi[swz(l)] = src[j];
+      if (lphi) s_phi[swz(l)] = srcf[j];
+    });
   }
-  if (DUAL && (flags & F_LOAD_PHI)) {
-    const double2* src = A.phi + (size_t)bl * N;
-    for (int l = threadIdx.x; l < Nt; l += blockDim.x)
-      s_phi[swz((uint32_t)l)] = src[tile_base | local_to_global(*pd, (uint32_t)l, k)];
-  }
-  __syncthreads();
+  build_tables(D, A, pd, b, true, s_cs, s_u, s_av, threadIdx.x, blockDim.x);
+  const SampleTables T{s_cs, s_u, pd->rot_begin, pd->blk_begin};
   int red_buf = 0;
   if (flags & F_FWD)
-    run_segments<R, false>(D, A, pd->seg_begin, pd->seg_end, s_psi, s_psi, s_cs, pd->rot_begin, s_red,
-                           red_buf, grp, tile_base, bl, A.nb, 0, tile, n_tiles);
+    run_segments<R, false>(D, A, pd->seg_begin, pd->seg_end, s_psi, s_psi, T, s_av, 0, pd->av_begin, s_red,
+                           red_buf, grp, tile_base, bl, 0, tile, n_tiles);
   if (flags & F_STORE_FIN) {
     double2* dst = A.psi_fin + (size_t)bl * N;
-    for (int l = threadIdx.x; l < Nt; l += blockDim.x)
-      dst[tile_base | local_to_global(*pd, (uint32_t)l, k)] = s_psi[swz((uint32_t)l)];
+    for_tile(tw, threadIdx.x, blockDim.x, [&](uint32_t l, uint32_t j) { dst[j] = s_psi[swz(l)]; });
   }
   if (flags & (F_OBSERVE | F_SEED)) {
-    observe<DUAL>(D, A, pd, s_psi, s_phi, s_u, grp, s_red, red_buf, tile_base, k, bl,
+    observe<DUAL>(D, A, pd, s_psi, s_phi, s_up, grp, s_red, red_buf, tile_base, k, bl,
                   (flags & F_OBSERVE) != 0, (flags & F_SEED) ? (A.bra < 0 ? 1 : 2) : 0, A.bra, tile,
                   n_tiles);
     __syncthreads();
   }
   if constexpr (DUAL) {
     if (flags & F_BWD)
-      run_segments<R, true>(D, A, pd->bseg_begin, pd->bseg_end, s_psi, s_phi, s_cs, pd->rot_begin, s_red,
-                            red_buf, grp, tile_base, bl, A.nb, A.bra < 0 ? 0 : A.bra, tile, n_tiles);
+      run_segments<R, true>(D, A, pd->bseg_begin, pd->bseg_end, s_psi, s_phi, T, s_av, 0, pd->av_begin,
+                            s_red, red_buf, grp, tile_base, bl, A.bra < 0 ? 0 : A.bra, tile, n_tiles);
   }
-  if (flags & F_STORE_PSI) {
+  const bool sphi = DUAL && (flags & F_STORE_PHI);
+  if ((flags & F_STORE_PSI) || sphi) {
     double2* dst = A.psi + (size_t)bl * N;
-    for (int l = threadIdx.x; l < Nt; l += blockDim.x)
-      dst[tile_base | local_to_global(*pd, (uint32_t)l, k)] = s_psi[swz((uint32_t)l)];
-  }
-  if (DUAL && (flags & F_STORE_PHI)) {
-    double2* dst = A.phi + (size_t)bl * N;
-    for (int l = threadIdx.x; l < Nt; l += blockDim.x)
-      dst[tile_base | local_to_global(*pd, (uint32_t)l, k)] = s_phi[swz((uint32_t)l)];
+    double2* dstf = A.phi + (size_t)bl * N;
+    const bool spsi = (flags & F_STORE_PSI) != 0;
+    for_tile(tw, threadIdx.x, blockDim.x, [&](uint32_t l, uint32_t j) {
+      if (spsi) dst[j] = s_psi[swz(l)];
+      if (sphi) dstf[j] = s_phi[swz(l)];
+    });
   }
 }
 
@@ -278,7 +296,10 @@ KFn smem_kernel(int R, bool dual) {
     default: return dual ? k_smem<4, true> : k_smem<4, false>;
   }
 }
-KFn pass_kernel(bool dual) { return dual ? k_pass<kMaxR, true> : k_pass<kMaxR, false>; }
+KFn pass_kernel(int R, bool dual) {
+  if (R >= 4) return dual ? k_pass<4, true> : k_pass<4, false>;
+  return dual ? k_pass<3, true> : k_pass<3, false>;
+}
 
 }  // namespace vqc
 
@@ -378,7 +399,10 @@ struct VqcPlan {
   // device tables
   Op* d_ops = nullptr;
   SegDesc* d_segs = nullptr;
-  int32_t* d_seg_ip = nullptr;
+  IpOut* d_ipouts = nullptr;
+  BlockDesc* d_blocks = nullptr;
+  MemberDesc* d_members = nullptr;
+  DiagRun* d_diag = nullptr;
   PassDesc* d_passes = nullptr;
   RotDesc* d_rots = nullptr;
   int32_t* d_term_offs = nullptr;
@@ -440,7 +464,7 @@ Layout make_layout(const VqcPlan* p, int64_t B, int mode) {
   return L;
 }
 
-int red_slots(const VqcPlan* p) { return std::max(1, std::max(p->M, p->prog.max_ip_per_seg)); }
+int red_slots(const VqcPlan* p) { return std::max(1, std::max(p->M, p->prog.max_red_per_seg)); }
 
 // samples per CTA in smem mode
 int smem_samples(const VqcPlan* p, int64_t B, bool dual, size_t* smem_bytes) {
@@ -448,10 +472,9 @@ int smem_samples(const VqcPlan* p, int64_t B, bool dual, size_t* smem_bytes) {
   const int TPS = 1 << (P.n - P.R);
   const int W = TPS >= 32 ? TPS / 32 : 1;
   auto bytes_for = [&](int S) {
-    return (size_t)S * (dual ? 2 : 1) * ((size_t)16 << P.n) + (size_t)S * P.n_rot * 16 +
-           (size_t)2 * red_slots(p) * S * W * 8 + (size_t)S * p->M * 8;
+    return SmemLayout(S, 1 << P.n, dual, P.n_rot, P.n_blk, P.n_av, red_slots(p), W, p->M).total;
   };
-  int smax = std::max(1, 256 / TPS);
+  int smax = std::max(1, (P.R >= 4 ? 256 : 512) / TPS);
   const int64_t want = std::max<int64_t>(1, (B + 2 * p->sms - 1) / (2 * p->sms));
   int S = 1;
   while (S * 2 <= smax && S * 2 <= want && bytes_for(S * 2) <= (size_t)kMaxSmemBytes) S *= 2;
@@ -463,8 +486,8 @@ size_t pass_smem(const VqcPlan* p, bool dual) {
   const HostProgram& P = p->prog;
   const int TPS = 1 << (P.k - P.R);
   const int W = TPS >= 32 ? TPS / 32 : 1;
-  return (size_t)(dual ? 2 : 1) * ((size_t)16 << P.k) + (size_t)P.max_rot_per_pass * 16 +
-         (size_t)2 * red_slots(p) * W * 8 + (size_t)p->M * 8 + 16;
+  return SmemLayout(1, 1 << P.k, dual, P.max_rot_per_pass, P.max_blk_per_pass, P.max_av_per_pass,
+                    red_slots(p), W, p->M).total;
 }
 
 int launch(const char* name, KFn fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
@@ -551,33 +574,33 @@ int run_core(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, const
     for (int pi = 0; pi < NP - 1; ++pi) {
       A.pass = pi;
       A.flags = (pi == 0 ? F_INIT : F_LOAD_PSI) | F_FWD | F_STORE_PSI;
-      if ((rc = launch("pass_forward", pass_kernel(false), grid, block, sm1, st, D, A))) return rc;
+      if ((rc = launch("pass_forward", pass_kernel(P.R, false), grid, block, sm1, st, D, A))) return rc;
     }
     const uint32_t first = NP == 1 ? F_INIT : F_LOAD_PSI;
     A.pass = NP - 1;
     if (mode == VQC_MODE_FORWARD) {
       A.flags = first | F_FWD | F_OBSERVE;
-      if ((rc = launch("pass_forward", pass_kernel(false), grid, block, sm1, st, D, A))) return rc;
+      if ((rc = launch("pass_forward", pass_kernel(P.R, false), grid, block, sm1, st, D, A))) return rc;
     } else if (mode == VQC_MODE_VJP) {
       A.flags = first | F_FWD | F_OBSERVE | F_SEED | F_BWD | (NP > 1 ? (F_STORE_PSI | F_STORE_PHI) : 0);
-      if ((rc = launch("pass_adjoint", pass_kernel(true), grid, block, sm2, st, D, A))) return rc;
+      if ((rc = launch("pass_adjoint", pass_kernel(P.R, true), grid, block, sm2, st, D, A))) return rc;
       for (int pi = NP - 2; pi >= 0; --pi) {
         A.pass = pi;
         A.flags = F_LOAD_PSI | F_LOAD_PHI | F_BWD | (pi > 0 ? (F_STORE_PSI | F_STORE_PHI) : 0);
-        if ((rc = launch("pass_adjoint", pass_kernel(true), grid, block, sm2, st, D, A))) return rc;
+        if ((rc = launch("pass_adjoint", pass_kernel(P.R, true), grid, block, sm2, st, D, A))) return rc;
       }
     } else {
       A.flags = first | F_FWD | F_OBSERVE | F_STORE_FIN;
-      if ((rc = launch("pass_forward", pass_kernel(false), grid, block, sm1, st, D, A))) return rc;
+      if ((rc = launch("pass_forward", pass_kernel(P.R, false), grid, block, sm1, st, D, A))) return rc;
       for (int m = 0; m < p->M; ++m) {
         A.bra = m;
         A.pass = NP - 1;
         A.flags = F_LOAD_FIN | F_SEED | F_BWD | (NP > 1 ? (F_STORE_PSI | F_STORE_PHI) : 0);
-        if ((rc = launch("pass_adjoint", pass_kernel(true), grid, block, sm2, st, D, A))) return rc;
+        if ((rc = launch("pass_adjoint", pass_kernel(P.R, true), grid, block, sm2, st, D, A))) return rc;
         for (int pi = NP - 2; pi >= 0; --pi) {
           A.pass = pi;
           A.flags = F_LOAD_PSI | F_LOAD_PHI | F_BWD | (pi > 0 ? (F_STORE_PSI | F_STORE_PHI) : 0);
-          if ((rc = launch("pass_adjoint", pass_kernel(true), grid, block, sm2, st, D, A))) return rc;
+          if ((rc = launch("pass_adjoint", pass_kernel(P.R, true), grid, block, sm2, st, D, A))) return rc;
         }
       }
     }
@@ -699,6 +722,7 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
   VqcPlan* p = new VqcPlan();
   ScheduleOptions opt;
   opt.tile_qubits = env_int("VQC_TILE_QUBITS", 11);
+  opt.reg_slots = std::max(3, std::min(kMaxR, env_int("VQC_REG_SLOTS", kMaxR)));
   std::string err = build_program(gates, c->n_qubits, c->total_params, wcol, opt, &p->prog);
   if (!err.empty()) {
     delete p;
@@ -739,7 +763,10 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
   const HostProgram& P = p->prog;
   if (e == cudaSuccess) e = upload(P.ops, &p->d_ops);
   if (e == cudaSuccess) e = upload(P.segs, &p->d_segs);
-  if (e == cudaSuccess) e = upload(P.seg_ip, &p->d_seg_ip);
+  if (e == cudaSuccess) e = upload(P.ipouts, &p->d_ipouts);
+  if (e == cudaSuccess) e = upload(P.blocks, &p->d_blocks);
+  if (e == cudaSuccess) e = upload(P.members, &p->d_members);
+  if (e == cudaSuccess) e = upload(P.diag, &p->d_diag);
   if (e == cudaSuccess) e = upload(P.passes, &p->d_passes);
   if (e == cudaSuccess) e = upload(P.rots, &p->d_rots);
   if (e == cudaSuccess) e = upload(p->term_offs, &p->d_term_offs);
@@ -754,7 +781,15 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
   DevProgram& D = p->D;
   D.ops = p->d_ops;
   D.segs = p->d_segs;
-  D.seg_ip = p->d_seg_ip;
+  D.ipouts = p->d_ipouts;
+  D.blocks = p->d_blocks;
+  D.members = p->d_members;
+  D.diag = p->d_diag;
+  D.n_blk = P.n_blk;
+  D.n_av = P.n_av;
+  D.max_rot_pass = P.max_rot_per_pass;
+  D.max_blk_pass = P.max_blk_per_pass;
+  D.max_av_pass = P.max_av_per_pass;
   D.passes = p->d_passes;
   D.rots = p->d_rots;
   D.term_offs = p->d_term_offs;
@@ -778,7 +813,10 @@ void vqc_plan_destroy(VqcPlan* p) {
   if (!p) return;
   cudaFree(p->d_ops);
   cudaFree(p->d_segs);
-  cudaFree(p->d_seg_ip);
+  cudaFree(p->d_ipouts);
+  cudaFree(p->d_blocks);
+  cudaFree(p->d_members);
+  cudaFree(p->d_diag);
   cudaFree(p->d_passes);
   cudaFree(p->d_rots);
   cudaFree(p->d_term_offs);

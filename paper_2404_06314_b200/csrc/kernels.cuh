@@ -14,6 +14,7 @@
 
 #include <type_traits>
 
+#include "blockmath.h"
 #include "program.h"
 
 namespace vqc {
@@ -21,13 +22,17 @@ namespace vqc {
 struct DevProgram {
   const Op* ops;
   const SegDesc* segs;
-  const int32_t* seg_ip;
   const PassDesc* passes;
   const RotDesc* rots;
+  const IpOut* ipouts;
+  const BlockDesc* blocks;
+  const MemberDesc* members;
+  const DiagRun* diag;
   const int32_t* term_offs;  // M + 1
   const uint32_t* t_smask;   // T
   const double* t_coeff;     // T (coeff * Re(phase); Z strings only)
   int n, k, R, NG, n_rot, M, n_pass;
+  int n_blk, n_av, max_rot_pass, max_blk_pass, max_av_pass;
   int64_t enc_off, enc_size;
 };
 
@@ -256,15 +261,66 @@ struct Group {
   __device__ __forceinline__ int red_index(int slot) const { return (slot * S + sl) * W + (gi >> 5); }
 };
 
+// general 2x2 on slot S: a0' = u00 a0 + u01 a1 ; a1' = u10 a0 + u11 a1
+template <int R, int S>
+__device__ __forceinline__ void g_u2(double2 (&a)[1 << R], const double2 u00, const double2 u01,
+                                     const double2 u10, const double2 u11) {
+#pragma unroll
+  for (int i = 0; i < (1 << R); ++i)
+    if (!((i >> S) & 1)) {
+      const int j = i | (1 << S);
+      const double2 x = a[i], y = a[j];
+      a[i] = make_double2(u00.x * x.x - u00.y * x.y + u01.x * y.x - u01.y * y.y,
+                          u00.x * x.y + u00.y * x.x + u01.x * y.y + u01.y * y.x);
+      a[j] = make_double2(u10.x * x.x - u10.y * x.y + u11.x * y.x - u11.y * y.y,
+                          u10.x * x.y + u10.y * x.x + u11.x * y.y + u11.y * y.x);
+    }
+}
+
+// the three Pauli inner products Im<phi|P|psi>, P in {X, Y, Z} on slot S
+template <int R, int S>
+__device__ __forceinline__ void ip_xyz(const double2 (&p)[1 << R], const double2 (&f)[1 << R], double& ix,
+                                       double& iy, double& iz) {
+#pragma unroll
+  for (int i = 0; i < (1 << R); ++i)
+    if (!((i >> S) & 1)) {
+      const int j = i | (1 << S);
+      const double2 f0 = f[i], f1 = f[j], p0 = p[i], p1 = p[j];
+      ix += f0.x * p1.y - f0.y * p1.x;
+      ix += f1.x * p0.y - f1.y * p0.x;
+      iy -= f0.x * p1.x + f0.y * p1.y;
+      iy += f1.x * p0.x + f1.y * p0.y;
+      iz += f0.x * p0.y - f0.y * p0.x;
+      iz -= f1.x * p1.y - f1.y * p1.x;
+    }
+}
+
+// fused CZ run (program.h DiagRun): per-register sign from a quadratic form
+template <int R>
+__device__ __forceinline__ void g_czrun(double2 (&a)[1 << R], uint32_t qreg, uint32_t m, uint32_t qc) {
+#pragma unroll
+  for (int i = 0; i < (1 << R); ++i) {
+    const bool neg = ((qc ^ (qreg >> i) ^ (uint32_t)__popc((uint32_t)i & m)) & 1u) != 0u;
+    a[i] = make_double2(neg_if(a[i].x, neg), neg_if(a[i].y, neg));
+  }
+}
+
+// per-sample parameter tables in shared memory
+struct SampleTables {
+  const double2* cs;  // (cos, sin) of theta/2 per rotation (relative to rot_base)
+  const double2* u;   // 4 entries per fused block (relative to blk_base)
+  int rot_base, blk_base;
+};
+
 template <int R, bool DUAL>
-__device__ __forceinline__ void exec_op(const Op op, double2 (&a)[1 << R], double2 (&f)[1 << R],
-                                        uint32_t J0, const double2* s_cs, int rot_base,
+__device__ __forceinline__ void exec_op(const DevProgram& D, const Op op, double2 (&a)[1 << R],
+                                        double2 (&f)[1 << R], uint32_t J0, const SampleTables& T,
                                         double* s_redbuf, const Group& grp) {
   const uint32_t w0 = op.w0;
   const uint32_t A = op_a(w0), Bq = op_b(w0);
   switch (op_code(w0)) {
     case OP_RX: {
-      const double2 cs = s_cs[(int)op.param - rot_base];
+      const double2 cs = T.cs[(int)op.param - T.rot_base];
       const double sn = op_adj(w0) ? -cs.y : cs.y;
       with_slot<R>(A & 7u, [&](auto SL) {
         g_rx<R, SL.value>(a, cs.x, sn);
@@ -272,7 +328,7 @@ __device__ __forceinline__ void exec_op(const Op op, double2 (&a)[1 << R], doubl
       });
     } break;
     case OP_RY: {
-      const double2 cs = s_cs[(int)op.param - rot_base];
+      const double2 cs = T.cs[(int)op.param - T.rot_base];
       const double sn = op_adj(w0) ? -cs.y : cs.y;
       with_slot<R>(A & 7u, [&](auto SL) {
         g_ry<R, SL.value>(a, cs.x, sn);
@@ -280,26 +336,41 @@ __device__ __forceinline__ void exec_op(const Op op, double2 (&a)[1 << R], doubl
       });
     } break;
     case OP_RZ: {
-      const double2 cs = s_cs[(int)op.param - rot_base];
+      const double2 cs = T.cs[(int)op.param - T.rot_base];
       const double sn = op_adj(w0) ? -cs.y : cs.y;
       const uint32_t m = (A & kSlotFlag) ? (1u << (A & 7u)) : 0u;
       const bool cb = (A & kSlotFlag) ? false : ((J0 >> A) & 1u);
       g_rz<R>(a, cs.x, sn, m, cb);
       if constexpr (DUAL) g_rz<R>(f, cs.x, sn, m, cb);
     } break;
+    case OP_U2: {
+      const double2* u = T.u + 4 * ((int)op.param - T.blk_base);
+      double2 u00 = u[0], u01 = u[1], u10 = u[2], u11 = u[3];
+      if (op_adj(w0)) {  // U^dagger
+        const double2 t = u01;
+        u00.y = -u00.y;
+        u11.y = -u11.y;
+        u01 = make_double2(u10.x, -u10.y);
+        u10 = make_double2(t.x, -t.y);
+      }
+      with_slot<R>(A & 7u, [&](auto SL) {
+        g_u2<R, SL.value>(a, u00, u01, u10, u11);
+        if constexpr (DUAL) g_u2<R, SL.value>(f, u00, u01, u10, u11);
+      });
+    } break;
     case OP_CNOT: {
       if (A & kSlotFlag) {
         with_slot<R>(A & 7u, [&](auto C) {
-          with_slot<R>(Bq & 7u, [&](auto T) {
-            g_cnot_rr<R, C.value, T.value>(a);
-            if constexpr (DUAL) g_cnot_rr<R, C.value, T.value>(f);
+          with_slot<R>(Bq & 7u, [&](auto Tt) {
+            g_cnot_rr<R, C.value, Tt.value>(a);
+            if constexpr (DUAL) g_cnot_rr<R, C.value, Tt.value>(f);
           });
         });
       } else {
         const bool cb = (J0 >> A) & 1u;
-        with_slot<R>(Bq & 7u, [&](auto T) {
-          g_cnot_cr<R, T.value>(a, cb);
-          if constexpr (DUAL) g_cnot_cr<R, T.value>(f, cb);
+        with_slot<R>(Bq & 7u, [&](auto Tt) {
+          g_cnot_cr<R, Tt.value>(a, cb);
+          if constexpr (DUAL) g_cnot_cr<R, Tt.value>(f, cb);
         });
       }
     } break;
@@ -323,6 +394,31 @@ __device__ __forceinline__ void exec_op(const Op op, double2 (&a)[1 << R], doubl
       g_cz<R>(a, m, cond);
       if constexpr (DUAL) g_cz<R>(f, m, cond);
     } break;
+    case OP_CZRUN: {
+      const DiagRun* dr = D.diag + op.param;
+      uint32_t qc = 0, m = 0;
+      for (uint32_t rest = J0; rest != 0; rest &= rest - 1) qc ^= (uint32_t)__popc(J0 & dr->upper[__ffs(rest) - 1]);
+#pragma unroll
+      for (int s = 0; s < R; ++s) m |= ((uint32_t)__popc(J0 & dr->part[s]) & 1u) << s;
+      const uint32_t qreg = dr->qreg;
+      g_czrun<R>(a, qreg, m, qc);
+      if constexpr (DUAL) g_czrun<R>(f, qreg, m, qc);
+    } break;
+    case OP_IP3:
+      if constexpr (DUAL) {
+        double ix = 0.0, iy = 0.0, iz = 0.0;
+        with_slot<R>(A & 7u, [&](auto SL) { ip_xyz<R, SL.value>(a, f, ix, iy, iz); });
+        ix = grp.reduce(ix);
+        iy = grp.reduce(iy);
+        iz = grp.reduce(iz);
+        if (grp.leader()) {
+          const int r0 = (int)op_ip(w0);
+          s_redbuf[grp.red_index(r0)] = ix;
+          s_redbuf[grp.red_index(r0 + 1)] = iy;
+          s_redbuf[grp.red_index(r0 + 2)] = iz;
+        }
+      }
+      break;
     default:
       if constexpr (DUAL) {
         double v = 0.0;
@@ -344,12 +440,15 @@ __device__ __forceinline__ void exec_op(const Op op, double2 (&a)[1 << R], doubl
 }
 
 // Run segments [sb, se) on the tile(s) in shared memory. s_psi / s_phi point at
-// this thread's sample block. IP results go to ip_out (relative row bl).
+// this thread's sample block; T / s_av are this thread's sample tables.
+// Gradient outputs go to A.ip (rows relative to A.b0, times n_tiles).
 template <int R, bool DUAL>
-__device__ void run_segments(const DevProgram& D, const RunArgs& A, int sb, int se, double2* s_psi,
-                             double2* s_phi, const double2* s_cs, int rot_base, double* s_red,
-                             int& red_buf, const Group& grp, uint32_t tile_base, int64_t bl0,
-                             int64_t nb, int bra, int tile, int n_tiles) {
+__device__ __forceinline__ void run_segments(const DevProgram& D, const RunArgs& A, int sb, int se,
+                                             double2* s_psi, double2* s_phi, const SampleTables& T,
+                                             const double* s_av_all, int av_stride, int av_base,
+                                             double* s_red, int& red_buf, const Group& grp,
+                                             uint32_t tile_base, int64_t bl0, int bra, int tile,
+                                             int n_tiles) {
   constexpr int N = 1 << R;
   const int red_stride = A.red_slots * grp.S * grp.W;
   for (int sg = sb; sg < se; ++sg) {
@@ -364,42 +463,126 @@ __device__ void run_segments(const DevProgram& D, const RunArgs& A, int sb, int 
     uint32_t ps[R];
 #pragma unroll
     for (int s = 0; s < R; ++s) ps[s] = swz(1u << sd->reg_l[s]);
-    uint32_t addr[N];
-    addr[0] = swz(L0);
-#pragma unroll
-    for (int i = 1; i < N; ++i) addr[i] = addr[i & (i - 1)] ^ ps[ctz_const(i)];
+    const uint32_t p0 = swz(L0);
     double2 a[N], f[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      a[i] = s_psi[addr[i]];
-      if constexpr (DUAL) f[i] = s_phi[addr[i]];
+      uint32_t ad = p0;
+#pragma unroll
+      for (int s = 0; s < R; ++s)
+        if ((i >> s) & 1) ad ^= ps[s];
+      a[i] = s_psi[ad];
+      if constexpr (DUAL) f[i] = s_phi[ad];
     }
     double* redbuf = s_red + red_buf * red_stride;
     const int ob = sd->op_begin, oe = sd->op_end;
-    for (int o = ob; o < oe; ++o) exec_op<R, DUAL>(D.ops[o], a, f, J0, s_cs, rot_base, redbuf, grp);
+    if (ob < oe) {
+      for (int o = ob; o < oe; ++o) exec_op<R, DUAL>(D, D.ops[o], a, f, J0, T, redbuf, grp);
+    }
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      s_psi[addr[i]] = a[i];
-      if constexpr (DUAL) s_phi[addr[i]] = f[i];
+      uint32_t ad = p0;
+#pragma unroll
+      for (int s = 0; s < R; ++s)
+        if ((i >> s) & 1) ad ^= ps[s];
+      s_psi[ad] = a[i];
+      if constexpr (DUAL) s_phi[ad] = f[i];
     }
     __syncthreads();
     if constexpr (DUAL) {
-      const int nip = sd->ip_count;
-      if (nip > 0) {
-        const int total = nip * grp.S;
+      const int nout = sd->ip_count;
+      if (nout > 0) {
+        const int total = nout * grp.S;
         for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-          const int ipl = idx / grp.S, s_ = idx - ipl * grp.S;
-          double v = 0.0;
-          for (int w = 0; w < grp.W; ++w) v += redbuf[(ipl * grp.S + s_) * grp.W + w];
-          const int64_t bl = bl0 + s_;
-          if (bl < nb) {
-            const int g = D.seg_ip[sd->ip_begin + ipl];
-            A.ip[(((bl * A.K) + bra) * D.NG + g) * n_tiles + tile] = v;
+          const int oi = idx / grp.S, s_ = idx - oi * grp.S;
+          const IpOut io = D.ipouts[sd->ip_begin + oi];
+          auto red = [&](int slot) {
+            double v = 0.0;
+            for (int w = 0; w < grp.W; ++w) v += redbuf[(slot * grp.S + s_) * grp.W + w];
+            return v;
+          };
+          double v;
+          if (io.avec < 0) {
+            v = red(io.red);
+          } else {
+            const double* av = s_av_all + (size_t)s_ * av_stride + 4 * (io.avec - av_base);
+            v = av[0] * red(io.red) + av[1] * red(io.red + 1) + av[2] * red(io.red + 2);
           }
+          const int64_t bl = bl0 + s_;
+          if (bl < A.nb) A.ip[(((bl * A.K) + bra) * D.NG + io.gslot) * n_tiles + tile] = v;
         }
         red_buf ^= 1;
       }
     }
+  }
+}
+
+// Per-sample tables for one pass: (cos, sin) of every rotation, then each
+// fused block's unitary and gradient vectors (blockmath.h). Ends synchronised.
+__device__ __forceinline__ void build_tables(const DevProgram& D, const RunArgs& A, const PassDesc* pd,
+                                             int64_t b, bool valid, double2* cs, double2* u, double* av,
+                                             int lane, int width) {
+  const int nrot = pd->rot_end - pd->rot_begin;
+  for (int r = lane; r < nrot; r += width)
+    cs[r] = valid ? rot_cs(D, A, b, pd->rot_begin + r) : make_double2(1.0, 0.0);
+  __syncthreads();
+  const int nblk = pd->blk_end - pd->blk_begin;
+  for (int k = lane; k < nblk; k += width) {
+    const BlockDesc bd = D.blocks[pd->blk_begin + k];
+    const M2 U = block_unitary(
+        D.members + bd.mem_begin, bd.mem_end - bd.mem_begin,
+        [&](int rot) { return cs[rot - pd->rot_begin]; },
+        [&](int slot, const double* v) {
+          double* o = av + 4 * (slot - pd->av_begin);
+          o[0] = v[0];
+          o[1] = v[1];
+          o[2] = v[2];
+          o[3] = 0.0;
+        });
+    double2* o = u + 4 * k;
+    o[0] = make_double2(U.a.re, U.a.im);
+    o[1] = make_double2(U.b.re, U.b.im);
+    o[2] = make_double2(U.c.re, U.c.im);
+    o[3] = make_double2(U.d.re, U.d.im);
+  }
+  __syncthreads();
+}
+
+// Global indices of the tile elements a thread visits in a strided loop
+// l = lane + i * stride (stride a power of two): dep() is GF(2)-linear, so
+// j(i) = base ^ XOR_{b in i} hi[b]; visiting i in Gray-code order costs one
+// XOR per element.
+struct TileWalk {
+  uint32_t base;
+  uint32_t hi[kMaxQubits];
+  int count;
+};
+
+__device__ __forceinline__ uint32_t dep_local(const PassDesc& pd, uint32_t l, int k) {
+  uint32_t j = 0;
+  for (int p = 0; p < k; ++p) j |= ((l >> p) & 1u) << pd.local_q[p];
+  return j;
+}
+
+__device__ __forceinline__ TileWalk tile_walk(const PassDesc* pd, uint32_t tile_base, int k, int lane,
+                                              int stride) {
+  TileWalk w;
+  const int Nt = 1 << k;
+  w.count = Nt / stride;
+  w.base = tile_base | (pd ? dep_local(*pd, (uint32_t)lane, k) : (uint32_t)lane);
+  int b = 0;
+  for (int s = stride; s < Nt; s <<= 1, ++b) w.hi[b] = pd ? dep_local(*pd, (uint32_t)s, k) : (uint32_t)s;
+  return w;
+}
+
+// calls f(l, j) for every element of this thread: l tile-local, j global
+template <class F>
+__device__ __forceinline__ void for_tile(const TileWalk& w, int lane, int stride, F&& f) {
+  uint32_t j = w.base;
+  for (int i = 0; i < w.count; ++i) {
+    if (i) j ^= w.hi[__ffs(i) - 1];
+    const uint32_t g = (uint32_t)(i ^ (i >> 1));
+    f((uint32_t)lane + g * (uint32_t)stride, j);
   }
 }
 

@@ -36,17 +36,20 @@ enum GateKind : int { G_RX = 0, G_RY = 1, G_RZ = 2, G_CNOT = 3, G_H = 4, G_X = 5
 enum OpCode : uint32_t {
   OP_RX = 0, OP_RY = 1, OP_RZ = 2, OP_CNOT = 3, OP_H = 4, OP_X = 5, OP_CZ = 6,
   OP_IPX = 7, OP_IPY = 8, OP_IPZ = 9,
+  OP_U2 = 10,     // fused run of 1q gates on a register slot: param = block id
+  OP_IP3 = 11,    // Im<phi|X|psi>, Im<phi|Y|psi>, Im<phi|Z|psi> on a slot (3 red slots)
+  OP_CZRUN = 12,  // fused run of CZ gates: param = diagonal-run id
 };
 
 // operand field (6 bits): bit 5 set -> register slot (low 3 bits), else a
 // global qubit number whose bit is constant per thread.
 constexpr uint32_t kSlotFlag = 32u;
 
-// w0: [0,5) opcode | [5,11) operand a | [11,17) operand b | [17,27) local ip
-//     index | bit 31 adjoint (rotations: negate the angle)
+// w0: [0,5) opcode | [5,11) operand a | [11,17) operand b | [17,27) local
+//     reduction slot | bit 31 adjoint (rotations: negate the angle; U2: U^dagger)
 struct Op {
   uint32_t w0;
-  uint32_t param;  // rotation id (rotations) or grad slot (IP ops)
+  uint32_t param;  // rotation id / block id / run id
 };
 
 VQC_HD inline uint32_t op_code(uint32_t w0) { return w0 & 31u; }
@@ -55,9 +58,19 @@ VQC_HD inline uint32_t op_b(uint32_t w0) { return (w0 >> 11) & 63u; }
 VQC_HD inline uint32_t op_ip(uint32_t w0) { return (w0 >> 17) & 1023u; }
 VQC_HD inline bool op_adj(uint32_t w0) { return (w0 >> 31) & 1u; }
 
+// A gradient output of a segment: ip[gslot] = red[red] (direct IP op) or
+// a . (red[red], red[red+1], red[red+2]) with a = the avec table entry
+// (member of a fused block).
+struct IpOut {
+  int32_t gslot;
+  int32_t red;
+  int32_t avec;  // -1: direct
+};
+
 struct SegDesc {
   int32_t op_begin, op_end;
-  int32_t ip_begin, ip_count;  // seg_ip[ip_begin + i] = grad slot of local ip i
+  int32_t ip_begin, ip_count;  // IpOut entries of this segment
+  int32_t red_count;           // reduction slots used
   int8_t nreg, nthr, pad0, pad1;
   int8_t reg_l[kMaxR];         // tile-local bit position of each register slot
   int8_t reg_g[kMaxR];         // global qubit of each register slot
@@ -69,6 +82,8 @@ struct PassDesc {
   int32_t seg_begin, seg_end;    // forward segments
   int32_t bseg_begin, bseg_end;  // adjoint segments (executed in order)
   int32_t rot_begin, rot_end;    // rotation ids used by this pass (contiguous)
+  int32_t blk_begin, blk_end;    // fused blocks (contiguous)
+  int32_t av_begin, av_end;      // block gradient vectors (contiguous)
   int32_t k;                     // local qubits (tile = 2^k amplitudes)
   uint32_t local_mask;           // global qubits local to the tile
   int8_t local_q[kMaxQubits];    // tile-local position -> global qubit
@@ -79,6 +94,28 @@ struct RotDesc {
   double coeff;
   int32_t nf;
   int32_t fidx[kMaxFactors];
+};
+
+// Fused block: members [mem_begin, mem_end) in forward order. U = M_last..M_first.
+struct BlockDesc {
+  int32_t mem_begin, mem_end;
+};
+// kind: G_RX/G_RY/G_RZ/G_H/G_X; rot: rotation id (rotations); avec: gradient
+// vector slot (rotations with a requested factor) or -1.
+struct MemberDesc {
+  int32_t kind, rot, avec;
+};
+
+// Fused CZ run as a quadratic form over the index bits, split for a thread
+// whose non-register bits J0 are fixed and register pattern r varies:
+//   Q(J0 ^ r) = Q(J0) ^ Q(r) ^ parity(r & m(J0)),
+//   Q(r)      = bit r of qreg,
+//   m(J0)_s   = parity(J0 & part[s]),
+//   Q(J0)     = parity(sum_{c in J0} popc(J0 & upper[c])).
+struct DiagRun {
+  uint32_t qreg;
+  uint32_t part[kMaxR];
+  uint32_t upper[kMaxQubits];
 };
 
 // chain rule (_kernels.py:269-278): column col accumulates

@@ -204,6 +204,8 @@ std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total
       if (pg.mask >> q & 1u) { pd.local_q[p] = (int8_t)q; pos_of[q] = p++; }
     }
     pd.rot_begin = next_rot;
+    pd.blk_begin = (int)P->blocks.size();
+    pd.av_begin = P->n_av;
 
     // ---- level 2: register segments inside the tile ----
     std::vector<uint8_t> st2(G, 1);
@@ -211,9 +213,14 @@ std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total
     std::vector<Group> segs = greedy_groups(pg.gates, info, R, 0u, st2);
     if (!pg.gates.empty() && segs.empty()) return "segment scheduling failed";
 
+    struct Item {
+      int type;               // 0 single gate, 1 block (1q run on a slot), 2 CZ run
+      std::vector<int> gates;
+      int id = -1;            // block id / diag-run id
+    };
     pd.seg_begin = (int)P->segs.size();
     std::vector<SegDesc> fwd_descs;
-    std::vector<std::vector<int>> fwd_gates;
+    std::vector<std::vector<Item>> fwd_items;
     for (Group& sgp : segs) {
       // pad register set to exactly R local qubits
       for (int q = 0; q < n && popc(sgp.mask) < R; ++q)
@@ -231,7 +238,7 @@ std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total
       sd.nreg = (int8_t)ns;
       // thread bits: remaining local positions; the first three cover distinct
       // residues mod 3 so each quarter-warp's 16-byte smem accesses hit 8
-      // distinct bank groups under the mod-3 fold swizzle (kernels.cu swz()).
+      // distinct bank groups under the mod-3 fold swizzle (kernels.cuh swz()).
       std::vector<int> rest;
       for (int p = 0; p < k; ++p)
         if (!(sgp.mask >> pd.local_q[p] & 1u)) rest.push_back(p);
@@ -249,39 +256,122 @@ std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total
       auto operand = [&](int q) -> uint32_t {
         return slot_of[q] >= 0 ? (kSlotFlag | (uint32_t)slot_of[q]) : (uint32_t)q;
       };
-      sd.op_begin = (int)P->ops.size();
+
+      // group the segment's gates into items: runs of 1q gates on one register
+      // qubit become a fused block (placed at its first member; later members
+      // only cross gates on other qubits), consecutive CZs become one run
+      std::vector<Item> items;
+      int open_blk[kMaxQubits];
+      for (int q = 0; q < kMaxQubits; ++q) open_blk[q] = -1;
+      int open_run = -1;
       for (int g : sgp.gates) {
         const GateIn& gi = gates[g];
-        Op op{};
-        switch (gi.kind) {
-          case G_RX: case G_RY: case G_RZ:
-            rot_id[g] = next_rot++;
-            if (info[g].need_grad) gslot[g] = next_g++;
-            op.w0 = enc(gi.kind, operand(gi.q0), 0, 0, false);
-            op.param = (uint32_t)rot_id[g];
-            break;
-          case G_H: case G_X:
-            op.w0 = enc(gi.kind, operand(gi.q0), 0, 0, false);
-            break;
-          case G_CNOT: case G_CZ:
-            op.w0 = enc(gi.kind, operand(gi.q0), operand(gi.q1), 0, false);
-            break;
+        const bool one_q = gi.kind == G_RX || gi.kind == G_RY || gi.kind == G_RZ || gi.kind == G_H ||
+                           gi.kind == G_X;
+        if (one_q && slot_of[gi.q0] >= 0) {
+          if (open_blk[gi.q0] >= 0) {
+            items[open_blk[gi.q0]].gates.push_back(g);
+          } else {
+            open_run = -1;
+            items.push_back({1, {g}});
+            open_blk[gi.q0] = (int)items.size() - 1;
+          }
+          continue;
         }
-        if ((info[g].mix & sgp.mask) != info[g].mix) return "internal: mixing qubit not in registers";
+        if (gi.kind == G_CZ) {
+          open_blk[gi.q0] = open_blk[gi.q1] = -1;
+          if (open_run >= 0) {
+            items[open_run].gates.push_back(g);
+          } else {
+            items.push_back({2, {g}});
+            open_run = (int)items.size() - 1;
+          }
+          continue;
+        }
+        open_run = -1;
+        if (gi.kind == G_CNOT) open_blk[gi.q0] = open_blk[gi.q1] = -1;
+        items.push_back({0, {g}});
+      }
+
+      sd.op_begin = (int)P->ops.size();
+      for (Item& it : items) {
+        const int g0 = it.gates[0];
+        const GateIn& gi0 = gates[g0];
+        for (int g : it.gates)
+          if ((info[g].mix & sgp.mask) != info[g].mix) return "internal: mixing qubit not in registers";
+        if (it.type == 1) {
+          for (int g : it.gates)
+            if (gates[g].kind <= G_RZ) {
+              rot_id[g] = next_rot++;
+              if (info[g].need_grad) gslot[g] = next_g++;
+            }
+        }
+        Op op{};
+        if (it.type == 1 && it.gates.size() > 1) {
+          it.id = (int)P->blocks.size();
+          BlockDesc bd{};
+          bd.mem_begin = (int)P->members.size();
+          for (int g : it.gates) {
+            MemberDesc md{};
+            md.kind = gates[g].kind;
+            md.rot = rot_id[g];
+            md.avec = (gates[g].kind <= G_RZ && info[g].need_grad) ? P->n_av++ : -1;
+            P->members.push_back(md);
+          }
+          bd.mem_end = (int)P->members.size();
+          P->blocks.push_back(bd);
+          op.w0 = enc(OP_U2, operand(gi0.q0), 0, 0, false);
+          op.param = (uint32_t)it.id;
+        } else if (it.type == 2 && it.gates.size() > 1) {
+          it.id = (int)P->diag.size();
+          DiagRun dr{};
+          for (int g : it.gates) {
+            const int a = gates[g].q0, b = gates[g].q1;
+            const int sa = slot_of[a], sb = slot_of[b];
+            if (sa >= 0 && sb >= 0) {
+              for (int r = 0; r < (1 << R); ++r)
+                if ((r >> sa & 1) && (r >> sb & 1)) dr.qreg ^= 1u << r;
+            } else if (sa >= 0) {
+              dr.part[sa] ^= 1u << b;
+            } else if (sb >= 0) {
+              dr.part[sb] ^= 1u << a;
+            } else {
+              dr.upper[std::min(a, b)] ^= 1u << std::max(a, b);
+            }
+          }
+          P->diag.push_back(dr);
+          op.w0 = enc(OP_CZRUN, 0, 0, 0, false);
+          op.param = (uint32_t)it.id;
+        } else if (gi0.kind <= G_RZ) {
+          op.w0 = enc(gi0.kind, operand(gi0.q0), 0, 0, false);
+          op.param = (uint32_t)rot_id[g0];
+        } else if (gi0.kind == G_H || gi0.kind == G_X) {
+          op.w0 = enc(gi0.kind, operand(gi0.q0), 0, 0, false);
+        } else {
+          op.w0 = enc(gi0.kind, operand(gi0.q0), operand(gi0.q1), 0, false);
+        }
+        if (it.type == 0 && gi0.kind <= G_RZ) {  // RZ on a non-register qubit
+          rot_id[g0] = next_rot++;
+          if (info[g0].need_grad) gslot[g0] = next_g++;
+          op.param = (uint32_t)rot_id[g0];
+        }
         P->ops.push_back(op);
       }
       sd.op_end = (int)P->ops.size();
-      sd.ip_begin = 0;
-      sd.ip_count = 0;
       P->segs.push_back(sd);
       fwd_descs.push_back(sd);
-      fwd_gates.push_back(sgp.gates);
+      fwd_items.push_back(std::move(items));
     }
     pd.seg_end = (int)P->segs.size();
     pd.rot_end = next_rot;
+    pd.blk_end = (int)P->blocks.size();
+    pd.av_end = P->n_av;
     P->max_rot_per_pass = std::max(P->max_rot_per_pass, pd.rot_end - pd.rot_begin);
+    P->max_blk_per_pass = std::max(P->max_blk_per_pass, pd.blk_end - pd.blk_begin);
+    P->max_av_per_pass = std::max(P->max_av_per_pass, pd.av_end - pd.av_begin);
 
-    // adjoint segments: forward segments reversed, ops reversed, IP before un-apply
+    // adjoint segments: forward segments reversed, items reversed; gradient
+    // inner products before each un-apply
     pd.bseg_begin = (int)P->segs.size();
     for (int si = (int)fwd_descs.size() - 1; si >= 0; --si) {
       SegDesc sd = fwd_descs[si];
@@ -292,35 +382,62 @@ std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total
         return slot_of[q] >= 0 ? (kSlotFlag | (uint32_t)slot_of[q]) : (uint32_t)q;
       };
       sd.op_begin = (int)P->ops.size();
-      sd.ip_begin = (int)P->seg_ip.size();
-      int nip = 0;
-      const std::vector<int>& gl = fwd_gates[si];
-      for (int gi_ = (int)gl.size() - 1; gi_ >= 0; --gi_) {
-        const int g = gl[gi_];
-        const GateIn& gi = gates[g];
-        if (info[g].rot && info[g].need_grad) {
-          Op ip{};
-          ip.w0 = enc(OP_IPX + gi.kind, operand(gi.q0), 0, (uint32_t)nip, false);
-          ip.param = (uint32_t)gslot[g];
-          P->ops.push_back(ip);
-          P->seg_ip.push_back(gslot[g]);
-          ++nip;
-        }
+      sd.ip_begin = (int)P->ipouts.size();
+      int nred = 0, nout = 0;
+      const std::vector<Item>& items = fwd_items[si];
+      for (int ii = (int)items.size() - 1; ii >= 0; --ii) {
+        const Item& it = items[ii];
+        const int g0 = it.gates[0];
+        const GateIn& gi0 = gates[g0];
         Op op{};
-        if (info[g].rot) {
-          op.w0 = enc(gi.kind, operand(gi.q0), 0, 0, true);
-          op.param = (uint32_t)rot_id[g];
-        } else if (gi.kind == G_H || gi.kind == G_X) {
-          op.w0 = enc(gi.kind, operand(gi.q0), 0, 0, false);
+        if (it.type == 1 && it.gates.size() > 1) {
+          bool any = false;
+          for (int g : it.gates) any = any || (gates[g].kind <= G_RZ && info[g].need_grad);
+          if (any) {
+            Op ip{};
+            ip.w0 = enc(OP_IP3, operand(gi0.q0), 0, (uint32_t)nred, false);
+            ip.param = (uint32_t)it.id;
+            P->ops.push_back(ip);
+            const BlockDesc& bd = P->blocks[it.id];
+            for (int mi = bd.mem_begin; mi < bd.mem_end; ++mi) {
+              const MemberDesc& md = P->members[mi];
+              if (md.avec < 0) continue;
+              const int g = it.gates[mi - bd.mem_begin];
+              P->ipouts.push_back({gslot[g], nred, md.avec});
+              ++nout;
+            }
+            nred += 3;
+          }
+          op.w0 = enc(OP_U2, operand(gi0.q0), 0, 0, true);
+          op.param = (uint32_t)it.id;
+        } else if (it.type == 2 && it.gates.size() > 1) {
+          op.w0 = enc(OP_CZRUN, 0, 0, 0, false);
+          op.param = (uint32_t)it.id;
+        } else if (gi0.kind <= G_RZ) {
+          if (info[g0].need_grad) {
+            Op ip{};
+            ip.w0 = enc(OP_IPX + gi0.kind, operand(gi0.q0), 0, (uint32_t)nred, false);
+            ip.param = (uint32_t)gslot[g0];
+            P->ops.push_back(ip);
+            P->ipouts.push_back({gslot[g0], nred, -1});
+            ++nred;
+            ++nout;
+          }
+          op.w0 = enc(gi0.kind, operand(gi0.q0), 0, 0, true);
+          op.param = (uint32_t)rot_id[g0];
+        } else if (gi0.kind == G_H || gi0.kind == G_X) {
+          op.w0 = enc(gi0.kind, operand(gi0.q0), 0, 0, false);
         } else {
-          op.w0 = enc(gi.kind, operand(gi.q0), operand(gi.q1), 0, false);
+          op.w0 = enc(gi0.kind, operand(gi0.q0), operand(gi0.q1), 0, false);
         }
         P->ops.push_back(op);
       }
-      if (nip > 1023) return "too many gradient rotations in one segment";
+      if (nred > 1023) return "too many gradient rotations in one segment";
       sd.op_end = (int)P->ops.size();
-      sd.ip_count = nip;
-      P->max_ip_per_seg = std::max(P->max_ip_per_seg, nip);
+      sd.ip_count = nout;
+      sd.red_count = nred;
+      P->max_red_per_seg = std::max(P->max_red_per_seg, nred);
+      P->max_ipout_per_seg = std::max(P->max_ipout_per_seg, nout);
       P->segs.push_back(sd);
     }
     pd.bseg_end = (int)P->segs.size();
@@ -328,7 +445,7 @@ std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total
   }
   P->n_rot = next_rot;
   P->NG = next_g;
-  for (const SegDesc& s : P->segs) (void)s;
+  P->n_blk = (int)P->blocks.size();
   P->n_fwd_ops = 0;
   P->n_bwd_ops = 0;
   for (const PassDesc& pd : P->passes) {

@@ -29,13 +29,18 @@ struct HostProgram {
   bool hbm = false;
   int n_rot = 0;   // rotations (angle table entries)
   int NG = 0;      // grad slots (rotations with a requested factor)
-  int max_ip_per_seg = 0;
-  int max_rot_per_pass = 0;
+  int n_blk = 0, n_av = 0;
+  int max_red_per_seg = 0;    // reduction slots
+  int max_ipout_per_seg = 0;
+  int max_rot_per_pass = 0, max_blk_per_pass = 0, max_av_per_pass = 0;
   std::vector<PassDesc> passes;
   std::vector<SegDesc> segs;
   std::vector<Op> ops;
-  std::vector<int32_t> seg_ip;
+  std::vector<IpOut> ipouts;
   std::vector<RotDesc> rots;
+  std::vector<BlockDesc> blocks;
+  std::vector<MemberDesc> members;
+  std::vector<DiagRun> diag;
   int n_cols = 0;
   std::vector<int32_t> col_offs;  // n_cols + 1
   std::vector<ChainEntry> chain;

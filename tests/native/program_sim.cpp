@@ -9,6 +9,7 @@
 // rely on (tile sizes, slot/thread-bit partitions, mixing operands in
 // registers). It does not model the kernels' tiling arithmetic (swizzle,
 // pdep); the GPU parity tests cover that.
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <complex>
@@ -16,6 +17,7 @@
 #include <string>
 #include <vector>
 
+#include "../../paper_2404_06314_b200/csrc/blockmath.h"
 #include "../../paper_2404_06314_b200/csrc/scheduler.h"
 
 using namespace vqc;
@@ -110,6 +112,13 @@ std::string check_program(const HostProgram& P, const ScheduleOptions& opt) {
           return true;
         };
         switch (code) {
+          case OP_CZRUN:
+            if ((int)op.param >= (int)P.diag.size()) return "bad diag run id";
+            break;
+          case OP_U2: case OP_IP3:
+            if ((int)op.param < pd.blk_begin || (int)op.param >= pd.blk_end) return "block id outside pass range";
+            if (!in_regs(a)) return "block operand not a register slot";
+            break;
           case OP_RX: case OP_RY: case OP_H: case OP_X: case OP_IPX: case OP_IPY:
             if (!in_regs(a)) return "mixing operand not a register slot";
             break;
@@ -195,12 +204,46 @@ int sim_run(int n, int64_t G, const int64_t* kinds, const int64_t* q0, const int
   auto qubit_of = [](const SegDesc& sd, uint32_t x) -> int {
     return (x & kSlotFlag) ? sd.reg_g[x & 7u] : (int)x;
   };
+  // per-sample block tables (same math as the kernels' build_tables)
+  struct CS { double x, y; };
+  std::vector<M2> U(P.blocks.size());
+  std::vector<std::array<double, 3>> avec((size_t)P.n_av);
+  for (size_t bi = 0; bi < P.blocks.size(); ++bi) {
+    const BlockDesc& bd = P.blocks[bi];
+    U[bi] = block_unitary(P.members.data() + bd.mem_begin, bd.mem_end - bd.mem_begin,
+                          [&](int r) { return CS{c[r], s[r]}; },
+                          [&](int slot, const double* v) { avec[slot] = {v[0], v[1], v[2]}; });
+  }
   auto apply = [&](std::vector<cd>& st, const SegDesc& sd, const Op& op) {
     const uint32_t code = op_code(op.w0);
     const int qa = qubit_of(sd, op_a(op.w0)), qb = qubit_of(sd, op_b(op.w0));
     if (code <= OP_RZ) {
       const double sn = op_adj(op.w0) ? -s[op.param] : s[op.param];
       S.rot(st, (int)code, qa, c[op.param], sn);
+    } else if (code == OP_U2) {
+      M2 u = U[op.param];
+      if (op_adj(op.w0)) u = mdag(u);
+      const size_t m = (size_t)1 << qa;
+      for (size_t j = 0; j < st.size(); ++j) {
+        if (j & m) continue;
+        const cd x = st[j], y = st[j | m];
+        st[j] = cd(u.a.re, u.a.im) * x + cd(u.b.re, u.b.im) * y;
+        st[j | m] = cd(u.c.re, u.c.im) * x + cd(u.d.re, u.d.im) * y;
+      }
+    } else if (code == OP_CZRUN) {
+      const DiagRun& dr = P.diag[op.param];
+      uint32_t regmask = 0;
+      for (int q = 0; q < sd.nreg; ++q) regmask |= 1u << sd.reg_g[q];
+      for (size_t j = 0; j < st.size(); ++j) {
+        const uint32_t J0 = (uint32_t)j & ~regmask;
+        uint32_t r = 0;
+        for (int q = 0; q < sd.nreg; ++q) r |= ((uint32_t)(j >> sd.reg_g[q]) & 1u) << q;
+        uint32_t qc = 0, mm = 0;
+        for (int cb = 0; cb < n; ++cb)
+          if (J0 >> cb & 1u) qc ^= (uint32_t)__builtin_popcount(J0 & dr.upper[cb]);
+        for (int q = 0; q < sd.nreg; ++q) mm |= ((uint32_t)__builtin_popcount(J0 & dr.part[q]) & 1u) << q;
+        if ((qc ^ (dr.qreg >> r) ^ (uint32_t)__builtin_popcount(r & mm)) & 1u) st[j] = -st[j];
+      }
     } else {
       S.fixed(st, (int)code, qa, qb);
     }
@@ -240,19 +283,29 @@ int sim_run(int n, int64_t G, const int64_t* kinds, const int64_t* q0, const int
       const PassDesc& pd = P.passes[pi];
       for (int sg = pd.bseg_begin; sg < pd.bseg_end; ++sg) {
         const SegDesc& sd = P.segs[sg];
+        std::vector<double> red((size_t)std::max(1, sd.red_count), 0.0);
         for (int o = sd.op_begin; o < sd.op_end; ++o) {
           const Op& op = P.ops[o];
           const uint32_t code = op_code(op.w0);
-          if (code >= OP_IPX) {
-            ipv[op.param] = S.ip((int)(code - OP_IPX), qubit_of(sd, op_a(op.w0)));
-            if (P.seg_ip[sd.ip_begin + op_ip(op.w0)] != (int32_t)op.param) {
-              snprintf(err, (size_t)errcap, "seg_ip table mismatch");
-              return -1;
-            }
+          const int q = qubit_of(sd, op_a(op.w0));
+          if (code == OP_IPX || code == OP_IPY || code == OP_IPZ) {
+            red[op_ip(op.w0)] = S.ip((int)(code - OP_IPX), q);
+          } else if (code == OP_IP3) {
+            for (int ax = 0; ax < 3; ++ax) red[op_ip(op.w0) + ax] = S.ip(ax, q);
           } else {
             apply(S.psi, sd, op);
             apply(S.phi, sd, op);
           }
+        }
+        for (int oi = 0; oi < sd.ip_count; ++oi) {
+          const IpOut& io = P.ipouts[sd.ip_begin + oi];
+          if (io.red < 0 || io.red >= sd.red_count) {
+            snprintf(err, (size_t)errcap, "IpOut reduction slot out of range");
+            return -1;
+          }
+          ipv[io.gslot] = io.avec < 0 ? red[io.red]
+                                      : avec[io.avec][0] * red[io.red] + avec[io.avec][1] * red[io.red + 1] +
+                                            avec[io.avec][2] * red[io.red + 2];
         }
       }
     }
