@@ -20,19 +20,19 @@ namespace vqc {
 // ------------------------------------------------------------------ kernels
 
 template <bool DUAL>
-__device__ void observe(const DevProgram& D, const RunArgs& A, const PassDesc* pd, double2* s_psi,
+__device__ __forceinline__ void observe(const DevProgram& D, const RunArgs& A, const PassDesc* pd, double2* s_psi,
                         double2* s_phi, const double* s_u_row, const Group& grp, double* s_red,
-                        int& red_buf, uint32_t tile_base, int k, int64_t bl0, bool do_expect,
+                        uint32_t tile_base, int k, int64_t bl0, bool do_expect,
                         int seed_mode, int bra, int tile, int n_tiles) {
   const int Nt = 1 << k;
   if (do_expect) {
-    const int red_stride = A.red_slots * grp.S * grp.W;
-    double* redbuf = s_red + red_buf * red_stride;
-    const TileWalk tw = tile_walk(pd, tile_base, k, grp.gi, grp.TPS);
+    double* redbuf = s_red;
+    const int lane = grp.lane_in_sample();
+    const TileWalk tw = tile_walk(pd, tile_base, k, lane, grp.TT);
     for (int m = 0; m < D.M; ++m) {
       const int lo = D.term_offs[m], hi = D.term_offs[m + 1];
       double acc = 0.0;
-      for_tile(tw, grp.gi, grp.TPS, [&](uint32_t l, uint32_t j) {
+      for_tile(tw, lane, grp.TT, [&](uint32_t l, uint32_t j) {
         const double2 x = s_psi[swz(l)];
         acc += zweight(D, j, lo, hi) * (x.x * x.x + x.y * x.y);
       });
@@ -48,12 +48,13 @@ __device__ void observe(const DevProgram& D, const RunArgs& A, const PassDesc* p
       const int64_t bl = bl0 + s_;
       if (bl < A.nb) A.expect[(bl * D.M + m) * n_tiles + tile] = v;
     }
-    red_buf ^= 1;
+    __syncthreads();
   }
   if constexpr (DUAL) {
     if (seed_mode != 0) {
-      const TileWalk tw = tile_walk(pd, tile_base, k, grp.gi, grp.TPS);
-      for_tile(tw, grp.gi, grp.TPS, [&](uint32_t l, uint32_t j) {
+      const int lane = grp.lane_in_sample();
+      const TileWalk tw = tile_walk(pd, tile_base, k, lane, grp.TT);
+      for_tile(tw, lane, grp.TT, [&](uint32_t l, uint32_t j) {
         double w = 0.0;
         if (seed_mode == 1) {
           for (int m = 0; m < D.M; ++m) {
@@ -75,39 +76,56 @@ __device__ void observe(const DevProgram& D, const RunArgs& A, const PassDesc* p
 struct SmemLayout {
   size_t psi, phi, cs, u, av, red, up, total;  // byte offsets
   __host__ __device__ SmemLayout(int S, int n_amp, bool dual, int nrot, int nblk, int nav, int red_slots,
-                                 int W, int M) {
+                                 int threads, int M) {
     size_t o = 0;
     psi = o; o += (size_t)S * n_amp * 16;
     phi = o; o += dual ? (size_t)S * n_amp * 16 : 0;
     cs = o; o += (size_t)S * nrot * 16;
     u = o; o += (size_t)S * nblk * 64;
     av = o; o += (size_t)S * nav * 32;
-    red = o; o += (size_t)2 * red_slots * S * W * 8;
+    red = o; o += (size_t)red_slots * threads * 8;
     up = o; o += (size_t)S * M * 8;
     total = o + 16;
   }
 };
 
+// kernel modes: forward only / adjoint with both states per thread (small n) /
+// adjoint split over (psi, phi) thread pairs
+enum { KM_FWD = 0, KM_DUAL = 1, KM_SPLIT = 2 };
+
+template <int R, int KM>
+__device__ __forceinline__ Group make_group(int threads_per_role, int samples) {
+  Group g;
+  g.tid = threadIdx.x;
+  g.TPS = threads_per_role;
+  g.TT = KM == KM_SPLIT ? 2 * threads_per_role : threads_per_role;
+  g.S = samples;
+  const int lane = threadIdx.x % g.TT;
+  g.sl = threadIdx.x / g.TT;
+  g.role = lane / g.TPS;
+  g.gi = lane % g.TPS;
+  g.W = g.TT >= 32 ? g.TT >> 5 : 1;
+  return g;
+}
+
 // Whole state on chip: one CTA owns S samples of n <= 12 qubits and runs
 // forward, expectations, seed and the adjoint sweep without touching HBM.
-template <int R, bool DUAL>
-__global__ void __launch_bounds__(R >= 4 ? 256 : 512) k_smem(DevProgram D, RunArgs A) {
+template <int R, int KM>
+__global__ void __launch_bounds__(KM == KM_SPLIT ? 512 : (R >= 4 ? 256 : 512))
+    k_smem(DevProgram D, RunArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr bool ADJ = KM != KM_FWD;
+  constexpr int BM = KM == KM_SPLIT ? MODE_SPLIT : MODE_DUAL;
   const int n = D.n, N = 1 << n;
-  Group grp;
-  grp.tid = threadIdx.x;
-  grp.TPS = 1 << (n - R);
-  grp.S = A.S;
-  grp.gi = threadIdx.x & (grp.TPS - 1);
-  grp.sl = threadIdx.x >> (n - R);
-  grp.W = grp.TPS >= 32 ? grp.TPS >> 5 : 1;
+  const Group grp = make_group<R, KM>(1 << (n - R), A.S);
+  const int lane = grp.lane_in_sample();
   const int64_t bl0 = (int64_t)blockIdx.x * A.S;
   const int64_t bl = bl0 + grp.sl;
   const bool valid = bl < A.nb;
   const int64_t b = A.b0 + (valid ? bl : 0);
   const PassDesc* pd = D.passes;
   const int nrot = D.n_rot, nblk = D.n_blk, nav = D.n_av;
-  const SmemLayout L(A.S, N, DUAL, nrot, nblk, nav, A.red_slots, grp.W, D.M);
+  const SmemLayout L(A.S, N, ADJ, nrot, nblk, nav, A.red_slots, (int)blockDim.x, D.M);
   double2* s_psi = reinterpret_cast<double2*>(smem_raw + L.psi) + (size_t)grp.sl * N;
   double2* s_phi = reinterpret_cast<double2*>(smem_raw + L.phi) + (size_t)grp.sl * N;
   double2* s_cs = reinterpret_cast<double2*>(smem_raw + L.cs) + (size_t)grp.sl * nrot;
@@ -116,60 +134,59 @@ __global__ void __launch_bounds__(R >= 4 ? 256 : 512) k_smem(DevProgram D, RunAr
   double* s_red = reinterpret_cast<double*>(smem_raw + L.red);
   double* s_up = reinterpret_cast<double*>(smem_raw + L.up);
 
-  for (int l = grp.gi; l < N; l += grp.TPS) s_psi[swz((uint32_t)l)] = make_double2(l == 0 ? 1.0 : 0.0, 0.0);
-  if (DUAL && A.upstream != nullptr)
-    for (int m = grp.gi; m < D.M; m += grp.TPS) s_up[grp.sl * D.M + m] = valid ? A.upstream[b * D.M + m] : 0.0;
-  build_tables(D, A, pd, b, valid, s_cs, s_u, s_av_all + (size_t)grp.sl * nav * 4, grp.gi, grp.TPS);
+  for (int l = lane; l < N; l += grp.TT) s_psi[swz((uint32_t)l)] = make_double2(l == 0 ? 1.0 : 0.0, 0.0);
+  if (ADJ && A.upstream != nullptr)
+    for (int m = lane; m < D.M; m += grp.TT) s_up[grp.sl * D.M + m] = valid ? A.upstream[b * D.M + m] : 0.0;
+  build_tables(D, A, pd, b, valid, s_cs, s_u, s_av_all + (size_t)grp.sl * nav * 4, lane, grp.TT);
   const SampleTables T{s_cs, s_u, 0, 0};
 
-  int red_buf = 0;
-  run_segments<R, false>(D, A, pd->seg_begin, pd->seg_end, s_psi, s_psi, T, s_av_all, nav * 4, 0, s_red,
-                         red_buf, grp, 0u, bl0, 0, 0, 1);
-  if constexpr (!DUAL) {
-    observe<false>(D, A, nullptr, s_psi, s_psi, nullptr, grp, s_red, red_buf, 0u, n, bl0, true, 0, 0, 0, 1);
+  run_segments<R, MODE_FWD>(D, A, pd->seg_begin, pd->seg_end, s_psi, s_psi, T, s_av_all, nav * 4, 0, s_red,
+                            grp, grp.role == 0, 0u, bl0, 0, 0, 1);
+  if constexpr (!ADJ) {
+    observe<false>(D, A, nullptr, s_psi, s_psi, nullptr, grp, s_red, 0u, n, bl0, true, 0, 0, 0, 1);
   } else {
     if (!A.jacobian) {
-      observe<true>(D, A, nullptr, s_psi, s_phi, s_up + grp.sl * D.M, grp, s_red, red_buf, 0u, n, bl0,
+      observe<true>(D, A, nullptr, s_psi, s_phi, s_up + grp.sl * D.M, grp, s_red, 0u, n, bl0,
                     A.expect != nullptr, 1, 0, 0, 1);
       __syncthreads();
-      run_segments<R, true>(D, A, pd->bseg_begin, pd->bseg_end, s_psi, s_phi, T, s_av_all, nav * 4, 0, s_red,
-                            red_buf, grp, 0u, bl0, 0, 0, 1);
+      run_segments<R, BM>(D, A, pd->bseg_begin, pd->bseg_end, s_psi, s_phi, T, s_av_all, nav * 4, 0, s_red,
+                          grp, true, 0u, bl0, 0, 0, 1);
     } else {
-      observe<true>(D, A, nullptr, s_psi, s_phi, nullptr, grp, s_red, red_buf, 0u, n, bl0,
+      observe<true>(D, A, nullptr, s_psi, s_phi, nullptr, grp, s_red, 0u, n, bl0,
                     A.expect != nullptr, 0, 0, 0, 1);
       double2* fin = A.psi_fin + (size_t)bl * N;
       if (D.M > 1 && valid)
-        for (int l = grp.gi; l < N; l += grp.TPS) fin[l] = s_psi[swz((uint32_t)l)];
+        for (int l = lane; l < N; l += grp.TT) fin[l] = s_psi[swz((uint32_t)l)];
       for (int m = 0; m < D.M; ++m) {
         if (m > 0) {
           __syncthreads();
           if (valid)
-            for (int l = grp.gi; l < N; l += grp.TPS) s_psi[swz((uint32_t)l)] = fin[l];
+            for (int l = lane; l < N; l += grp.TT) s_psi[swz((uint32_t)l)] = fin[l];
         }
-        observe<true>(D, A, nullptr, s_psi, s_phi, nullptr, grp, s_red, red_buf, 0u, n, bl0, false, 2, m,
-                      0, 1);
+        observe<true>(D, A, nullptr, s_psi, s_phi, nullptr, grp, s_red, 0u, n, bl0, false, 2, m, 0, 1);
         __syncthreads();
-        run_segments<R, true>(D, A, pd->bseg_begin, pd->bseg_end, s_psi, s_phi, T, s_av_all, nav * 4, 0,
-                              s_red, red_buf, grp, 0u, bl0, m, 0, 1);
+        run_segments<R, BM>(D, A, pd->bseg_begin, pd->bseg_end, s_psi, s_phi, T, s_av_all, nav * 4, 0,
+                            s_red, grp, true, 0u, bl0, m, 0, 1);
       }
     }
   }
 }
 
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 // One pass over HBM-resident states: CTA (tile, row) stages 2^k amplitudes.
-template <int R, bool DUAL>
-__global__ void __launch_bounds__(R >= 4 ? 256 : 512) k_pass(DevProgram D, RunArgs A) {
+template <int R, int KM>
+__global__ void __launch_bounds__(R >= 4 ? 256 : 512, R >= 4 ? 2 : 1) k_pass(DevProgram D, RunArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr bool ADJ = KM != KM_FWD;
   const PassDesc* pd = D.passes + A.pass;
   const int k = pd->k, Nt = 1 << k;
   const uint32_t flags = A.flags;
-  Group grp;
-  grp.tid = threadIdx.x;
-  grp.TPS = blockDim.x;
-  grp.S = 1;
-  grp.gi = threadIdx.x;
-  grp.sl = 0;
-  grp.W = grp.TPS >= 32 ? grp.TPS >> 5 : 1;
+  const Group grp = make_group<R, KM>(1 << (k - R), 1);
   const int tile = blockIdx.x, n_tiles = gridDim.x;
   const int64_t bl = blockIdx.y;
   const int64_t b = A.b0 + bl;
@@ -181,7 +198,8 @@ __global__ void __launch_bounds__(R >= 4 ? 256 : 512) k_pass(DevProgram D, RunAr
     for (int q = 0; q < D.n; ++q)
       if (!((lm >> q) & 1u)) tile_base |= (((uint32_t)tile >> c++) & 1u) << q;
   }
-  const SmemLayout L(1, Nt, DUAL, D.max_rot_pass, D.max_blk_pass, D.max_av_pass, A.red_slots, grp.W, D.M);
+  const SmemLayout L(1, Nt, ADJ, D.max_rot_pass, D.max_blk_pass, D.max_av_pass, A.red_slots, (int)blockDim.x,
+                     D.M);
   double2* s_psi = reinterpret_cast<double2*>(smem_raw + L.psi);
   double2* s_phi = reinterpret_cast<double2*>(smem_raw + L.phi);
   double2* s_cs = reinterpret_cast<double2*>(smem_raw + L.cs);
@@ -190,43 +208,45 @@ __global__ void __launch_bounds__(R >= 4 ? 256 : 512) k_pass(DevProgram D, RunAr
   double* s_red = reinterpret_cast<double*>(smem_raw + L.red);
   double* s_up = reinterpret_cast<double*>(smem_raw + L.up);
 
-  if (DUAL && (flags & F_SEED) && A.bra < 0)
+  if (ADJ && (flags & F_SEED) && A.bra < 0)
     for (int m = threadIdx.x; m < D.M; m += blockDim.x) s_up[m] = A.upstream[b * D.M + m];
   const TileWalk tw = tile_walk(pd, tile_base, k, threadIdx.x, blockDim.x);
   if (flags & F_INIT) {
     for (int l = threadIdx.x; l < Nt; l += blockDim.x)
       s_psi[swz((uint32_t)l)] = make_double2((tile_base == 0 && l == 0) ? 1.0 : 0.0, 0.0);
   } else {
+    // asynchronous 16-byte copies straight into the swizzled tile; they land
+    // while the per-sample tables are built
     const double2* src = ((flags & F_LOAD_FIN) ? A.psi_fin : A.psi) + (size_t)bl * N;
     const double2* srcf = A.phi + (size_t)bl * N;
-    const bool lphi = DUAL && (flags & F_LOAD_PHI);
+    const bool lphi = ADJ && (flags & F_LOAD_PHI);
     for_tile(tw, threadIdx.x, blockDim.x, [&](uint32_t l, uint32_t j) {
-      s_psi[swz(l)] = src[j];
-      if (lphi) s_phi[swz(l)] = srcf[j];
+      cp_async16(s_psi + swz(l), src + j);
+      if (lphi) cp_async16(s_phi + swz(l), srcf + j);
     });
   }
   build_tables(D, A, pd, b, true, s_cs, s_u, s_av, threadIdx.x, blockDim.x);
+  cp_async_wait_all();
+  __syncthreads();
   const SampleTables T{s_cs, s_u, pd->rot_begin, pd->blk_begin};
-  int red_buf = 0;
   if (flags & F_FWD)
-    run_segments<R, false>(D, A, pd->seg_begin, pd->seg_end, s_psi, s_psi, T, s_av, 0, pd->av_begin, s_red,
-                           red_buf, grp, tile_base, bl, 0, tile, n_tiles);
+    run_segments<R, MODE_FWD>(D, A, pd->seg_begin, pd->seg_end, s_psi, s_psi, T, s_av, 0, pd->av_begin, s_red,
+                              grp, grp.role == 0, tile_base, bl, 0, tile, n_tiles);
   if (flags & F_STORE_FIN) {
     double2* dst = A.psi_fin + (size_t)bl * N;
     for_tile(tw, threadIdx.x, blockDim.x, [&](uint32_t l, uint32_t j) { dst[j] = s_psi[swz(l)]; });
   }
   if (flags & (F_OBSERVE | F_SEED)) {
-    observe<DUAL>(D, A, pd, s_psi, s_phi, s_up, grp, s_red, red_buf, tile_base, k, bl,
-                  (flags & F_OBSERVE) != 0, (flags & F_SEED) ? (A.bra < 0 ? 1 : 2) : 0, A.bra, tile,
-                  n_tiles);
+    observe<ADJ>(D, A, pd, s_psi, s_phi, s_up, grp, s_red, tile_base, k, bl, (flags & F_OBSERVE) != 0,
+                 (flags & F_SEED) ? (A.bra < 0 ? 1 : 2) : 0, A.bra, tile, n_tiles);
     __syncthreads();
   }
-  if constexpr (DUAL) {
+  if constexpr (ADJ) {
     if (flags & F_BWD)
-      run_segments<R, true>(D, A, pd->bseg_begin, pd->bseg_end, s_psi, s_phi, T, s_av, 0, pd->av_begin,
-                            s_red, red_buf, grp, tile_base, bl, A.bra < 0 ? 0 : A.bra, tile, n_tiles);
+      run_segments<R, MODE_SPLIT>(D, A, pd->bseg_begin, pd->bseg_end, s_psi, s_phi, T, s_av, 0, pd->av_begin,
+                                  s_red, grp, true, tile_base, bl, A.bra < 0 ? 0 : A.bra, tile, n_tiles);
   }
-  const bool sphi = DUAL && (flags & F_STORE_PHI);
+  const bool sphi = ADJ && (flags & F_STORE_PHI);
   if ((flags & F_STORE_PSI) || sphi) {
     double2* dst = A.psi + (size_t)bl * N;
     double2* dstf = A.phi + (size_t)bl * N;
@@ -288,17 +308,30 @@ __global__ void k_batch_sum(const double* __restrict__ rows, int64_t nb, int nco
 
 using KFn = void (*)(DevProgram, RunArgs);
 
-KFn smem_kernel(int R, bool dual) {
+// small registers sets (n < 9) keep both states per thread; larger tiles
+// split the adjoint over (psi, phi) thread pairs
+bool use_split(int n, int R) { return (n - R) >= 5; }
+
+KFn smem_kernel(int R, bool dual, bool split) {
+  if (!dual) {
+    switch (R) {
+      case 1: return k_smem<1, KM_FWD>;
+      case 2: return k_smem<2, KM_FWD>;
+      case 3: return k_smem<3, KM_FWD>;
+      default: return k_smem<4, KM_FWD>;
+    }
+  }
+  if (split) return R >= 4 ? k_smem<4, KM_SPLIT> : k_smem<3, KM_SPLIT>;
   switch (R) {
-    case 1: return dual ? k_smem<1, true> : k_smem<1, false>;
-    case 2: return dual ? k_smem<2, true> : k_smem<2, false>;
-    case 3: return dual ? k_smem<3, true> : k_smem<3, false>;
-    default: return dual ? k_smem<4, true> : k_smem<4, false>;
+    case 1: return k_smem<1, KM_DUAL>;
+    case 2: return k_smem<2, KM_DUAL>;
+    case 3: return k_smem<3, KM_DUAL>;
+    default: return k_smem<4, KM_DUAL>;
   }
 }
 KFn pass_kernel(int R, bool dual) {
-  if (R >= 4) return dual ? k_pass<4, true> : k_pass<4, false>;
-  return dual ? k_pass<3, true> : k_pass<3, false>;
+  if (R >= 4) return dual ? k_pass<4, KM_SPLIT> : k_pass<4, KM_FWD>;
+  return dual ? k_pass<3, KM_SPLIT> : k_pass<3, KM_FWD>;
 }
 
 }  // namespace vqc
@@ -467,14 +500,17 @@ Layout make_layout(const VqcPlan* p, int64_t B, int mode) {
 int red_slots(const VqcPlan* p) { return std::max(1, std::max(p->M, p->prog.max_red_per_seg)); }
 
 // samples per CTA in smem mode
-int smem_samples(const VqcPlan* p, int64_t B, bool dual, size_t* smem_bytes) {
+int smem_samples(const VqcPlan* p, int64_t B, bool dual, size_t* smem_bytes, int* threads_per_sample) {
   const HostProgram& P = p->prog;
   const int TPS = 1 << (P.n - P.R);
-  const int W = TPS >= 32 ? TPS / 32 : 1;
+  const bool split = dual && use_split(P.n, P.R);
+  const int TT = split ? 2 * TPS : TPS;
+  *threads_per_sample = TT;
   auto bytes_for = [&](int S) {
-    return SmemLayout(S, 1 << P.n, dual, P.n_rot, P.n_blk, P.n_av, red_slots(p), W, p->M).total;
+    return SmemLayout(S, 1 << P.n, dual, P.n_rot, P.n_blk, P.n_av, red_slots(p), S * TT, p->M).total;
   };
-  int smax = std::max(1, (P.R >= 4 ? 256 : 512) / TPS);
+  const int max_threads = split ? 512 : (P.R >= 4 ? 256 : 512);
+  int smax = std::max(1, max_threads / TT);
   const int64_t want = std::max<int64_t>(1, (B + 2 * p->sms - 1) / (2 * p->sms));
   int S = 1;
   while (S * 2 <= smax && S * 2 <= want && bytes_for(S * 2) <= (size_t)kMaxSmemBytes) S *= 2;
@@ -485,9 +521,8 @@ int smem_samples(const VqcPlan* p, int64_t B, bool dual, size_t* smem_bytes) {
 size_t pass_smem(const VqcPlan* p, bool dual) {
   const HostProgram& P = p->prog;
   const int TPS = 1 << (P.k - P.R);
-  const int W = TPS >= 32 ? TPS / 32 : 1;
   return SmemLayout(1, 1 << P.k, dual, P.max_rot_per_pass, P.max_blk_per_pass, P.max_av_per_pass,
-                    red_slots(p), W, p->M).total;
+                    red_slots(p), dual ? 2 * TPS : TPS, p->M).total;
 }
 
 int launch(const char* name, KFn fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
@@ -536,7 +571,8 @@ int run_core(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, const
   const bool adj = mode != VQC_MODE_FORWARD;
   if (!P.hbm) {
     size_t smem = 0;
-    const int S = smem_samples(p, B, adj, &smem);
+    int TT = 1;
+    const int S = smem_samples(p, B, adj, &smem, &TT);
     A.b0 = 0;
     A.nb = B;
     A.S = S;
@@ -545,9 +581,9 @@ int run_core(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, const
     A.ip = ip;
     A.psi_fin = reinterpret_cast<double2*>(ws + L.fin);
     A.jacobian = mode == VQC_MODE_JACOBIAN;
-    const int TPS = 1 << (P.n - P.R);
-    const dim3 grid((unsigned)((B + S - 1) / S)), block((unsigned)(S * TPS));
-    return launch(adj ? "smem_fwd_adjoint" : "smem_forward", smem_kernel(P.R, adj), grid, block, smem, st, D, A);
+    const dim3 grid((unsigned)((B + S - 1) / S)), block((unsigned)(S * TT));
+    return launch(adj ? "smem_fwd_adjoint" : "smem_forward", smem_kernel(P.R, adj, use_split(P.n, P.R)), grid,
+                  block, smem, st, D, A);
   }
   // HBM passes, chunked over rows
   double2* psi = reinterpret_cast<double2*>(ws + L.psi);
@@ -569,7 +605,7 @@ int run_core(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, const
     A.expect = epart;
     A.ip = ipart;
     A.bra = -1;
-    const dim3 grid((unsigned)L.n_tiles, (unsigned)nb), block((unsigned)TPS);
+    const dim3 grid((unsigned)L.n_tiles, (unsigned)nb), block((unsigned)TPS), block2((unsigned)(2 * TPS));
     int rc;
     for (int pi = 0; pi < NP - 1; ++pi) {
       A.pass = pi;
@@ -583,11 +619,11 @@ int run_core(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, const
       if ((rc = launch("pass_forward", pass_kernel(P.R, false), grid, block, sm1, st, D, A))) return rc;
     } else if (mode == VQC_MODE_VJP) {
       A.flags = first | F_FWD | F_OBSERVE | F_SEED | F_BWD | (NP > 1 ? (F_STORE_PSI | F_STORE_PHI) : 0);
-      if ((rc = launch("pass_adjoint", pass_kernel(P.R, true), grid, block, sm2, st, D, A))) return rc;
+      if ((rc = launch("pass_adjoint", pass_kernel(P.R, true), grid, block2, sm2, st, D, A))) return rc;
       for (int pi = NP - 2; pi >= 0; --pi) {
         A.pass = pi;
         A.flags = F_LOAD_PSI | F_LOAD_PHI | F_BWD | (pi > 0 ? (F_STORE_PSI | F_STORE_PHI) : 0);
-        if ((rc = launch("pass_adjoint", pass_kernel(P.R, true), grid, block, sm2, st, D, A))) return rc;
+        if ((rc = launch("pass_adjoint", pass_kernel(P.R, true), grid, block2, sm2, st, D, A))) return rc;
       }
     } else {
       A.flags = first | F_FWD | F_OBSERVE | F_STORE_FIN;
@@ -596,11 +632,11 @@ int run_core(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, const
         A.bra = m;
         A.pass = NP - 1;
         A.flags = F_LOAD_FIN | F_SEED | F_BWD | (NP > 1 ? (F_STORE_PSI | F_STORE_PHI) : 0);
-        if ((rc = launch("pass_adjoint", pass_kernel(P.R, true), grid, block, sm2, st, D, A))) return rc;
+        if ((rc = launch("pass_adjoint", pass_kernel(P.R, true), grid, block2, sm2, st, D, A))) return rc;
         for (int pi = NP - 2; pi >= 0; --pi) {
           A.pass = pi;
           A.flags = F_LOAD_PSI | F_LOAD_PHI | F_BWD | (pi > 0 ? (F_STORE_PSI | F_STORE_PHI) : 0);
-          if ((rc = launch("pass_adjoint", pass_kernel(P.R, true), grid, block, sm2, st, D, A))) return rc;
+          if ((rc = launch("pass_adjoint", pass_kernel(P.R, true), grid, block2, sm2, st, D, A))) return rc;
         }
       }
     }

@@ -66,11 +66,7 @@ struct RunArgs {
 // shared-memory swizzle: 16-byte element l lives at l ^ fold3(l >> 3), i.e.
 // bank group (p mod 8) = XOR of l's bits grouped by (bit position mod 3).
 // Linear over GF(2), so swz(a ^ b) = swz(a) ^ swz(b).
-__device__ __forceinline__ uint32_t swz(uint32_t l) {
-  const uint32_t x = l >> 3;
-  const uint32_t f = x ^ (x >> 3) ^ (x >> 6) ^ (x >> 9) ^ (x >> 12) ^ (x >> 15) ^ (x >> 18);
-  return l ^ (f & 7u);
-}
+__device__ __forceinline__ uint32_t swz(uint32_t l) { return swz_index(l); }
 
 __host__ __device__ constexpr int ctz_const(int i) { return (i & 1) ? 0 : 1 + ctz_const(i >> 1); }
 
@@ -210,55 +206,95 @@ __device__ __forceinline__ void g_cz(double2 (&a)[1 << R], uint32_t mask, bool c
   }
 }
 
-// Im<phi|P|psi> partial sums over this thread's registers (_kernels.py:266-268)
-template <int R, int S>
-__device__ __forceinline__ double ip_x(const double2 (&p)[1 << R], const double2 (&f)[1 << R]) {
+// ---------------------------------------------------------------------------
+// Im<phi|P|psi> partial sums (_kernels.py:266-268). P(i), F(i) return element
+// i of psi / phi (registers, or the partner thread's copy in shared memory).
+// PART = -1 sums every pair; PART = 0/1 sums the half of the pairs whose
+// balance bit (the lowest register bit other than S) equals PART, so the two
+// threads of a split (psi, phi) pair share the work.
+template <int R, int S, int PART>
+__device__ __forceinline__ constexpr bool take_pair(int i) {
+  if constexpr (PART < 0 || R < 2) {
+    return PART <= 0;
+  } else {
+    constexpr int BB = S == 0 ? 1 : 0;
+    return ((i >> BB) & 1) == PART;
+  }
+}
+
+template <int R, int S, int PART, class P, class F>
+__device__ __forceinline__ double ip_x(P&& p, F&& f) {
   double acc = 0.0;
 #pragma unroll
   for (int i = 0; i < (1 << R); ++i)
-    if (!((i >> S) & 1)) {
+    if (!((i >> S) & 1) && take_pair<R, S, PART>(i)) {
       const int j = i | (1 << S);
-      acc += f[i].x * p[j].y - f[i].y * p[j].x;
-      acc += f[j].x * p[i].y - f[j].y * p[i].x;
+      const double2 f0 = f(i), f1 = f(j), p0 = p(i), p1 = p(j);
+      acc += f0.x * p1.y - f0.y * p1.x;
+      acc += f1.x * p0.y - f1.y * p0.x;
     }
   return acc;
 }
-template <int R, int S>
-__device__ __forceinline__ double ip_y(const double2 (&p)[1 << R], const double2 (&f)[1 << R]) {
+template <int R, int S, int PART, class P, class F>
+__device__ __forceinline__ double ip_y(P&& p, F&& f) {
   double acc = 0.0;
 #pragma unroll
   for (int i = 0; i < (1 << R); ++i)
-    if (!((i >> S) & 1)) {
+    if (!((i >> S) & 1) && take_pair<R, S, PART>(i)) {
       const int j = i | (1 << S);
-      acc -= f[i].x * p[j].x + f[i].y * p[j].y;
-      acc += f[j].x * p[i].x + f[j].y * p[i].y;
+      const double2 f0 = f(i), f1 = f(j), p0 = p(i), p1 = p(j);
+      acc -= f0.x * p1.x + f0.y * p1.y;
+      acc += f1.x * p0.x + f1.y * p0.y;
     }
   return acc;
 }
-template <int R>
-__device__ __forceinline__ double ip_z(const double2 (&p)[1 << R], const double2 (&f)[1 << R],
-                                       uint32_t slot_mask, bool cbit) {
+// Z on a register slot (mask = 1 << slot) or a per-thread constant bit (mask 0)
+template <int R, int PART, class P, class F>
+__device__ __forceinline__ double ip_z(P&& p, F&& f, uint32_t slot_mask, bool cbit) {
   double acc = 0.0;
 #pragma unroll
   for (int i = 0; i < (1 << R); ++i) {
+    if (PART >= 0 && R >= 1 && (i & 1) != PART) continue;
     const bool one = slot_mask ? ((i & slot_mask) != 0) : cbit;
-    const double v = f[i].x * p[i].y - f[i].y * p[i].x;
+    const double2 fi = f(i), pi = p(i);
+    const double v = fi.x * pi.y - fi.y * pi.x;
     acc += one ? -v : v;
   }
   return acc;
 }
+template <int R, int S, int PART, class P, class F>
+__device__ __forceinline__ void ip_xyz(P&& p, F&& f, double& ix, double& iy, double& iz) {
+#pragma unroll
+  for (int i = 0; i < (1 << R); ++i)
+    if (!((i >> S) & 1) && take_pair<R, S, PART>(i)) {
+      const int j = i | (1 << S);
+      const double2 f0 = f(i), f1 = f(j), p0 = p(i), p1 = p(j);
+      ix += f0.x * p1.y - f0.y * p1.x;
+      ix += f1.x * p0.y - f1.y * p0.x;
+      iy -= f0.x * p1.x + f0.y * p1.y;
+      iy += f1.x * p0.x + f1.y * p0.y;
+      iz += f0.x * p0.y - f0.y * p0.x;
+      iz -= f1.x * p1.y - f1.y * p1.x;
+    }
+}
 
 // ---------------------------------------------------------------------------
-// per-sample group reduction (TPS threads per sample, power of two)
+// Threads of one sample. Forward / dual: TPS threads, one register group each.
+// Split adjoint: 2*TPS threads, role 0 holds psi and role 1 phi of group gi.
 struct Group {
   int tid, gi, sl, TPS, S, W;  // W = partials per sample (warps per sample, >= 1)
+  int role = 0, TT = 0;        // TT = threads per sample
   __device__ __forceinline__ double reduce(double v) const {
-    const int width = TPS < 32 ? TPS : 32;
-    for (int off = width >> 1; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    const int width = TT < 32 ? TT : 32;
+    const unsigned mask = blockDim.x >= 32 ? 0xffffffffu : ((1u << blockDim.x) - 1u);
+    for (int off = width >> 1; off > 0; off >>= 1) v += __shfl_xor_sync(mask, v, off);
     return v;
   }
-  __device__ __forceinline__ bool leader() const { return (gi & 31) == 0; }
-  __device__ __forceinline__ int red_index(int slot) const { return (slot * S + sl) * W + (gi >> 5); }
+  __device__ __forceinline__ int lane_in_sample() const { return role * TPS + gi; }
+  __device__ __forceinline__ bool leader() const { return (lane_in_sample() & 31) == 0; }
+  __device__ __forceinline__ int red_index(int slot) const {
+    return (slot * S + sl) * W + (lane_in_sample() >> 5);
+  }
 };
 
 // general 2x2 on slot S: a0' = u00 a0 + u01 a1 ; a1' = u10 a0 + u11 a1
@@ -277,24 +313,6 @@ __device__ __forceinline__ void g_u2(double2 (&a)[1 << R], const double2 u00, co
     }
 }
 
-// the three Pauli inner products Im<phi|P|psi>, P in {X, Y, Z} on slot S
-template <int R, int S>
-__device__ __forceinline__ void ip_xyz(const double2 (&p)[1 << R], const double2 (&f)[1 << R], double& ix,
-                                       double& iy, double& iz) {
-#pragma unroll
-  for (int i = 0; i < (1 << R); ++i)
-    if (!((i >> S) & 1)) {
-      const int j = i | (1 << S);
-      const double2 f0 = f[i], f1 = f[j], p0 = p[i], p1 = p[j];
-      ix += f0.x * p1.y - f0.y * p1.x;
-      ix += f1.x * p0.y - f1.y * p0.x;
-      iy -= f0.x * p1.x + f0.y * p1.y;
-      iy += f1.x * p0.x + f1.y * p0.y;
-      iz += f0.x * p0.y - f0.y * p0.x;
-      iz -= f1.x * p1.y - f1.y * p1.x;
-    }
-}
-
 // fused CZ run (program.h DiagRun): per-register sign from a quadratic form
 template <int R>
 __device__ __forceinline__ void g_czrun(double2 (&a)[1 << R], uint32_t qreg, uint32_t m, uint32_t qc) {
@@ -305,6 +323,21 @@ __device__ __forceinline__ void g_czrun(double2 (&a)[1 << R], uint32_t qreg, uin
   }
 }
 
+// this thread's partial inner product for reduction slot `slot` (reduced over
+// the sample's threads at the end of the segment, in a fixed order)
+__device__ __forceinline__ void put_partial(double* redbuf, int slot, double v) {
+  redbuf[slot * blockDim.x + threadIdx.x] = v;
+}
+
+// compile-time slot from an unrolled loop index (no branch after unrolling)
+template <int R, typename F>
+__device__ __forceinline__ void with_const_slot(int s, F&& f) {
+  if (s == 0) f(std::integral_constant<int, 0>{});
+  if constexpr (R > 1) if (s == 1) f(std::integral_constant<int, 1>{});
+  if constexpr (R > 2) if (s == 2) f(std::integral_constant<int, 2>{});
+  if constexpr (R > 3) if (s == 3) f(std::integral_constant<int, 3>{});
+}
+
 // per-sample parameter tables in shared memory
 struct SampleTables {
   const double2* cs;  // (cos, sin) of theta/2 per rotation (relative to rot_base)
@@ -312,12 +345,51 @@ struct SampleTables {
   int rot_base, blk_base;
 };
 
-template <int R, bool DUAL>
+enum { MODE_FWD = 0, MODE_DUAL = 1, MODE_SPLIT = 2 };
+
+// Register-tile context of the current segment: the state registers live in
+// a[] (and f[] in dual mode); in split mode the partner's copy of element i
+// is in shared memory at addr(i) (the segment's load map).
+template <int R>
+struct SegCtx {
+  uint32_t J0;
+  uint32_t lp0;
+  uint32_t lc[R];
+  double2* own;
+  const double2* partner;
+  __device__ __forceinline__ uint32_t addr(int i) const {
+    uint32_t ad = lp0;
+#pragma unroll
+    for (int s = 0; s < R; ++s)
+      if ((i >> s) & 1) ad ^= lc[s];
+    return ad;
+  }
+};
+
+// Run one inner-product op: dual reads both register sets; split computes
+// half of the pairs from its own registers and the partner's shared copy.
+template <int R, int MODE, class K>
+__device__ __forceinline__ void ip_dispatch(const SegCtx<R>& C, const double2 (&a)[1 << R],
+                                            const double2 (&f)[1 << R], int role, K&& kernel) {
+  auto ra = [&](int i) { return a[i]; };
+  if constexpr (MODE == MODE_DUAL) {
+    auto rf = [&](int i) { return f[i]; };
+    kernel(std::integral_constant<int, -1>{}, ra, rf);
+  } else {
+    auto sm = [&](int i) { return C.partner[C.addr(i)]; };
+    if (role == 0) kernel(std::integral_constant<int, 0>{}, ra, sm);
+    else kernel(std::integral_constant<int, 1>{}, sm, ra);
+  }
+}
+
+template <int R, int MODE>
 __device__ __forceinline__ void exec_op(const DevProgram& D, const Op op, double2 (&a)[1 << R],
-                                        double2 (&f)[1 << R], uint32_t J0, const SampleTables& T,
-                                        double* s_redbuf, const Group& grp) {
+                                        double2 (&f)[1 << R], const SegCtx<R>& C, int role,
+                                        const SampleTables& T, double* s_redbuf) {
+  constexpr bool DUAL = MODE == MODE_DUAL;
   const uint32_t w0 = op.w0;
   const uint32_t A = op_a(w0), Bq = op_b(w0);
+  const uint32_t J0 = C.J0;
   switch (op_code(w0)) {
     case OP_RX: {
       const double2 cs = T.cs[(int)op.param - T.rot_base];
@@ -358,12 +430,33 @@ __device__ __forceinline__ void exec_op(const DevProgram& D, const Op op, double
         if constexpr (DUAL) g_u2<R, SL.value>(f, u00, u01, u10, u11);
       });
     } break;
+    case OP_U2SET: {
+      const bool adj = op_adj(w0);
+#pragma unroll
+      for (int sl = 0; sl < R; ++sl) {
+        const uint32_t id = (op.param >> (8 * sl)) & 0xFFu;
+        if (id == kNoBlock) continue;
+        const double2* u = T.u + 4 * id;
+        double2 u00 = u[0], u01 = u[1], u10 = u[2], u11 = u[3];
+        if (adj) {
+          const double2 t = u01;
+          u00.y = -u00.y;
+          u11.y = -u11.y;
+          u01 = make_double2(u10.x, -u10.y);
+          u10 = make_double2(t.x, -t.y);
+        }
+        with_const_slot<R>(sl, [&](auto SL) {
+          g_u2<R, SL.value>(a, u00, u01, u10, u11);
+          if constexpr (DUAL) g_u2<R, SL.value>(f, u00, u01, u10, u11);
+        });
+      }
+    } break;
     case OP_CNOT: {
       if (A & kSlotFlag) {
-        with_slot<R>(A & 7u, [&](auto C) {
+        with_slot<R>(A & 7u, [&](auto Cc) {
           with_slot<R>(Bq & 7u, [&](auto Tt) {
-            g_cnot_rr<R, C.value, Tt.value>(a);
-            if constexpr (DUAL) g_cnot_rr<R, C.value, Tt.value>(f);
+            g_cnot_rr<R, Cc.value, Tt.value>(a);
+            if constexpr (DUAL) g_cnot_rr<R, Cc.value, Tt.value>(f);
           });
         });
       } else {
@@ -404,101 +497,182 @@ __device__ __forceinline__ void exec_op(const DevProgram& D, const Op op, double
       g_czrun<R>(a, qreg, m, qc);
       if constexpr (DUAL) g_czrun<R>(f, qreg, m, qc);
     } break;
+    case OP_PUBLISH:
+      if constexpr (MODE == MODE_SPLIT) {
+        __syncthreads();  // partners finished reading the previous copy
+#pragma unroll
+        for (int i = 0; i < (1 << R); ++i) C.own[C.addr(i)] = a[i];
+        __syncthreads();
+      }
+      break;
     case OP_IP3:
-      if constexpr (DUAL) {
+      if constexpr (MODE != MODE_FWD) {
         double ix = 0.0, iy = 0.0, iz = 0.0;
-        with_slot<R>(A & 7u, [&](auto SL) { ip_xyz<R, SL.value>(a, f, ix, iy, iz); });
-        ix = grp.reduce(ix);
-        iy = grp.reduce(iy);
-        iz = grp.reduce(iz);
-        if (grp.leader()) {
-          const int r0 = (int)op_ip(w0);
-          s_redbuf[grp.red_index(r0)] = ix;
-          s_redbuf[grp.red_index(r0 + 1)] = iy;
-          s_redbuf[grp.red_index(r0 + 2)] = iz;
+        with_slot<R>(A & 7u, [&](auto SL) {
+          ip_dispatch<R, MODE>(C, a, f, role, [&](auto PART, auto&& p, auto&& q) {
+            ip_xyz<R, SL.value, PART.value>(p, q, ix, iy, iz);
+          });
+        });
+        const int r0 = (int)op_ip(w0);
+        put_partial(s_redbuf, r0, ix);
+        put_partial(s_redbuf, r0 + 1, iy);
+        put_partial(s_redbuf, r0 + 2, iz);
+      }
+      break;
+    case OP_IP3SET:
+      if constexpr (MODE != MODE_FWD) {
+        const uint32_t mask = Bq;
+        int r0 = (int)op_ip(w0);
+#pragma unroll
+        for (int sl = 0; sl < R; ++sl) {
+          if (!((mask >> sl) & 1u)) continue;
+          double ix = 0.0, iy = 0.0, iz = 0.0;
+          with_const_slot<R>(sl, [&](auto SL) {
+            ip_dispatch<R, MODE>(C, a, f, role, [&](auto PART, auto&& p, auto&& q) {
+              ip_xyz<R, SL.value, PART.value>(p, q, ix, iy, iz);
+            });
+          });
+          put_partial(s_redbuf, r0, ix);
+          put_partial(s_redbuf, r0 + 1, iy);
+          put_partial(s_redbuf, r0 + 2, iz);
+          r0 += 3;
         }
       }
       break;
     default:
-      if constexpr (DUAL) {
+      if constexpr (MODE != MODE_FWD) {
         double v = 0.0;
         const uint32_t code = op_code(w0);
         if (code == OP_IPX) {
-          with_slot<R>(A & 7u, [&](auto SL) { v = ip_x<R, SL.value>(a, f); });
+          with_slot<R>(A & 7u, [&](auto SL) {
+            ip_dispatch<R, MODE>(C, a, f, role, [&](auto PART, auto&& p, auto&& q) {
+              v = ip_x<R, SL.value, PART.value>(p, q);
+            });
+          });
         } else if (code == OP_IPY) {
-          with_slot<R>(A & 7u, [&](auto SL) { v = ip_y<R, SL.value>(a, f); });
+          with_slot<R>(A & 7u, [&](auto SL) {
+            ip_dispatch<R, MODE>(C, a, f, role, [&](auto PART, auto&& p, auto&& q) {
+              v = ip_y<R, SL.value, PART.value>(p, q);
+            });
+          });
         } else {
           const uint32_t m = (A & kSlotFlag) ? (1u << (A & 7u)) : 0u;
           const bool cb = (A & kSlotFlag) ? false : ((J0 >> A) & 1u);
-          v = ip_z<R>(a, f, m, cb);
+          ip_dispatch<R, MODE>(C, a, f, role, [&](auto PART, auto&& p, auto&& q) {
+            v = ip_z<R, PART.value>(p, q, m, cb);
+          });
         }
-        v = grp.reduce(v);
-        if (grp.leader()) s_redbuf[grp.red_index((int)op_ip(w0))] = v;
+        put_partial(s_redbuf, (int)op_ip(w0), v);
       }
       break;
   }
 }
 
-// Run segments [sb, se) on the tile(s) in shared memory. s_psi / s_phi point at
-// this thread's sample block; T / s_av are this thread's sample tables.
-// Gradient outputs go to A.ip (rows relative to A.b0, times n_tiles).
-template <int R, bool DUAL>
+// Run segments [sb, se) on the tile(s) in shared memory. MODE_FWD: psi only;
+// MODE_DUAL: each thread holds psi and phi of its register group; MODE_SPLIT:
+// role-0 threads hold psi, role-1 threads phi. s_psi / s_phi point at this
+// thread's sample block; T / s_av are this thread's sample tables. Gradient
+// outputs go to A.ip (rows relative to A.b0, times n_tiles). Threads with
+// active == false only take part in the barriers.
+template <int R, int MODE>
 __device__ __forceinline__ void run_segments(const DevProgram& D, const RunArgs& A, int sb, int se,
                                              double2* s_psi, double2* s_phi, const SampleTables& T,
                                              const double* s_av_all, int av_stride, int av_base,
-                                             double* s_red, int& red_buf, const Group& grp,
+                                             double* s_red, const Group& grp, bool active,
                                              uint32_t tile_base, int64_t bl0, int bra, int tile,
                                              int n_tiles) {
   constexpr int N = 1 << R;
-  const int red_stride = A.red_slots * grp.S * grp.W;
+  constexpr bool DUAL = MODE == MODE_DUAL;
+  double2* own = (MODE == MODE_SPLIT && grp.role) ? s_phi : s_psi;
+  const double2* partner = (MODE == MODE_SPLIT && grp.role) ? s_psi : s_phi;
   for (int sg = sb; sg < se; ++sg) {
     const SegDesc* sd = D.segs + sg;
     const int nthr = sd->nthr;
-    uint32_t L0 = 0, J0 = tile_base;
+    SegCtx<R> C;
+    C.own = own;
+    C.partner = partner;
+    uint32_t p0 = 0;
+    C.J0 = tile_base;
     for (int i = 0; i < nthr; ++i)
       if ((grp.gi >> i) & 1) {
-        L0 |= 1u << sd->thr_l[i];
-        J0 |= 1u << sd->thr_g[i];
+        p0 ^= sd->tsw[i];
+        C.J0 |= 1u << sd->thr_g[i];
       }
-    uint32_t ps[R];
+    // folded CNOT runs: register bit s loads from / stores to column col[s],
+    // translated by the J0-controlled slots (program.h SegDesc)
+    C.lp0 = p0;
 #pragma unroll
-    for (int s = 0; s < R; ++s) ps[s] = swz(1u << sd->reg_l[s]);
-    const uint32_t p0 = swz(L0);
+    for (int t = 0; t < R; ++t) {
+      if (__popc(C.J0 & sd->ld_k[t]) & 1) C.lp0 ^= sd->ps[t];
+      C.lc[t] = sd->ldc[t];
+    }
     double2 a[N], f[N];
+    if (active) {
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
-      uint32_t ad = p0;
-#pragma unroll
-      for (int s = 0; s < R; ++s)
-        if ((i >> s) & 1) ad ^= ps[s];
-      a[i] = s_psi[ad];
-      if constexpr (DUAL) f[i] = s_phi[ad];
+      for (int i = 0; i < N; ++i) {
+        const uint32_t ad = C.addr(i);
+        a[i] = own[ad];
+        if constexpr (DUAL) f[i] = s_phi[ad];
+      }
     }
-    double* redbuf = s_red + red_buf * red_stride;
     const int ob = sd->op_begin, oe = sd->op_end;
-    if (ob < oe) {
-      for (int o = ob; o < oe; ++o) exec_op<R, DUAL>(D, D.ops[o], a, f, J0, T, redbuf, grp);
+    Op nxt = ob < oe ? D.ops[ob] : Op{0u, 0u};
+    for (int o = ob; o < oe; ++o) {
+      const Op op = nxt;
+      if (o + 1 < oe) nxt = D.ops[o + 1];
+      if (MODE == MODE_SPLIT && op_code(op.w0) == OP_PUBLISH) {
+        __syncthreads();
+        if (active) {
+#pragma unroll
+          for (int i = 0; i < N; ++i) own[C.addr(i)] = a[i];
+        }
+        __syncthreads();
+        continue;
+      }
+      if (active) exec_op<R, MODE>(D, op, a, f, C, grp.role, T, s_red);
     }
+    if (MODE == MODE_SPLIT && sd->ip_count > 0) __syncthreads();  // partners done reading
+    if (active) {
+      uint32_t sp0 = p0, sc[R];
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
-      uint32_t ad = p0;
+      for (int t = 0; t < R; ++t) {
+        if (__popc(C.J0 & sd->st_k[t]) & 1) sp0 ^= sd->ps[t];
+        sc[t] = sd->stc[t];
+      }
 #pragma unroll
-      for (int s = 0; s < R; ++s)
-        if ((i >> s) & 1) ad ^= ps[s];
-      s_psi[ad] = a[i];
-      if constexpr (DUAL) s_phi[ad] = f[i];
+      for (int i = 0; i < N; ++i) {
+        uint32_t ad = sp0;
+#pragma unroll
+        for (int s = 0; s < R; ++s)
+          if ((i >> s) & 1) ad ^= sc[s];
+        own[ad] = a[i];
+        if constexpr (DUAL) s_phi[ad] = f[i];
+      }
     }
     __syncthreads();
-    if constexpr (DUAL) {
+    if constexpr (MODE != MODE_FWD) {
       const int nout = sd->ip_count;
       if (nout > 0) {
+        // one warp per (output, sample): fixed-order sum of the sample's
+        // per-thread partials, then the block's gradient vector if fused.
+        // Blocks narrower than a warp (tiny n) finalise serially on thread 0.
+        const bool narrow = blockDim.x < 32;
+        const int lane = narrow ? 0 : (threadIdx.x & 31);
+        const int warp = narrow ? (threadIdx.x == 0 ? 0 : 1 << 30) : (threadIdx.x >> 5);
+        const int nwarp = narrow ? 1 : (blockDim.x >> 5);
         const int total = nout * grp.S;
-        for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-          const int oi = idx / grp.S, s_ = idx - oi * grp.S;
+        for (int task = warp; task < total; task += nwarp) {
+          const int oi = task / grp.S, s_ = task - oi * grp.S;
           const IpOut io = D.ipouts[sd->ip_begin + oi];
+          const double* base = s_red + s_ * grp.TT;
           auto red = [&](int slot) {
             double v = 0.0;
-            for (int w = 0; w < grp.W; ++w) v += redbuf[(slot * grp.S + s_) * grp.W + w];
+            if (narrow) {
+              for (int t = 0; t < grp.TT; ++t) v += base[slot * (int)blockDim.x + t];
+              return v;
+            }
+            for (int t = lane; t < grp.TT; t += 32) v += base[slot * (int)blockDim.x + t];
+            for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
             return v;
           };
           double v;
@@ -506,12 +680,13 @@ __device__ __forceinline__ void run_segments(const DevProgram& D, const RunArgs&
             v = red(io.red);
           } else {
             const double* av = s_av_all + (size_t)s_ * av_stride + 4 * (io.avec - av_base);
-            v = av[0] * red(io.red) + av[1] * red(io.red + 1) + av[2] * red(io.red + 2);
+            const double r0 = red(io.red), r1 = red(io.red + 1), r2 = red(io.red + 2);
+            v = av[0] * r0 + av[1] * r1 + av[2] * r2;
           }
           const int64_t bl = bl0 + s_;
-          if (bl < A.nb) A.ip[(((bl * A.K) + bra) * D.NG + io.gslot) * n_tiles + tile] = v;
+          if (lane == 0 && bl < A.nb) A.ip[(((bl * A.K) + bra) * D.NG + io.gslot) * n_tiles + tile] = v;
         }
-        red_buf ^= 1;
+        __syncthreads();  // the reduction buffer is reused by the next segment
       }
     }
   }
@@ -554,8 +729,8 @@ __device__ __forceinline__ void build_tables(const DevProgram& D, const RunArgs&
 // XOR per element.
 struct TileWalk {
   uint32_t base;
-  uint32_t hi[kMaxQubits];
-  int count;
+  uint32_t hi[kMaxR];
+  int count;  // elements per thread: 2^k / stride = 2^R <= 16
 };
 
 __device__ __forceinline__ uint32_t dep_local(const PassDesc& pd, uint32_t l, int k) {
@@ -570,8 +745,11 @@ __device__ __forceinline__ TileWalk tile_walk(const PassDesc* pd, uint32_t tile_
   const int Nt = 1 << k;
   w.count = Nt / stride;
   w.base = tile_base | (pd ? dep_local(*pd, (uint32_t)lane, k) : (uint32_t)lane);
-  int b = 0;
-  for (int s = stride; s < Nt; s <<= 1, ++b) w.hi[b] = pd ? dep_local(*pd, (uint32_t)s, k) : (uint32_t)s;
+#pragma unroll
+  for (int b = 0; b < kMaxR; ++b) {
+    const uint32_t s = (uint32_t)stride << b;
+    w.hi[b] = s < (uint32_t)Nt ? (pd ? dep_local(*pd, s, k) : s) : 0u;
+  }
   return w;
 }
 
@@ -579,8 +757,10 @@ __device__ __forceinline__ TileWalk tile_walk(const PassDesc* pd, uint32_t tile_
 template <class F>
 __device__ __forceinline__ void for_tile(const TileWalk& w, int lane, int stride, F&& f) {
   uint32_t j = w.base;
-  for (int i = 0; i < w.count; ++i) {
-    if (i) j ^= w.hi[__ffs(i) - 1];
+#pragma unroll
+  for (int i = 0; i < (1 << kMaxR); ++i) {
+    if (i >= w.count) break;
+    if (i) j ^= w.hi[ctz_const(i)];
     const uint32_t g = (uint32_t)(i ^ (i >> 1));
     f((uint32_t)lane + g * (uint32_t)stride, j);
   }

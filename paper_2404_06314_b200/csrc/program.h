@@ -39,7 +39,13 @@ enum OpCode : uint32_t {
   OP_U2 = 10,     // fused run of 1q gates on a register slot: param = block id
   OP_IP3 = 11,    // Im<phi|X|psi>, Im<phi|Y|psi>, Im<phi|Z|psi> on a slot (3 red slots)
   OP_CZRUN = 12,  // fused run of CZ gates: param = diagonal-run id
+  OP_U2SET = 13,  // fused blocks on several slots: param = 8-bit block id (relative to the
+                  // pass) per slot, 0xFF = none
+  OP_IP3SET = 14, // IP3 on the slots in operand b's mask; 3 reduction slots each from op_ip
+  OP_PUBLISH = 15, // split adjoint: write this thread's registers back to shared memory so
+                   // the partner thread (other state) can read them for inner products
 };
+constexpr uint32_t kNoBlock = 0xFFu;
 
 // operand field (6 bits): bit 5 set -> register slot (low 3 bits), else a
 // global qubit number whose bit is constant per thread.
@@ -51,6 +57,15 @@ struct Op {
   uint32_t w0;
   uint32_t param;  // rotation id / block id / run id
 };
+
+// shared-memory swizzle of 16-byte tile element l: l ^ fold3(l >> 3); the
+// bank group (p mod 8) is the XOR of l's bits grouped by position mod 3, and
+// the map is GF(2)-linear (swz(a ^ b) = swz(a) ^ swz(b)).
+VQC_HD inline uint32_t swz_index(uint32_t l) {
+  const uint32_t x = l >> 3;
+  const uint32_t f = x ^ (x >> 3) ^ (x >> 6) ^ (x >> 9) ^ (x >> 12) ^ (x >> 15) ^ (x >> 18);
+  return l ^ (f & 7u);
+}
 
 VQC_HD inline uint32_t op_code(uint32_t w0) { return w0 & 31u; }
 VQC_HD inline uint32_t op_a(uint32_t w0) { return (w0 >> 5) & 63u; }
@@ -71,6 +86,16 @@ struct SegDesc {
   int32_t op_begin, op_end;
   int32_t ip_begin, ip_count;  // IpOut entries of this segment
   int32_t red_count;           // reduction slots used
+  // Leading / trailing CNOT runs folded into the shared-memory address maps:
+  // register index bit s is stored at / loaded from the tile position whose
+  // register bits are col[s] (an R-bit mask over slots) translated by the
+  // slots t with parity(J0 & k[t]) = 1 (CNOTs controlled by thread/tile bits).
+  uint8_t ld_col[kMaxR], st_col[kMaxR];
+  uint32_t ld_k[kMaxR], st_k[kMaxR];
+  // precomputed swizzled tile addresses (swz_index): ps[s] of register bit s,
+  // ldc/stc[s] of the folded load/store columns, tsw[i] of thread bit i
+  uint16_t ps[kMaxR], ldc[kMaxR], stc[kMaxR];
+  uint16_t tsw[kMaxQubits];
   int8_t nreg, nthr, pad0, pad1;
   int8_t reg_l[kMaxR];         // tile-local bit position of each register slot
   int8_t reg_g[kMaxR];         // global qubit of each register slot

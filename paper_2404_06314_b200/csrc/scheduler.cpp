@@ -25,6 +25,7 @@ struct GateInfo {
   int act[2] = {0, 0};
   uint32_t mix = 0;  // qubits that must be local (tile) / a register slot (segment)
   bool rot = false;
+  bool cnot = false;
   bool need_grad = false;
   std::vector<int> preds;
 };
@@ -67,6 +68,7 @@ std::string analyze(const std::vector<GateIn>& gates, int n, int64_t total_param
         inf.nq = 2; inf.q[0] = gi.q0; inf.q[1] = gi.q1;
         inf.act[0] = A_Z; inf.act[1] = gi.kind == G_CNOT ? A_X : A_Z;
         inf.mix = gi.kind == G_CNOT ? (1u << gi.q1) : 0u;
+        inf.cnot = gi.kind == G_CNOT;
         break;
       default:
         snprintf(buf, sizeof buf, "gate %d: unknown gate kind %d", g, gi.kind); return buf;
@@ -107,23 +109,31 @@ std::string analyze(const std::vector<GateIn>& gates, int n, int64_t total_param
 // Greedy partition of `todo` (a topological order) into groups whose mixing
 // qubits fit `cap` local qubits (always including `forced`). status: 0 pending,
 // 1 done; gates outside `todo` must be marked done.
+// fold_cnots (register segments): keep each group of the form
+// [CNOTs][body][CNOTs] so both CNOT runs fold into the segment's shared-memory
+// address maps instead of costing register permutations.
 std::vector<Group> greedy_groups(const std::vector<int>& todo, const std::vector<GateInfo>& info,
-                                 int cap, uint32_t forced, std::vector<uint8_t>& status) {
+                                 int cap, uint32_t forced, std::vector<uint8_t>& status,
+                                 bool fold_cnots = false) {
   std::vector<Group> groups;
   std::vector<int> remaining = todo;
   while (!remaining.empty()) {
     Group grp;
     grp.mask = forced;
+    int phase = 0;  // 0 leading CNOTs, 1 body, 2 trailing CNOTs
     for (int g : remaining) {
       bool ok = true;
       for (int p : info[g].preds)
         if (status[p] != 1 && status[p] != 2) { ok = false; break; }
+      if (ok && fold_cnots && phase == 2 && !info[g].cnot) ok = false;
       if (ok) {
         const uint32_t m = grp.mask | info[g].mix;
         if (popc(m) <= cap) {
           grp.mask = m;
           status[g] = 2;
           grp.gates.push_back(g);
+          if (!info[g].cnot) phase = 1;
+          else if (phase == 1) phase = 2;
         } else {
           ok = false;
         }
@@ -210,13 +220,14 @@ std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total
     // ---- level 2: register segments inside the tile ----
     std::vector<uint8_t> st2(G, 1);
     for (int g : pg.gates) st2[g] = 0;
-    std::vector<Group> segs = greedy_groups(pg.gates, info, R, 0u, st2);
+    std::vector<Group> segs = greedy_groups(pg.gates, info, R, 0u, st2, true);
     if (!pg.gates.empty() && segs.empty()) return "segment scheduling failed";
 
     struct Item {
-      int type;               // 0 single gate, 1 block (1q run on a slot), 2 CZ run
+      int type;               // 0 single gate, 1 block (1q run on a slot), 2 CZ run, 3 block set
       std::vector<int> gates;
-      int id = -1;            // block id / diag-run id
+      int id = -1;            // block id / diag-run id / packed set ids
+      std::vector<Item> sub;  // blocks of a set
     };
     pd.seg_begin = (int)P->segs.size();
     std::vector<SegDesc> fwd_descs;
@@ -252,7 +263,9 @@ std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total
       for (size_t i = 0; i < order.size(); ++i) {
         sd.thr_l[i] = (int8_t)order[i];
         sd.thr_g[i] = pd.local_q[order[i]];
+        sd.tsw[i] = (uint16_t)swz_index(1u << order[i]);
       }
+      for (int s2 = 0; s2 < ns; ++s2) sd.ps[s2] = (uint16_t)swz_index(1u << sd.reg_l[s2]);
       auto operand = [&](int q) -> uint32_t {
         return slot_of[q] >= 0 ? (kSlotFlag | (uint32_t)slot_of[q]) : (uint32_t)q;
       };
@@ -292,57 +305,138 @@ std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total
         if (gi.kind == G_CNOT) open_blk[gi.q0] = open_blk[gi.q1] = -1;
         items.push_back({0, {g}});
       }
-
-      sd.op_begin = (int)P->ops.size();
-      for (Item& it : items) {
-        const int g0 = it.gates[0];
-        const GateIn& gi0 = gates[g0];
+      for (const Item& it : items)
         for (int g : it.gates)
           if ((info[g].mix & sgp.mask) != info[g].mix) return "internal: mixing qubit not in registers";
-        if (it.type == 1) {
-          for (int g : it.gates)
-            if (gates[g].kind <= G_RZ) {
-              rot_id[g] = next_rot++;
-              if (info[g].need_grad) gslot[g] = next_g++;
-            }
+
+      // leading / trailing CNOT runs fold into the load / store address maps
+      auto is_cnot = [&](const Item& it) { return it.type == 0 && gates[it.gates[0]].kind == G_CNOT; };
+      size_t lead = 0;
+      while (lead < items.size() && is_cnot(items[lead])) ++lead;
+      size_t trail = items.size();
+      while (trail > lead && is_cnot(items[trail - 1])) --trail;
+      // affine map of a CNOT sequence, restricted to register bits: register
+      // output bit t = XOR of register inputs col-masks + const qubits kmask
+      auto fold = [&](const std::vector<int>& cnots, uint8_t* col, uint32_t* kmask) {
+        uint32_t row[kMaxQubits];  // row[q]: global-bit mask feeding output bit q
+        for (int q = 0; q < n; ++q) row[q] = 1u << q;
+        for (int g : cnots) row[gates[g].q1] ^= row[gates[g].q0];
+        uint32_t regmask = 0;
+        for (int s2 = 0; s2 < ns; ++s2) regmask |= 1u << sd.reg_g[s2];
+        for (int s2 = 0; s2 < kMaxR; ++s2) { col[s2] = 0; kmask[s2] = 0; }
+        for (int t = 0; t < ns; ++t) {
+          const uint32_t r = row[(int)sd.reg_g[t]];
+          kmask[t] = r & ~regmask;
+          for (int s2 = 0; s2 < ns; ++s2)
+            if (r >> sd.reg_g[s2] & 1u) col[s2] |= (uint8_t)(1u << t);
         }
-        Op op{};
-        if (it.type == 1 && it.gates.size() > 1) {
-          it.id = (int)P->blocks.size();
-          BlockDesc bd{};
-          bd.mem_begin = (int)P->members.size();
-          for (int g : it.gates) {
-            MemberDesc md{};
-            md.kind = gates[g].kind;
-            md.rot = rot_id[g];
-            md.avec = (gates[g].kind <= G_RZ && info[g].need_grad) ? P->n_av++ : -1;
-            P->members.push_back(md);
+      };
+      std::vector<int> lead_g, trail_g;
+      for (size_t i = 0; i < lead; ++i) lead_g.push_back(items[i].gates[0]);
+      for (size_t i = trail; i < items.size(); ++i) trail_g.push_back(items[i].gates[0]);
+      {
+        // loads see C_lead^{-1} (the lead CNOTs in reverse order); stores C_trail
+        std::vector<int> inv(lead_g.rbegin(), lead_g.rend());
+        fold(inv, sd.ld_col, sd.ld_k);
+        fold(trail_g, sd.st_col, sd.st_k);
+        for (int s2 = 0; s2 < kMaxR; ++s2) {
+          uint32_t lcv = 0, scv = 0;
+          for (int t = 0; t < ns; ++t) {
+            if (sd.ld_col[s2] >> t & 1u) lcv ^= sd.ps[t];
+            if (sd.st_col[s2] >> t & 1u) scv ^= sd.ps[t];
           }
-          bd.mem_end = (int)P->members.size();
-          P->blocks.push_back(bd);
+          sd.ldc[s2] = (uint16_t)lcv;
+          sd.stc[s2] = (uint16_t)scv;
+        }
+      }
+      std::vector<Item> body(items.begin() + lead, items.begin() + trail);
+      // consecutive fused blocks (distinct slots, commuting) dispatch as one set
+      std::vector<Item> grouped;
+      for (size_t i = 0; i < body.size();) {
+        if (body[i].type == 1) {
+          size_t j = i;
+          while (j < body.size() && body[j].type == 1) ++j;
+          if (j - i >= 2) {
+            Item set{3, {}};
+            set.sub.assign(body.begin() + i, body.begin() + j);
+            grouped.push_back(std::move(set));
+            i = j;
+            continue;
+          }
+        }
+        grouped.push_back(body[i]);
+        ++i;
+      }
+
+      auto new_block = [&](const Item& it) {
+        for (int g : it.gates)
+          if (gates[g].kind <= G_RZ) {
+            rot_id[g] = next_rot++;
+            if (info[g].need_grad) gslot[g] = next_g++;
+          }
+        BlockDesc bd{};
+        bd.mem_begin = (int)P->members.size();
+        for (int g : it.gates) {
+          MemberDesc md{};
+          md.kind = gates[g].kind;
+          md.rot = rot_id[g];
+          md.avec = (gates[g].kind <= G_RZ && info[g].need_grad) ? P->n_av++ : -1;
+          P->members.push_back(md);
+        }
+        bd.mem_end = (int)P->members.size();
+        P->blocks.push_back(bd);
+        return (int)P->blocks.size() - 1;
+      };
+
+      sd.op_begin = (int)P->ops.size();
+      for (Item& it : grouped) {
+        Op op{};
+        if (it.type == 3) {
+          uint32_t ids = 0xFFFFFFFFu;
+          bool fits = true;
+          for (Item& sub : it.sub) {
+            sub.id = new_block(sub);
+            const int rel = sub.id - pd.blk_begin;
+            if (rel >= (int)kNoBlock) fits = false;
+            const int slot = slot_of[gates[sub.gates[0]].q0];
+            ids = (ids & ~(0xFFu << (8 * slot))) | ((uint32_t)(rel & 0xFF) << (8 * slot));
+          }
+          if (!fits) return "too many fused blocks in one pass";
+          it.id = (int)ids;
+          op.w0 = enc(OP_U2SET, 0, 0, 0, false);
+          op.param = ids;
+          P->ops.push_back(op);
+          continue;
+        }
+        const int g0 = it.gates[0];
+        const GateIn& gi0 = gates[g0];
+        if (it.type == 1 && it.gates.size() > 1) {
+          it.id = new_block(it);
           op.w0 = enc(OP_U2, operand(gi0.q0), 0, 0, false);
           op.param = (uint32_t)it.id;
         } else if (it.type == 2 && it.gates.size() > 1) {
           it.id = (int)P->diag.size();
           DiagRun dr{};
           for (int g : it.gates) {
-            const int a = gates[g].q0, b = gates[g].q1;
-            const int sa = slot_of[a], sb = slot_of[b];
+            const int qa = gates[g].q0, qb = gates[g].q1;
+            const int sa = slot_of[qa], sb = slot_of[qb];
             if (sa >= 0 && sb >= 0) {
               for (int r = 0; r < (1 << R); ++r)
                 if ((r >> sa & 1) && (r >> sb & 1)) dr.qreg ^= 1u << r;
             } else if (sa >= 0) {
-              dr.part[sa] ^= 1u << b;
+              dr.part[sa] ^= 1u << qb;
             } else if (sb >= 0) {
-              dr.part[sb] ^= 1u << a;
+              dr.part[sb] ^= 1u << qa;
             } else {
-              dr.upper[std::min(a, b)] ^= 1u << std::max(a, b);
+              dr.upper[std::min(qa, qb)] ^= 1u << std::max(qa, qb);
             }
           }
           P->diag.push_back(dr);
           op.w0 = enc(OP_CZRUN, 0, 0, 0, false);
           op.param = (uint32_t)it.id;
         } else if (gi0.kind <= G_RZ) {
+          rot_id[g0] = next_rot++;
+          if (info[g0].need_grad) gslot[g0] = next_g++;
           op.w0 = enc(gi0.kind, operand(gi0.q0), 0, 0, false);
           op.param = (uint32_t)rot_id[g0];
         } else if (gi0.kind == G_H || gi0.kind == G_X) {
@@ -350,17 +444,12 @@ std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total
         } else {
           op.w0 = enc(gi0.kind, operand(gi0.q0), operand(gi0.q1), 0, false);
         }
-        if (it.type == 0 && gi0.kind <= G_RZ) {  // RZ on a non-register qubit
-          rot_id[g0] = next_rot++;
-          if (info[g0].need_grad) gslot[g0] = next_g++;
-          op.param = (uint32_t)rot_id[g0];
-        }
         P->ops.push_back(op);
       }
       sd.op_end = (int)P->ops.size();
       P->segs.push_back(sd);
       fwd_descs.push_back(sd);
-      fwd_items.push_back(std::move(items));
+      fwd_items.push_back(std::move(grouped));
     }
     pd.seg_end = (int)P->segs.size();
     pd.rot_end = next_rot;
@@ -370,42 +459,87 @@ std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total
     P->max_blk_per_pass = std::max(P->max_blk_per_pass, pd.blk_end - pd.blk_begin);
     P->max_av_per_pass = std::max(P->max_av_per_pass, pd.av_end - pd.av_begin);
 
-    // adjoint segments: forward segments reversed, items reversed; gradient
-    // inner products before each un-apply
+    // adjoint segments: forward segments reversed (load/store maps swapped),
+    // items reversed; gradient inner products before each un-apply
     pd.bseg_begin = (int)P->segs.size();
     for (int si = (int)fwd_descs.size() - 1; si >= 0; --si) {
       SegDesc sd = fwd_descs[si];
+      for (int s2 = 0; s2 < kMaxR; ++s2) {
+        std::swap(sd.ld_col[s2], sd.st_col[s2]);
+        std::swap(sd.ld_k[s2], sd.st_k[s2]);
+        std::swap(sd.ldc[s2], sd.stc[s2]);
+      }
       int slot_of[kMaxQubits];
       for (int q = 0; q < kMaxQubits; ++q) slot_of[q] = -1;
-      for (int s = 0; s < sd.nreg; ++s) slot_of[(int)sd.reg_g[s]] = s;
+      for (int s2 = 0; s2 < sd.nreg; ++s2) slot_of[(int)sd.reg_g[s2]] = s2;
       auto operand = [&](int q) -> uint32_t {
         return slot_of[q] >= 0 ? (kSlotFlag | (uint32_t)slot_of[q]) : (uint32_t)q;
       };
       sd.op_begin = (int)P->ops.size();
       sd.ip_begin = (int)P->ipouts.size();
       int nred = 0, nout = 0;
+      auto block_outputs = [&](const Item& it, int red0) {
+        const BlockDesc& bd = P->blocks[it.id];
+        for (int mi = bd.mem_begin; mi < bd.mem_end; ++mi) {
+          const MemberDesc& md = P->members[mi];
+          if (md.avec < 0) continue;
+          P->ipouts.push_back({gslot[it.gates[mi - bd.mem_begin]], red0, md.avec});
+          ++nout;
+        }
+      };
+      auto block_has_grad = [&](const Item& it) {
+        for (int g : it.gates)
+          if (gates[g].kind <= G_RZ && info[g].need_grad) return true;
+        return false;
+      };
       const std::vector<Item>& items = fwd_items[si];
+      // split adjoint: the partner's state is read from shared memory, which
+      // is current only until this segment modifies the registers
+      bool dirty = false;
+      auto publish_if_dirty = [&]() {
+        if (!dirty) return;
+        Op pub{};
+        pub.w0 = enc(OP_PUBLISH, 0, 0, 0, false);
+        P->ops.push_back(pub);
+        dirty = false;
+      };
       for (int ii = (int)items.size() - 1; ii >= 0; --ii) {
         const Item& it = items[ii];
+        Op op{};
+        dirty = dirty || ii < (int)items.size() - 1;
+        if (it.type == 3) {
+          uint32_t gmask = 0;
+          for (const Item& sub : it.sub)
+            if (block_has_grad(sub)) gmask |= 1u << slot_of[gates[sub.gates[0]].q0];
+          if (gmask) {
+            publish_if_dirty();
+            Op ip{};
+            ip.w0 = enc(OP_IP3SET, 0, gmask, (uint32_t)nred, false);
+            ip.param = (uint32_t)it.id;
+            P->ops.push_back(ip);
+            // reduction slots: 3 per flagged register slot, in slot order
+            for (const Item& sub : it.sub) {
+              const int slot = slot_of[gates[sub.gates[0]].q0];
+              if (!(gmask >> slot & 1u)) continue;
+              block_outputs(sub, nred + 3 * __builtin_popcount(gmask & ((1u << slot) - 1u)));
+            }
+            nred += 3 * __builtin_popcount(gmask);
+          }
+          op.w0 = enc(OP_U2SET, 0, 0, 0, true);
+          op.param = (uint32_t)it.id;
+          P->ops.push_back(op);
+          continue;
+        }
         const int g0 = it.gates[0];
         const GateIn& gi0 = gates[g0];
-        Op op{};
         if (it.type == 1 && it.gates.size() > 1) {
-          bool any = false;
-          for (int g : it.gates) any = any || (gates[g].kind <= G_RZ && info[g].need_grad);
-          if (any) {
+          if (block_has_grad(it)) {
+            publish_if_dirty();
             Op ip{};
             ip.w0 = enc(OP_IP3, operand(gi0.q0), 0, (uint32_t)nred, false);
             ip.param = (uint32_t)it.id;
             P->ops.push_back(ip);
-            const BlockDesc& bd = P->blocks[it.id];
-            for (int mi = bd.mem_begin; mi < bd.mem_end; ++mi) {
-              const MemberDesc& md = P->members[mi];
-              if (md.avec < 0) continue;
-              const int g = it.gates[mi - bd.mem_begin];
-              P->ipouts.push_back({gslot[g], nred, md.avec});
-              ++nout;
-            }
+            block_outputs(it, nred);
             nred += 3;
           }
           op.w0 = enc(OP_U2, operand(gi0.q0), 0, 0, true);
@@ -415,6 +549,7 @@ std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total
           op.param = (uint32_t)it.id;
         } else if (gi0.kind <= G_RZ) {
           if (info[g0].need_grad) {
+            publish_if_dirty();
             Op ip{};
             ip.w0 = enc(OP_IPX + gi0.kind, operand(gi0.q0), 0, (uint32_t)nred, false);
             ip.param = (uint32_t)gslot[g0];

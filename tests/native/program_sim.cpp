@@ -115,6 +115,15 @@ std::string check_program(const HostProgram& P, const ScheduleOptions& opt) {
           case OP_CZRUN:
             if ((int)op.param >= (int)P.diag.size()) return "bad diag run id";
             break;
+          case OP_PUBLISH:
+            break;
+          case OP_U2SET: case OP_IP3SET:
+            for (int sl = 0; sl < sd.nreg; ++sl) {
+              const uint32_t id = (op.param >> (8 * sl)) & 0xFFu;
+              if (id != kNoBlock && (int)id >= pd.blk_end - pd.blk_begin) return "set block id out of range";
+            }
+            if (code == OP_IP3SET && (b & ~((1u << sd.nreg) - 1u))) return "IP3SET mask beyond slots";
+            break;
           case OP_U2: case OP_IP3:
             if ((int)op.param < pd.blk_begin || (int)op.param >= pd.blk_end) return "block id outside pass range";
             if (!in_regs(a)) return "block operand not a register slot";
@@ -214,6 +223,35 @@ int sim_run(int n, int64_t G, const int64_t* kinds, const int64_t* q0, const int
                           [&](int r) { return CS{c[r], s[r]}; },
                           [&](int slot, const double* v) { avec[slot] = {v[0], v[1], v[2]}; });
   }
+  int cur_blk_base = 0;
+  // folded CNOT runs: register bits of every index are remapped through
+  // (col, k) exactly as the kernels compute their smem addresses
+  auto remap = [&](const SegDesc& sd, const uint8_t* col, const uint32_t* km, uint32_t x) {
+    uint32_t regmask = 0;
+    for (int q = 0; q < sd.nreg; ++q) regmask |= 1u << sd.reg_g[q];
+    const uint32_t J0 = x & ~regmask;
+    uint32_t i = 0;
+    for (int q = 0; q < sd.nreg; ++q) i |= ((x >> sd.reg_g[q]) & 1u) << q;
+    uint32_t y = 0;
+    for (int q = 0; q < sd.nreg; ++q)
+      if (i >> q & 1u) y ^= col[q];
+    for (int t = 0; t < sd.nreg; ++t)
+      if (__builtin_popcount(J0 & km[t]) & 1) y ^= 1u << t;
+    uint32_t out = J0;
+    for (int q = 0; q < sd.nreg; ++q) out |= ((y >> q) & 1u) << sd.reg_g[q];
+    return out;
+  };
+  // load: reg content at x = state[remap_ld(x)]; store: state'[remap_st(x)] = reg content at x
+  auto do_load = [&](std::vector<cd>& st, const SegDesc& sd) {
+    std::vector<cd> o(st.size());
+    for (size_t x = 0; x < st.size(); ++x) o[x] = st[remap(sd, sd.ld_col, sd.ld_k, (uint32_t)x)];
+    st.swap(o);
+  };
+  auto do_store = [&](std::vector<cd>& st, const SegDesc& sd) {
+    std::vector<cd> o(st.size());
+    for (size_t x = 0; x < st.size(); ++x) o[remap(sd, sd.st_col, sd.st_k, (uint32_t)x)] = st[x];
+    st.swap(o);
+  };
   auto apply = [&](std::vector<cd>& st, const SegDesc& sd, const Op& op) {
     const uint32_t code = op_code(op.w0);
     const int qa = qubit_of(sd, op_a(op.w0)), qb = qubit_of(sd, op_b(op.w0));
@@ -229,6 +267,20 @@ int sim_run(int n, int64_t G, const int64_t* kinds, const int64_t* q0, const int
         const cd x = st[j], y = st[j | m];
         st[j] = cd(u.a.re, u.a.im) * x + cd(u.b.re, u.b.im) * y;
         st[j | m] = cd(u.c.re, u.c.im) * x + cd(u.d.re, u.d.im) * y;
+      }
+    } else if (code == OP_U2SET) {
+      for (int sl = 0; sl < sd.nreg; ++sl) {
+        const uint32_t id = (op.param >> (8 * sl)) & 0xFFu;
+        if (id == kNoBlock) continue;
+        M2 u = U[cur_blk_base + (int)id];
+        if (op_adj(op.w0)) u = mdag(u);
+        const size_t m = (size_t)1 << sd.reg_g[sl];
+        for (size_t j = 0; j < st.size(); ++j) {
+          if (j & m) continue;
+          const cd x = st[j], y = st[j | m];
+          st[j] = cd(u.a.re, u.a.im) * x + cd(u.b.re, u.b.im) * y;
+          st[j | m] = cd(u.c.re, u.c.im) * x + cd(u.d.re, u.d.im) * y;
+        }
       }
     } else if (code == OP_CZRUN) {
       const DiagRun& dr = P.diag[op.param];
@@ -248,11 +300,15 @@ int sim_run(int n, int64_t G, const int64_t* kinds, const int64_t* q0, const int
       S.fixed(st, (int)code, qa, qb);
     }
   };
-  for (const PassDesc& pd : P.passes)
+  for (const PassDesc& pd : P.passes) {
+    cur_blk_base = pd.blk_begin;
     for (int sg = pd.seg_begin; sg < pd.seg_end; ++sg) {
       const SegDesc& sd = P.segs[sg];
+      do_load(S.psi, sd);
       for (int o = sd.op_begin; o < sd.op_end; ++o) apply(S.psi, sd, P.ops[o]);
+      do_store(S.psi, sd);
     }
+  }
   auto zw = [&](size_t j, int lo, int hi) {
     double w = 0;
     for (int t = lo; t < hi; ++t) w += (__builtin_popcountll(j & (size_t)t_smask[t]) & 1) ? -t_coeff[t] : t_coeff[t];
@@ -281,22 +337,36 @@ int sim_run(int n, int64_t G, const int64_t* kinds, const int64_t* q0, const int
     std::fill(ipv.begin(), ipv.end(), 0.0);
     for (int pi = (int)P.passes.size() - 1; pi >= 0; --pi) {
       const PassDesc& pd = P.passes[pi];
+      cur_blk_base = pd.blk_begin;
       for (int sg = pd.bseg_begin; sg < pd.bseg_end; ++sg) {
         const SegDesc& sd = P.segs[sg];
+        do_load(S.psi, sd);
+        do_load(S.phi, sd);
         std::vector<double> red((size_t)std::max(1, sd.red_count), 0.0);
         for (int o = sd.op_begin; o < sd.op_end; ++o) {
           const Op& op = P.ops[o];
           const uint32_t code = op_code(op.w0);
           const int q = qubit_of(sd, op_a(op.w0));
-          if (code == OP_IPX || code == OP_IPY || code == OP_IPZ) {
+          if (code == OP_PUBLISH) {
+            continue;
+          } else if (code == OP_IPX || code == OP_IPY || code == OP_IPZ) {
             red[op_ip(op.w0)] = S.ip((int)(code - OP_IPX), q);
           } else if (code == OP_IP3) {
             for (int ax = 0; ax < 3; ++ax) red[op_ip(op.w0) + ax] = S.ip(ax, q);
+          } else if (code == OP_IP3SET) {
+            int r0 = (int)op_ip(op.w0);
+            for (int sl = 0; sl < sd.nreg; ++sl) {
+              if (!(op_b(op.w0) >> sl & 1u)) continue;
+              for (int ax = 0; ax < 3; ++ax) red[r0 + ax] = S.ip(ax, sd.reg_g[sl]);
+              r0 += 3;
+            }
           } else {
             apply(S.psi, sd, op);
             apply(S.phi, sd, op);
           }
         }
+        do_store(S.psi, sd);
+        do_store(S.phi, sd);
         for (int oi = 0; oi < sd.ip_count; ++oi) {
           const IpOut& io = P.ipouts[sd.ip_begin + oi];
           if (io.red < 0 || io.red >= sd.red_count) {
