@@ -111,7 +111,7 @@ __device__ __forceinline__ Group make_group(int threads_per_role, int samples) {
 // Whole state on chip: one CTA owns S samples of n <= 12 qubits and runs
 // forward, expectations, seed and the adjoint sweep without touching HBM.
 template <int R, int KM>
-__global__ void __launch_bounds__(KM == KM_SPLIT ? 512 : (R >= 4 ? 256 : 512))
+__global__ void __launch_bounds__(R >= 5 ? 256 : (KM == KM_SPLIT ? 512 : (R >= 4 ? 256 : 512)))
     k_smem(DevProgram D, RunArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr bool ADJ = KM != KM_FWD;
@@ -180,7 +180,8 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 // One pass over HBM-resident states: CTA (tile, row) stages 2^k amplitudes.
 template <int R, int KM>
-__global__ void __launch_bounds__(R >= 4 ? 256 : 512, R >= 4 ? 2 : 1) k_pass(DevProgram D, RunArgs A) {
+__global__ void __launch_bounds__(R >= 5 ? 128 : (R >= 4 ? 256 : 512), R >= 4 ? 2 : 1)
+    k_pass(DevProgram D, RunArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr bool ADJ = KM != KM_FWD;
   const PassDesc* pd = D.passes + A.pass;
@@ -321,15 +322,17 @@ KFn smem_kernel(int R, bool dual, bool split) {
       default: return k_smem<4, KM_FWD>;
     }
   }
-  if (split) return R >= 4 ? k_smem<4, KM_SPLIT> : k_smem<3, KM_SPLIT>;
+  if (split) return R >= 5 ? k_smem<5, KM_SPLIT> : (R >= 4 ? k_smem<4, KM_SPLIT> : k_smem<3, KM_SPLIT>);
   switch (R) {
     case 1: return k_smem<1, KM_DUAL>;
     case 2: return k_smem<2, KM_DUAL>;
     case 3: return k_smem<3, KM_DUAL>;
-    default: return k_smem<4, KM_DUAL>;
+    case 4: return k_smem<4, KM_DUAL>;
+    default: return k_smem<5, KM_DUAL>;
   }
 }
 KFn pass_kernel(int R, bool dual) {
+  if (R >= 5) return dual ? k_pass<5, KM_SPLIT> : k_pass<5, KM_FWD>;
   if (R >= 4) return dual ? k_pass<4, KM_SPLIT> : k_pass<4, KM_FWD>;
   return dual ? k_pass<3, KM_SPLIT> : k_pass<3, KM_FWD>;
 }
@@ -436,6 +439,7 @@ struct VqcPlan {
   BlockDesc* d_blocks = nullptr;
   MemberDesc* d_members = nullptr;
   DiagRun* d_diag = nullptr;
+  int16_t* d_setids = nullptr;
   PassDesc* d_passes = nullptr;
   RotDesc* d_rots = nullptr;
   int32_t* d_term_offs = nullptr;
@@ -509,7 +513,7 @@ int smem_samples(const VqcPlan* p, int64_t B, bool dual, size_t* smem_bytes, int
   auto bytes_for = [&](int S) {
     return SmemLayout(S, 1 << P.n, dual, P.n_rot, P.n_blk, P.n_av, red_slots(p), S * TT, p->M).total;
   };
-  const int max_threads = split ? 512 : (P.R >= 4 ? 256 : 512);
+  const int max_threads = P.R >= 5 ? 256 : (split ? 512 : (P.R >= 4 ? 256 : 512));
   int smax = std::max(1, max_threads / TT);
   const int64_t want = std::max<int64_t>(1, (B + 2 * p->sms - 1) / (2 * p->sms));
   int S = 1;
@@ -758,7 +762,7 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
   VqcPlan* p = new VqcPlan();
   ScheduleOptions opt;
   opt.tile_qubits = env_int("VQC_TILE_QUBITS", 11);
-  opt.reg_slots = std::max(3, std::min(kMaxR, env_int("VQC_REG_SLOTS", kMaxR)));
+  opt.reg_slots = std::max(3, std::min(kMaxR, env_int("VQC_REG_SLOTS", 4)));
   std::string err = build_program(gates, c->n_qubits, c->total_params, wcol, opt, &p->prog);
   if (!err.empty()) {
     delete p;
@@ -803,6 +807,7 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
   if (e == cudaSuccess) e = upload(P.blocks, &p->d_blocks);
   if (e == cudaSuccess) e = upload(P.members, &p->d_members);
   if (e == cudaSuccess) e = upload(P.diag, &p->d_diag);
+  if (e == cudaSuccess) e = upload(P.setids, &p->d_setids);
   if (e == cudaSuccess) e = upload(P.passes, &p->d_passes);
   if (e == cudaSuccess) e = upload(P.rots, &p->d_rots);
   if (e == cudaSuccess) e = upload(p->term_offs, &p->d_term_offs);
@@ -821,6 +826,7 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
   D.blocks = p->d_blocks;
   D.members = p->d_members;
   D.diag = p->d_diag;
+  D.setids = p->d_setids;
   D.n_blk = P.n_blk;
   D.n_av = P.n_av;
   D.max_rot_pass = P.max_rot_per_pass;
@@ -853,6 +859,7 @@ void vqc_plan_destroy(VqcPlan* p) {
   cudaFree(p->d_blocks);
   cudaFree(p->d_members);
   cudaFree(p->d_diag);
+  cudaFree(p->d_setids);
   cudaFree(p->d_passes);
   cudaFree(p->d_rots);
   cudaFree(p->d_term_offs);

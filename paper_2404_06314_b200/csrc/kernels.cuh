@@ -28,6 +28,7 @@ struct DevProgram {
   const BlockDesc* blocks;
   const MemberDesc* members;
   const DiagRun* diag;
+  const int16_t* setids;
   const int32_t* term_offs;  // M + 1
   const uint32_t* t_smask;   // T
   const double* t_coeff;     // T (coeff * Re(phase); Z strings only)
@@ -98,7 +99,8 @@ __device__ __forceinline__ void with_slot(uint32_t s, F&& f) {
     case 0: f(std::integral_constant<int, 0>{}); break;
     case 1: if constexpr (R > 1) f(std::integral_constant<int, 1>{}); break;
     case 2: if constexpr (R > 2) f(std::integral_constant<int, 2>{}); break;
-    default: if constexpr (R > 3) f(std::integral_constant<int, 3>{}); break;
+    case 3: if constexpr (R > 3) f(std::integral_constant<int, 3>{}); break;
+    default: if constexpr (R > 4) f(std::integral_constant<int, 4>{}); break;
   }
 }
 
@@ -336,6 +338,7 @@ __device__ __forceinline__ void with_const_slot(int s, F&& f) {
   if constexpr (R > 1) if (s == 1) f(std::integral_constant<int, 1>{});
   if constexpr (R > 2) if (s == 2) f(std::integral_constant<int, 2>{});
   if constexpr (R > 3) if (s == 3) f(std::integral_constant<int, 3>{});
+  if constexpr (R > 4) if (s == 4) f(std::integral_constant<int, 4>{});
 }
 
 // per-sample parameter tables in shared memory
@@ -434,8 +437,8 @@ __device__ __forceinline__ void exec_op(const DevProgram& D, const Op op, double
       const bool adj = op_adj(w0);
 #pragma unroll
       for (int sl = 0; sl < R; ++sl) {
-        const uint32_t id = (op.param >> (8 * sl)) & 0xFFu;
-        if (id == kNoBlock) continue;
+        const int id = D.setids[op.param * kMaxR + sl];
+        if (id < 0) continue;
         const double2* u = T.u + 4 * id;
         double2 u00 = u[0], u01 = u[1], u10 = u[2], u11 = u[3];
         if (adj) {

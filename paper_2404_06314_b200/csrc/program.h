@@ -24,7 +24,7 @@
 
 namespace vqc {
 
-constexpr int kMaxR = 4;            // register slots per thread
+constexpr int kMaxR = 5;            // register slots per thread (max)
 constexpr int kMaxQubits = 24;      // statevector.py:21
 constexpr int kSmemMaxQubits = 12;  // on-chip (single pass) limit
 constexpr int kMaxFactors = 4;      // factors per angle expression on this path
@@ -39,13 +39,12 @@ enum OpCode : uint32_t {
   OP_U2 = 10,     // fused run of 1q gates on a register slot: param = block id
   OP_IP3 = 11,    // Im<phi|X|psi>, Im<phi|Y|psi>, Im<phi|Z|psi> on a slot (3 red slots)
   OP_CZRUN = 12,  // fused run of CZ gates: param = diagonal-run id
-  OP_U2SET = 13,  // fused blocks on several slots: param = 8-bit block id (relative to the
-                  // pass) per slot, 0xFF = none
+  OP_U2SET = 13,  // fused blocks on several slots: param = set id; setids[kMaxR * id + slot]
+                  // is the block id relative to the pass, -1 = none
   OP_IP3SET = 14, // IP3 on the slots in operand b's mask; 3 reduction slots each from op_ip
   OP_PUBLISH = 15, // split adjoint: write this thread's registers back to shared memory so
                    // the partner thread (other state) can read them for inner products
 };
-constexpr uint32_t kNoBlock = 0xFFu;
 
 // operand field (6 bits): bit 5 set -> register slot (low 3 bits), else a
 // global qubit number whose bit is constant per thread.

@@ -392,17 +392,17 @@ std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total
       for (Item& it : grouped) {
         Op op{};
         if (it.type == 3) {
-          uint32_t ids = 0xFFFFFFFFu;
-          bool fits = true;
+          const int set_id = (int)(P->setids.size() / kMaxR);
+          P->setids.resize(P->setids.size() + kMaxR, (int16_t)-1);
           for (Item& sub : it.sub) {
             sub.id = new_block(sub);
             const int rel = sub.id - pd.blk_begin;
-            if (rel >= (int)kNoBlock) fits = false;
+            if (rel > 32767) return "too many fused blocks in one pass";
             const int slot = slot_of[gates[sub.gates[0]].q0];
-            ids = (ids & ~(0xFFu << (8 * slot))) | ((uint32_t)(rel & 0xFF) << (8 * slot));
+            P->setids[(size_t)set_id * kMaxR + slot] = (int16_t)rel;
           }
-          if (!fits) return "too many fused blocks in one pass";
-          it.id = (int)ids;
+          it.id = set_id;
+          const uint32_t ids = (uint32_t)set_id;
           op.w0 = enc(OP_U2SET, 0, 0, 0, false);
           op.param = ids;
           P->ops.push_back(op);

@@ -19,7 +19,7 @@ struct GateIn {
 
 struct ScheduleOptions {
   int tile_qubits = 11;      // k for HBM passes
-  int reg_slots = kMaxR;     // R
+  int reg_slots = 4;         // R
   int forced_low = 3;        // qubits 0..forced_low-1 always local in HBM passes
   int smem_max_qubits = kSmemMaxQubits;  // n above this streams tiles through HBM
 };
@@ -41,6 +41,7 @@ struct HostProgram {
   std::vector<BlockDesc> blocks;
   std::vector<MemberDesc> members;
   std::vector<DiagRun> diag;
+  std::vector<int16_t> setids;  // kMaxR per block set
   int n_cols = 0;
   std::vector<int32_t> col_offs;  // n_cols + 1
   std::vector<ChainEntry> chain;

@@ -119,8 +119,8 @@ std::string check_program(const HostProgram& P, const ScheduleOptions& opt) {
             break;
           case OP_U2SET: case OP_IP3SET:
             for (int sl = 0; sl < sd.nreg; ++sl) {
-              const uint32_t id = (op.param >> (8 * sl)) & 0xFFu;
-              if (id != kNoBlock && (int)id >= pd.blk_end - pd.blk_begin) return "set block id out of range";
+              const int id = P.setids[op.param * kMaxR + sl];
+              if (id >= pd.blk_end - pd.blk_begin) return "set block id out of range";
             }
             if (code == OP_IP3SET && (b & ~((1u << sd.nreg) - 1u))) return "IP3SET mask beyond slots";
             break;
@@ -168,7 +168,7 @@ extern "C" {
 // stats: [passes, segments, rotations, grad_slots].
 int sim_run(int n, int64_t G, const int64_t* kinds, const int64_t* q0, const int64_t* q1,
             const double* coeff, const int64_t* f_offs, const int64_t* f_idx, int64_t total_params,
-            const int64_t* wrt_col, int tile_qubits, int smem_max_qubits, int M, const int64_t* term_offs,
+            const int64_t* wrt_col, int tile_qubits, int smem_max_qubits, int reg_slots, int M, const int64_t* term_offs,
             const double* t_coeff, const int64_t* t_smask, const double* flat, const double* upstream,
             double* expect_out, double* grad_out, int64_t* stats, char* err, int errcap) {
   std::vector<GateIn> gates((size_t)G);
@@ -184,6 +184,7 @@ int sim_run(int n, int64_t G, const int64_t* kinds, const int64_t* q0, const int
   ScheduleOptions opt;
   opt.tile_qubits = tile_qubits;
   opt.smem_max_qubits = smem_max_qubits;
+  opt.reg_slots = reg_slots;
   HostProgram P;
   std::string e = build_program(gates, n, total_params, wc, opt, &P);
   if (e.empty()) e = check_program(P, opt);
@@ -270,9 +271,9 @@ int sim_run(int n, int64_t G, const int64_t* kinds, const int64_t* q0, const int
       }
     } else if (code == OP_U2SET) {
       for (int sl = 0; sl < sd.nreg; ++sl) {
-        const uint32_t id = (op.param >> (8 * sl)) & 0xFFu;
-        if (id == kNoBlock) continue;
-        M2 u = U[cur_blk_base + (int)id];
+        const int id = P.setids[op.param * kMaxR + sl];
+        if (id < 0) continue;
+        M2 u = U[cur_blk_base + id];
         if (op_adj(op.w0)) u = mdag(u);
         const size_t m = (size_t)1 << sd.reg_g[sl];
         for (size_t j = 0; j < st.size(); ++j) {

@@ -40,7 +40,7 @@ def sim():
     return lib
 
 
-def run_sim(lib, circuit, observables, flat, wrt, tile_qubits=11, smem_max=12, upstream=None):
+def run_sim(lib, circuit, observables, flat, wrt, tile_qubits=11, smem_max=12, upstream=None, reg_slots=4):
     c = circuit.compiled()
     pack = ObservablePack.from_observables(observables, circuit.num_qubits)
     layout = WrtLayout.build(c, wrt)
@@ -62,7 +62,7 @@ def run_sim(lib, circuit, observables, flat, wrt, tile_qubits=11, smem_max=12, u
         circuit.num_qubits, ctypes.c_int64(len(c.kinds)), arrs[0].ctypes.data_as(_I64P),
         arrs[1].ctypes.data_as(_I64P), arrs[2].ctypes.data_as(_I64P), arrs[3].ctypes.data_as(_F64P),
         arrs[4].ctypes.data_as(_I64P), arrs[5].ctypes.data_as(_I64P), ctypes.c_int64(c.total_params),
-        arrs[6].ctypes.data_as(_I64P), tile_qubits, smem_max, M, arrs[7].ctypes.data_as(_I64P),
+        arrs[6].ctypes.data_as(_I64P), tile_qubits, smem_max, reg_slots, M, arrs[7].ctypes.data_as(_I64P),
         arrs[8].ctypes.data_as(_F64P), arrs[9].ctypes.data_as(_I64P), arrs[10].ctypes.data_as(_F64P),
         None if up is None else up.ctypes.data_as(_F64P), expect.ctypes.data_as(_F64P),
         grad.ctypes.data_as(_F64P), stats.ctypes.data_as(_I64P), err, 256)
@@ -80,12 +80,14 @@ def _flat_row(circuit, trainable, x_row):
 
 @pytest.mark.parametrize("cfg_id", [1, 2, 3, 4])
 @pytest.mark.parametrize("tile", [None, 6])
-def test_configs(sim, cfg_id, tile):
+@pytest.mark.parametrize("reg_slots", [4, 5])
+def test_configs(sim, cfg_id, tile, reg_slots):
     spec = configs.CONFIGS[cfg_id]
     circ, obs, wrt = configs.build(spec, configs.native_api())
     x, w = configs.inputs_and_weights(spec, batch=2)
     e_ref, j_ref = oracle_batch(circ, obs, {"w": w}, x, wrt)
     kw = {} if tile is None else {"tile_qubits": tile, "smem_max": min(tile, spec.n - 1)}
+    kw["reg_slots"] = reg_slots
     for b in range(len(x)):
         flat = _flat_row(circ, {"w": w}, x[b])
         e, jac, stats, layout = run_sim(sim, circ, obs, flat, wrt, **kw)
@@ -128,12 +130,15 @@ def _random(rng, n, n_gates):
 
 
 @pytest.mark.parametrize("n", list(range(1, 11)))
-@pytest.mark.parametrize("tile", [4, 5, 11])
-def test_random_circuits(sim, n, tile):
+@pytest.mark.parametrize("tile", [4, 6, 11])
+@pytest.mark.parametrize("reg_slots", [3, 4, 5])
+def test_random_circuits(sim, n, tile, reg_slots):
     if tile <= 3 or (tile < n and tile < 4):
         pytest.skip("tile too small")
+    if tile < reg_slots + 2 and tile < n:
+        pytest.skip("tile too small for the register slots")
     rng = np.random.default_rng(1000 * n + tile)
-    for rep in range(4):
+    for rep in range(2):
         circ, obs, tr = _random(rng, n, int(rng.integers(0, 60)))
         x = rng.uniform(-2, 2, (1, 3))
         wrt = ("a", "s", "b")
@@ -141,7 +146,7 @@ def test_random_circuits(sim, n, tile):
         flat = _flat_row(circ, tr, x[0])
         smem_max = 12 if tile >= n else min(tile, n - 1)
         e, jac, _, layout = run_sim(sim, circ, obs, flat, wrt, tile_qubits=min(tile, n),
-                                    smem_max=smem_max)
+                                    smem_max=smem_max, reg_slots=reg_slots)
         assert close(e, e_ref[0]) < 1e-12
         full = np.concatenate([j_ref[k][0] for k, _, _ in layout.slices], axis=1)
         assert close(jac, full) < 1e-12

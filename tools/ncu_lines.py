@@ -12,6 +12,7 @@ import tempfile
 
 rep, kname = sys.argv[1], sys.argv[2]
 lib = sys.argv[3] if len(sys.argv) > 3 else "paper_2404_06314_b200/_lib/libvqc.so"
+column = sys.argv[4] if len(sys.argv) > 4 else "Warp Stall Sampling (All Samples)"
 sass = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                       capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(sass)))
@@ -22,7 +23,7 @@ for r in rows[2:]:
         continue
     d = dict(zip(hdr, r))
     try:
-        samples[int(d["Address"], 16)] = (float(d["Warp Stall Sampling (All Samples)"] or 0), d["Source"])
+        samples[int(d["Address"], 16)] = (float(d[column] or 0), d["Source"])
     except ValueError:
         pass
 if samples:
