@@ -74,7 +74,7 @@ __device__ __forceinline__ void observe(const DevProgram& D, const RunArgs& A, c
 
 // Shared-memory carve-up (kernels and host sizing must agree).
 struct SmemLayout {
-  size_t psi, phi, cs, u, av, red, up, total;  // byte offsets
+  size_t psi, phi, cs, u, av, red, fin, up, total;  // byte offsets
   __host__ __device__ SmemLayout(int S, int n_amp, bool dual, int nrot, int nblk, int nav, int red_slots,
                                  int threads, int M) {
     size_t o = 0;
@@ -84,6 +84,7 @@ struct SmemLayout {
     u = o; o += (size_t)S * nblk * 64;
     av = o; o += (size_t)S * nav * 32;
     red = o; o += (size_t)red_slots * threads * 8;
+    fin = o; o += (size_t)red_slots * S * 8;
     up = o; o += (size_t)S * M * 8;
     total = o + 16;
   }
@@ -132,6 +133,7 @@ __global__ void __launch_bounds__(R >= 5 ? 256 : (KM == KM_SPLIT ? 512 : (R >= 4
   double2* s_u = reinterpret_cast<double2*>(smem_raw + L.u) + (size_t)grp.sl * nblk * 4;
   double* s_av_all = reinterpret_cast<double*>(smem_raw + L.av);
   double* s_red = reinterpret_cast<double*>(smem_raw + L.red);
+  double* s_fin = reinterpret_cast<double*>(smem_raw + L.fin);
   double* s_up = reinterpret_cast<double*>(smem_raw + L.up);
 
   for (int l = lane; l < N; l += grp.TT) s_psi[swz((uint32_t)l)] = make_double2(l == 0 ? 1.0 : 0.0, 0.0);
@@ -140,7 +142,7 @@ __global__ void __launch_bounds__(R >= 5 ? 256 : (KM == KM_SPLIT ? 512 : (R >= 4
   build_tables(D, A, pd, b, valid, s_cs, s_u, s_av_all + (size_t)grp.sl * nav * 4, lane, grp.TT);
   const SampleTables T{s_cs, s_u, 0, 0};
 
-  run_segments<R, MODE_FWD>(D, A, pd->seg_begin, pd->seg_end, s_psi, s_psi, T, s_av_all, nav * 4, 0, s_red,
+  run_segments<R, MODE_FWD>(D, A, pd->seg_begin, pd->seg_end, s_psi, s_psi, T, s_av_all, nav * 4, 0, s_red, s_fin,
                             grp, grp.role == 0, 0u, bl0, 0, 0, 1);
   if constexpr (!ADJ) {
     observe<false>(D, A, nullptr, s_psi, s_psi, nullptr, grp, s_red, 0u, n, bl0, true, 0, 0, 0, 1);
@@ -149,7 +151,7 @@ __global__ void __launch_bounds__(R >= 5 ? 256 : (KM == KM_SPLIT ? 512 : (R >= 4
       observe<true>(D, A, nullptr, s_psi, s_phi, s_up + grp.sl * D.M, grp, s_red, 0u, n, bl0,
                     A.expect != nullptr, 1, 0, 0, 1);
       __syncthreads();
-      run_segments<R, BM>(D, A, pd->bseg_begin, pd->bseg_end, s_psi, s_phi, T, s_av_all, nav * 4, 0, s_red,
+      run_segments<R, BM>(D, A, pd->bseg_begin, pd->bseg_end, s_psi, s_phi, T, s_av_all, nav * 4, 0, s_red, s_fin,
                           grp, true, 0u, bl0, 0, 0, 1);
     } else {
       observe<true>(D, A, nullptr, s_psi, s_phi, nullptr, grp, s_red, 0u, n, bl0,
@@ -166,7 +168,7 @@ __global__ void __launch_bounds__(R >= 5 ? 256 : (KM == KM_SPLIT ? 512 : (R >= 4
         observe<true>(D, A, nullptr, s_psi, s_phi, nullptr, grp, s_red, 0u, n, bl0, false, 2, m, 0, 1);
         __syncthreads();
         run_segments<R, BM>(D, A, pd->bseg_begin, pd->bseg_end, s_psi, s_phi, T, s_av_all, nav * 4, 0,
-                            s_red, grp, true, 0u, bl0, m, 0, 1);
+                            s_red, s_fin, grp, true, 0u, bl0, m, 0, 1);
       }
     }
   }
@@ -207,11 +209,13 @@ __global__ void __launch_bounds__(R >= 5 ? 128 : (R >= 4 ? 256 : 512), R >= 4 ? 
   double2* s_u = reinterpret_cast<double2*>(smem_raw + L.u);
   double* s_av = reinterpret_cast<double*>(smem_raw + L.av);
   double* s_red = reinterpret_cast<double*>(smem_raw + L.red);
+  double* s_fin = reinterpret_cast<double*>(smem_raw + L.fin);
   double* s_up = reinterpret_cast<double*>(smem_raw + L.up);
 
+  long long tdbg = A.dbg ? clock64() : 0;
+  if (A.dbg && threadIdx.x == 0) atomicAdd(A.dbg + DBG_CTAS, 1ull);
   if (ADJ && (flags & F_SEED) && A.bra < 0)
     for (int m = threadIdx.x; m < D.M; m += blockDim.x) s_up[m] = A.upstream[b * D.M + m];
-  const TileWalk tw = tile_walk(pd, tile_base, k, threadIdx.x, blockDim.x);
   if (flags & F_INIT) {
     for (int l = threadIdx.x; l < Nt; l += blockDim.x)
       s_psi[swz((uint32_t)l)] = make_double2((tile_base == 0 && l == 0) ? 1.0 : 0.0, 0.0);
@@ -221,19 +225,38 @@ __global__ void __launch_bounds__(R >= 5 ? 128 : (R >= 4 ? 256 : 512), R >= 4 ? 
     const double2* src = ((flags & F_LOAD_FIN) ? A.psi_fin : A.psi) + (size_t)bl * N;
     const double2* srcf = A.phi + (size_t)bl * N;
     const bool lphi = ADJ && (flags & F_LOAD_PHI);
+    const TileWalk tw = tile_walk(pd, tile_base, k, threadIdx.x, blockDim.x);
     for_tile(tw, threadIdx.x, blockDim.x, [&](uint32_t l, uint32_t j) {
       cp_async16(s_psi + swz(l), src + j);
       if (lphi) cp_async16(s_phi + swz(l), srcf + j);
     });
   }
-  build_tables(D, A, pd, b, true, s_cs, s_u, s_av, threadIdx.x, blockDim.x);
+  if (A.tables != nullptr) {
+    // per-sample tables precomputed by k_tables: copy this pass's slices
+    const double* t = A.tables + (size_t)bl * A.table_stride;
+    const int nrot = pd->rot_end - pd->rot_begin, nblk = pd->blk_end - pd->blk_begin,
+              nav = pd->av_end - pd->av_begin;
+    const double* tcs = t + 2 * pd->rot_begin;
+    const double* tu = t + 2 * (size_t)D.n_rot + 8 * (size_t)pd->blk_begin;
+    const double* tav = t + 2 * (size_t)D.n_rot + 8 * (size_t)D.n_blk + 4 * (size_t)pd->av_begin;
+    for (int i = threadIdx.x; i < nrot; i += blockDim.x) cp_async16(s_cs + i, tcs + 2 * i);
+    for (int i = threadIdx.x; i < 4 * nblk; i += blockDim.x) cp_async16(s_u + i, tu + 2 * i);
+    for (int i = threadIdx.x; i < 2 * nav; i += blockDim.x) cp_async16(s_av + 2 * i, tav + 2 * i);
+  } else {
+    build_tables(D, A, pd, b, true, s_cs, s_u, s_av, threadIdx.x, blockDim.x);
+  }
   cp_async_wait_all();
   __syncthreads();
+  dbg_add(A, DBG_PROLOGUE, tdbg);
   const SampleTables T{s_cs, s_u, pd->rot_begin, pd->blk_begin};
   if (flags & F_FWD)
-    run_segments<R, MODE_FWD>(D, A, pd->seg_begin, pd->seg_end, s_psi, s_psi, T, s_av, 0, pd->av_begin, s_red,
+    run_segments<R, MODE_FWD>(D, A, pd->seg_begin, pd->seg_end, s_psi, s_psi, T, s_av, 0, pd->av_begin, s_red, s_fin,
                               grp, grp.role == 0, tile_base, bl, 0, tile, n_tiles);
+  dbg_add(A, DBG_FWD, tdbg);
   if (flags & F_STORE_FIN) {
+    uint32_t tb = tile_base;
+    asm volatile("" : "+r"(tb));
+    const TileWalk tw = tile_walk(pd, tb, k, threadIdx.x, blockDim.x);
     double2* dst = A.psi_fin + (size_t)bl * N;
     for_tile(tw, threadIdx.x, blockDim.x, [&](uint32_t l, uint32_t j) { dst[j] = s_psi[swz(l)]; });
   }
@@ -242,21 +265,50 @@ __global__ void __launch_bounds__(R >= 5 ? 128 : (R >= 4 ? 256 : 512), R >= 4 ? 
                  (flags & F_SEED) ? (A.bra < 0 ? 1 : 2) : 0, A.bra, tile, n_tiles);
     __syncthreads();
   }
+  dbg_add(A, DBG_OBSERVE, tdbg);
   if constexpr (ADJ) {
     if (flags & F_BWD)
       run_segments<R, MODE_SPLIT>(D, A, pd->bseg_begin, pd->bseg_end, s_psi, s_phi, T, s_av, 0, pd->av_begin,
-                                  s_red, grp, true, tile_base, bl, A.bra < 0 ? 0 : A.bra, tile, n_tiles);
+                                  s_red, s_fin, grp, true, tile_base, bl, A.bra < 0 ? 0 : A.bra, tile, n_tiles);
   }
+  dbg_add(A, DBG_BWD, tdbg);
   const bool sphi = ADJ && (flags & F_STORE_PHI);
   if ((flags & F_STORE_PSI) || sphi) {
+    asm volatile("" ::: "memory");
+    uint32_t tb = tile_base;
+    asm volatile("" : "+r"(tb));  // rebuild the tile walk here rather than keep it live
+    const TileWalk tw = tile_walk(pd, tb, k, threadIdx.x, blockDim.x);
+    const bool spsi = (flags & F_STORE_PSI) != 0;
     double2* dst = A.psi + (size_t)bl * N;
     double2* dstf = A.phi + (size_t)bl * N;
-    const bool spsi = (flags & F_STORE_PSI) != 0;
     for_tile(tw, threadIdx.x, blockDim.x, [&](uint32_t l, uint32_t j) {
       if (spsi) dst[j] = s_psi[swz(l)];
       if (sphi) dstf[j] = s_phi[swz(l)];
     });
   }
+  dbg_add(A, DBG_STORE, tdbg);
+}
+
+// Per-sample angle / fused-block tables for every pass, once per call (HBM
+// mode): [cos/sin per rotation][U per block][gradient vector per member].
+__global__ void __launch_bounds__(256) k_tables(DevProgram D, RunArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int64_t bl = blockIdx.x;
+  const int64_t b = A.b0 + bl;
+  PassDesc all{};
+  all.rot_begin = 0;
+  all.rot_end = D.n_rot;
+  all.blk_begin = 0;
+  all.blk_end = D.n_blk;
+  all.av_begin = 0;
+  all.av_end = D.n_av;
+  double2* cs = reinterpret_cast<double2*>(smem_raw);
+  double2* u = cs + D.n_rot;
+  double* av = reinterpret_cast<double*>(u + 4 * (size_t)D.n_blk);
+  build_tables(D, A, &all, b, true, cs, u, av, threadIdx.x, blockDim.x);
+  const double* src = reinterpret_cast<const double*>(smem_raw);
+  double* dst = const_cast<double*>(A.tables) + (size_t)bl * A.table_stride;
+  for (int64_t i = threadIdx.x; i < A.table_stride; i += blockDim.x) dst[i] = src[i];
 }
 
 // out[i] = sum_t in[i * n_tiles + t], fixed order (one warp per output)
@@ -459,7 +511,8 @@ struct VqcPlan {
 namespace {
 
 struct Layout {
-  size_t ip = 0, rows = 0, psi = 0, phi = 0, fin = 0, ipart = 0, epart = 0, total = 0;
+  size_t ip = 0, rows = 0, psi = 0, phi = 0, fin = 0, ipart = 0, epart = 0, tables = 0, total = 0;
+  int64_t table_stride = 0;  // doubles per sample (0: tables rebuilt per CTA)
   int64_t chunk = 0;
   int n_tiles = 1;
   int K = 1;
@@ -496,6 +549,11 @@ Layout make_layout(const VqcPlan* p, int64_t B, int mode) {
     L.fin = take(mode == VQC_MODE_JACOBIAN ? (size_t)chunk * N * 16 : 0);
     L.ipart = take(adj ? (size_t)chunk * L.K * P.NG * L.n_tiles * 8 : 0);
     L.epart = take((size_t)chunk * M * L.n_tiles * 8);
+    const int64_t stride = 2 * (int64_t)P.n_rot + 8 * (int64_t)P.n_blk + 4 * (int64_t)P.n_av;
+    if (stride > 0 && stride * 8 <= 160 * 1024) {
+      L.table_stride = stride;
+      L.tables = take((size_t)chunk * stride * 8);
+    }
   }
   L.total = off + 256;
   return L;
@@ -571,6 +629,29 @@ int run_core(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, const
   A.upstream = d_up;
   A.K = L.K;
   A.red_slots = red_slots(p);
+  static unsigned long long* dbg = nullptr;
+  const bool dbg_on = env_int("VQC_DEBUG_TIMING", 0) != 0;
+  if (dbg_on) {
+    if (!dbg) cudaMalloc(&dbg, DBG_N * sizeof(unsigned long long));
+    cudaMemsetAsync(dbg, 0, DBG_N * sizeof(unsigned long long), st);
+    A.dbg = dbg;
+  }
+  struct DbgPrint {
+    bool on;
+    unsigned long long* d;
+    cudaStream_t st;
+    ~DbgPrint() {
+      if (!on) return;
+      unsigned long long h[DBG_N];
+      cudaMemcpyAsync(h, d, sizeof h, cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      const double ctas = h[DBG_CTAS] ? (double)h[DBG_CTAS] : 1.0;
+      fprintf(stderr, "[vqc timing] per CTA cycles: prologue %.0f fwd %.0f observe %.0f bwd %.0f store %.0f | "
+              "segments: load %.0f ops %.0f store %.0f final %.0f (ctas %.0f)\n",
+              h[0] / ctas, h[1] / ctas, h[2] / ctas, h[3] / ctas, h[4] / ctas, h[5] / ctas, h[6] / ctas,
+              h[7] / ctas, h[8] / ctas, ctas);
+    }
+  } dbg_print{dbg_on, dbg, st};
   double* ip = reinterpret_cast<double*>(ws + L.ip);
   const bool adj = mode != VQC_MODE_FORWARD;
   if (!P.hbm) {
@@ -609,6 +690,15 @@ int run_core(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, const
     A.expect = epart;
     A.ip = ipart;
     A.bra = -1;
+    A.tables = nullptr;
+    A.table_stride = 0;
+    if (L.table_stride > 0) {
+      A.tables = reinterpret_cast<double*>(ws + L.tables);
+      A.table_stride = L.table_stride;
+      int rc0;
+      if ((rc0 = launch("tables", k_tables, dim3((unsigned)nb), dim3(256), (size_t)L.table_stride * 8, st, D, A)))
+        return rc0;
+    }
     const dim3 grid((unsigned)L.n_tiles, (unsigned)nb), block((unsigned)TPS), block2((unsigned)(2 * TPS));
     int rc;
     for (int pi = 0; pi < NP - 1; ++pi) {
@@ -763,6 +853,9 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
   ScheduleOptions opt;
   opt.tile_qubits = env_int("VQC_TILE_QUBITS", 11);
   opt.reg_slots = std::max(3, std::min(kMaxR, env_int("VQC_REG_SLOTS", 4)));
+  // five register slots only where the adjoint runs split (one state per
+  // thread); the dual-state layout would need 256 state registers
+  if (opt.reg_slots > 4 && c->n_qubits <= kSmemMaxQubits && c->n_qubits - opt.reg_slots < 5) opt.reg_slots = 4;
   std::string err = build_program(gates, c->n_qubits, c->total_params, wcol, opt, &p->prog);
   if (!err.empty()) {
     delete p;

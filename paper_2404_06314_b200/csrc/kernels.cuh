@@ -61,7 +61,21 @@ struct RunArgs {
   int S;                   // samples per CTA (smem mode)
   int red_slots;           // reduction slots per buffer
   int jacobian;            // smem mode: loop over all M bras in-kernel
+  unsigned long long* dbg; // VQC_DEBUG_TIMING: per-phase clock64 totals (thread 0 of each CTA)
+  const double* tables;    // HBM mode: per-sample tables from k_tables (rows relative to b0)
+  int64_t table_stride;    // doubles per sample
 };
+
+// phase timing (debug only): dbg[slot] += clock64 delta, slots fixed below
+enum { DBG_PROLOGUE = 0, DBG_FWD = 1, DBG_OBSERVE = 2, DBG_BWD = 3, DBG_STORE = 4, DBG_SEG_LOAD = 5,
+       DBG_SEG_OPS = 6, DBG_SEG_STORE = 7, DBG_SEG_FINAL = 8, DBG_CTAS = 9, DBG_N = 10 };
+__device__ __forceinline__ void dbg_add(const RunArgs& A, int slot, long long& t) {
+  if (A.dbg != nullptr && threadIdx.x == 0) {
+    const long long now = clock64();
+    atomicAdd(A.dbg + slot, (unsigned long long)(now - t));
+    t = now;
+  }
+}
 
 // ---------------------------------------------------------------------------
 // shared-memory swizzle: 16-byte element l lives at l ^ fold3(l >> 3), i.e.
@@ -379,7 +393,17 @@ __device__ __forceinline__ void ip_dispatch(const SegCtx<R>& C, const double2 (&
     auto rf = [&](int i) { return f[i]; };
     kernel(std::integral_constant<int, -1>{}, ra, rf);
   } else {
-    auto sm = [&](int i) { return C.partner[C.addr(i)]; };
+    // recompute partner addresses here (pinned by the empty asm) instead of
+    // letting the compiler keep 2^R loop-invariant addresses live
+    uint32_t base = C.lp0;
+    asm volatile("" : "+r"(base));
+    auto sm = [&](int i) {
+      uint32_t ad = base;
+#pragma unroll
+      for (int s = 0; s < R; ++s)
+        if ((i >> s) & 1) ad ^= C.lc[s];
+      return C.partner[ad];
+    };
     if (role == 0) kernel(std::integral_constant<int, 0>{}, ra, sm);
     else kernel(std::integral_constant<int, 1>{}, sm, ra);
   }
@@ -581,11 +605,12 @@ template <int R, int MODE>
 __device__ __forceinline__ void run_segments(const DevProgram& D, const RunArgs& A, int sb, int se,
                                              double2* s_psi, double2* s_phi, const SampleTables& T,
                                              const double* s_av_all, int av_stride, int av_base,
-                                             double* s_red, const Group& grp, bool active,
+                                             double* s_red, double* s_fin, const Group& grp, bool active,
                                              uint32_t tile_base, int64_t bl0, int bra, int tile,
                                              int n_tiles) {
   constexpr int N = 1 << R;
   constexpr bool DUAL = MODE == MODE_DUAL;
+  long long tdbg = A.dbg ? clock64() : 0;
   double2* own = (MODE == MODE_SPLIT && grp.role) ? s_phi : s_psi;
   const double2* partner = (MODE == MODE_SPLIT && grp.role) ? s_psi : s_phi;
   for (int sg = sb; sg < se; ++sg) {
@@ -596,8 +621,9 @@ __device__ __forceinline__ void run_segments(const DevProgram& D, const RunArgs&
     C.partner = partner;
     uint32_t p0 = 0;
     C.J0 = tile_base;
-    for (int i = 0; i < nthr; ++i)
-      if ((grp.gi >> i) & 1) {
+#pragma unroll
+    for (int i = 0; i < kSmemMaxQubits; ++i)
+      if (i < nthr && ((grp.gi >> i) & 1)) {
         p0 ^= sd->tsw[i];
         C.J0 |= 1u << sd->thr_g[i];
       }
@@ -618,6 +644,7 @@ __device__ __forceinline__ void run_segments(const DevProgram& D, const RunArgs&
         if constexpr (DUAL) f[i] = s_phi[ad];
       }
     }
+    dbg_add(A, DBG_SEG_LOAD, tdbg);
     const int ob = sd->op_begin, oe = sd->op_end;
     Op nxt = ob < oe ? D.ops[ob] : Op{0u, 0u};
     for (int o = ob; o < oe; ++o) {
@@ -626,17 +653,28 @@ __device__ __forceinline__ void run_segments(const DevProgram& D, const RunArgs&
       if (MODE == MODE_SPLIT && op_code(op.w0) == OP_PUBLISH) {
         __syncthreads();
         if (active) {
+          uint32_t base = C.lp0;
+          asm volatile("" : "+r"(base));
 #pragma unroll
-          for (int i = 0; i < N; ++i) own[C.addr(i)] = a[i];
+          for (int i = 0; i < N; ++i) {
+            uint32_t ad = base;
+#pragma unroll
+            for (int s = 0; s < R; ++s)
+              if ((i >> s) & 1) ad ^= C.lc[s];
+            own[ad] = a[i];
+          }
         }
         __syncthreads();
         continue;
       }
       if (active) exec_op<R, MODE>(D, op, a, f, C, grp.role, T, s_red);
     }
+    dbg_add(A, DBG_SEG_OPS, tdbg);
     if (MODE == MODE_SPLIT && sd->ip_count > 0) __syncthreads();  // partners done reading
+    asm volatile("" ::: "memory");  // keep the store map's loads and math after the op loop
     if (active) {
       uint32_t sp0 = p0, sc[R];
+      asm volatile("" : "+r"(sp0));
 #pragma unroll
       for (int t = 0; t < R; ++t) {
         if (__popc(C.J0 & sd->st_k[t]) & 1) sp0 ^= sd->ps[t];
@@ -653,45 +691,49 @@ __device__ __forceinline__ void run_segments(const DevProgram& D, const RunArgs&
       }
     }
     __syncthreads();
+    dbg_add(A, DBG_SEG_STORE, tdbg);
     if constexpr (MODE != MODE_FWD) {
       const int nout = sd->ip_count;
       if (nout > 0) {
-        // one warp per (output, sample): fixed-order sum of the sample's
-        // per-thread partials, then the block's gradient vector if fused.
-        // Blocks narrower than a warp (tiny n) finalise serially on thread 0.
+        // phase 1: one warp per (reduction slot, sample) sums the sample's
+        // per-thread partials in a fixed order; phase 2: one thread per
+        // (output, sample) applies the block gradient vector. Blocks narrower
+        // than a warp (tiny n) reduce serially on thread 0.
+        const int nred = sd->red_count;
         const bool narrow = blockDim.x < 32;
         const int lane = narrow ? 0 : (threadIdx.x & 31);
         const int warp = narrow ? (threadIdx.x == 0 ? 0 : 1 << 30) : (threadIdx.x >> 5);
         const int nwarp = narrow ? 1 : (blockDim.x >> 5);
-        const int total = nout * grp.S;
-        for (int task = warp; task < total; task += nwarp) {
+        for (int task = warp; task < nred * grp.S; task += nwarp) {
+          const int slot = task / grp.S, s_ = task - slot * grp.S;
+          const double* base = s_red + slot * (int)blockDim.x + s_ * grp.TT;
+          double v = 0.0;
+          if (narrow) {
+            for (int t = 0; t < grp.TT; ++t) v += base[t];
+          } else {
+            for (int t = lane; t < grp.TT; t += 32) v += base[t];
+            for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+          }
+          if (lane == 0) s_fin[slot * grp.S + s_] = v;
+        }
+        __syncthreads();
+        for (int task = threadIdx.x; task < nout * grp.S; task += blockDim.x) {
           const int oi = task / grp.S, s_ = task - oi * grp.S;
           const IpOut io = D.ipouts[sd->ip_begin + oi];
-          const double* base = s_red + s_ * grp.TT;
-          auto red = [&](int slot) {
-            double v = 0.0;
-            if (narrow) {
-              for (int t = 0; t < grp.TT; ++t) v += base[slot * (int)blockDim.x + t];
-              return v;
-            }
-            for (int t = lane; t < grp.TT; t += 32) v += base[slot * (int)blockDim.x + t];
-            for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-            return v;
-          };
+          const double* r = s_fin + s_;
           double v;
           if (io.avec < 0) {
-            v = red(io.red);
+            v = r[io.red * grp.S];
           } else {
             const double* av = s_av_all + (size_t)s_ * av_stride + 4 * (io.avec - av_base);
-            const double r0 = red(io.red), r1 = red(io.red + 1), r2 = red(io.red + 2);
-            v = av[0] * r0 + av[1] * r1 + av[2] * r2;
+            v = av[0] * r[io.red * grp.S] + av[1] * r[(io.red + 1) * grp.S] + av[2] * r[(io.red + 2) * grp.S];
           }
           const int64_t bl = bl0 + s_;
-          if (lane == 0 && bl < A.nb) A.ip[(((bl * A.K) + bra) * D.NG + io.gslot) * n_tiles + tile] = v;
+          if (bl < A.nb) A.ip[(((bl * A.K) + bra) * D.NG + io.gslot) * n_tiles + tile] = v;
         }
-        __syncthreads();  // the reduction buffer is reused by the next segment
       }
     }
+    dbg_add(A, DBG_SEG_FINAL, tdbg);
   }
 }
 

@@ -395,3 +395,48 @@ int sim_run(int n, int64_t G, const int64_t* kinds, const int64_t* q0, const int
 }
 
 }  // extern "C"
+
+extern "C" {
+// Debug: print the lowered program (op codes per segment) to stdout.
+int sim_dump(int n, int64_t G, const int64_t* kinds, const int64_t* q0, const int64_t* q1,
+             const double* coeff, const int64_t* f_offs, const int64_t* f_idx, int64_t total_params,
+             const int64_t* wrt_col, int tile_qubits, int smem_max_qubits, int reg_slots) {
+  std::vector<GateIn> gates((size_t)G);
+  for (int64_t g = 0; g < G; ++g) {
+    gates[g].kind = (int)kinds[g];
+    gates[g].q0 = (int)q0[g];
+    gates[g].q1 = (int)q1[g];
+    gates[g].coeff = coeff[g];
+    if (kinds[g] <= 2)
+      for (int64_t t = f_offs[g]; t < f_offs[g + 1]; ++t) gates[g].fidx.push_back((int32_t)f_idx[t]);
+  }
+  std::vector<int64_t> wc(wrt_col, wrt_col + total_params);
+  ScheduleOptions opt;
+  opt.tile_qubits = tile_qubits;
+  opt.smem_max_qubits = smem_max_qubits;
+  opt.reg_slots = reg_slots;
+  HostProgram P;
+  std::string e = build_program(gates, n, total_params, wc, opt, &P);
+  if (!e.empty()) { printf("error: %s\n", e.c_str()); return -1; }
+  static const char* names[] = {"RX","RY","RZ","CNOT","H","X","CZ","IPX","IPY","IPZ","U2","IP3","CZRUN","U2SET","IP3SET","PUB"};
+  for (size_t pi = 0; pi < P.passes.size(); ++pi) {
+    const PassDesc& pd = P.passes[pi];
+    printf("pass %zu local=%x\n", pi, pd.local_mask);
+    for (int sg = pd.seg_begin; sg < pd.seg_end; ++sg) {
+      const SegDesc& sd = P.segs[sg];
+      printf("  fseg regs=");
+      for (int s = 0; s < sd.nreg; ++s) printf("%d,", sd.reg_g[s]);
+      printf(" ops:");
+      for (int o = sd.op_begin; o < sd.op_end; ++o) printf(" %s", names[op_code(P.ops[o].w0)]);
+      printf("\n");
+    }
+    for (int sg = pd.bseg_begin; sg < pd.bseg_end; ++sg) {
+      const SegDesc& sd = P.segs[sg];
+      printf("  bseg ops:");
+      for (int o = sd.op_begin; o < sd.op_end; ++o) printf(" %s", names[op_code(P.ops[o].w0)]);
+      printf("  (ipouts %d red %d)\n", sd.ip_count, sd.red_count);
+    }
+  }
+  return 0;
+}
+}
