@@ -182,8 +182,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 // One pass over HBM-resident states: CTA (tile, row) stages 2^k amplitudes.
 template <int R, int KM>
-__global__ void __launch_bounds__(R >= 5 ? 128 : (R >= 4 ? 256 : 512), R >= 4 ? 2 : 1)
-    k_pass(DevProgram D, RunArgs A) {
+__global__ void __launch_bounds__(R >= 5 ? 256 : 512, 1) k_pass(DevProgram D, RunArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr bool ADJ = KM != KM_FWD;
   const PassDesc* pd = D.passes + A.pass;

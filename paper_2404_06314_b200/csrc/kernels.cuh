@@ -798,16 +798,18 @@ __device__ __forceinline__ TileWalk tile_walk(const PassDesc* pd, uint32_t tile_
   return w;
 }
 
-// calls f(l, j) for every element of this thread: l tile-local, j global
+// calls f(l, j) for every element of this thread: l tile-local, j global.
+// Kept as a rolled loop (the element index bits select hi[] entries with
+// constant indices) so call sites stay small in the instruction cache.
 template <class F>
 __device__ __forceinline__ void for_tile(const TileWalk& w, int lane, int stride, F&& f) {
-  uint32_t j = w.base;
+#pragma unroll 1
+  for (int i = 0; i < w.count; ++i) {
+    uint32_t j = w.base;
 #pragma unroll
-  for (int i = 0; i < (1 << kMaxR); ++i) {
-    if (i >= w.count) break;
-    if (i) j ^= w.hi[ctz_const(i)];
-    const uint32_t g = (uint32_t)(i ^ (i >> 1));
-    f((uint32_t)lane + g * (uint32_t)stride, j);
+    for (int b = 0; b < kMaxR; ++b)
+      if ((i >> b) & 1) j ^= w.hi[b];
+    f((uint32_t)lane + (uint32_t)i * (uint32_t)stride, j);
   }
 }
 
