@@ -778,9 +778,14 @@ struct TileWalk {
   int count;  // elements per thread: 2^k / stride = 2^R <= 16
 };
 
-__device__ __forceinline__ uint32_t dep_local(const PassDesc& pd, uint32_t l, int k) {
+// pdep of tile-local index bits into the pass's global qubit positions
+// (visits only the set bits of l)
+__device__ __forceinline__ uint32_t dep_local(const PassDesc& pd, uint32_t l) {
   uint32_t j = 0;
-  for (int p = 0; p < k; ++p) j |= ((l >> p) & 1u) << pd.local_q[p];
+  while (l) {
+    j |= 1u << pd.local_q[__ffs(l) - 1];
+    l &= l - 1;
+  }
   return j;
 }
 
@@ -789,11 +794,12 @@ __device__ __forceinline__ TileWalk tile_walk(const PassDesc* pd, uint32_t tile_
   TileWalk w;
   const int Nt = 1 << k;
   w.count = Nt / stride;
-  w.base = tile_base | (pd ? dep_local(*pd, (uint32_t)lane, k) : (uint32_t)lane);
+  w.base = tile_base | (pd ? dep_local(*pd, (uint32_t)lane) : (uint32_t)lane);
+  const int s0 = __ffs(stride) - 1;  // stride is a power of two: hi[b] is one local bit
 #pragma unroll
   for (int b = 0; b < kMaxR; ++b) {
-    const uint32_t s = (uint32_t)stride << b;
-    w.hi[b] = s < (uint32_t)Nt ? (pd ? dep_local(*pd, s, k) : s) : 0u;
+    const int p = s0 + b;
+    w.hi[b] = p < k ? (pd ? (1u << pd->local_q[p]) : (1u << p)) : 0u;
   }
   return w;
 }
@@ -814,11 +820,7 @@ __device__ __forceinline__ void for_tile(const TileWalk& w, int lane, int stride
 }
 
 // global index of tile-local element l (pdep of l into the pass's local qubits)
-__device__ __forceinline__ uint32_t local_to_global(const PassDesc& pd, uint32_t l, int k) {
-  uint32_t j = 0;
-  for (int p = 0; p < k; ++p) j |= ((l >> p) & 1u) << pd.local_q[p];
-  return j;
-}
+
 
 // Z-string signs and weights for global index j over terms [lo, hi)
 __device__ __forceinline__ double zweight(const DevProgram& D, uint32_t j, int lo, int hi) {
