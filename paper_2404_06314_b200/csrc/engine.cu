@@ -851,6 +851,7 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
   VqcPlan* p = new VqcPlan();
   ScheduleOptions opt;
   opt.tile_qubits = env_int("VQC_TILE_QUBITS", 11);
+  opt.segment_cost = env_int("VQC_SEGMENT_COST", 4);
   opt.reg_slots = std::max(3, std::min(kMaxR, env_int("VQC_REG_SLOTS", 4)));
   // five register slots only where the adjoint runs split (one state per
   // thread); the dual-state layout would need 256 state registers

@@ -114,13 +114,17 @@ std::string analyze(const std::vector<GateIn>& gates, int n, int64_t total_param
 // address maps instead of costing register permutations.
 std::vector<Group> greedy_groups(const std::vector<int>& todo, const std::vector<GateInfo>& info,
                                  int cap, uint32_t forced, std::vector<uint8_t>& status,
-                                 bool fold_cnots = false) {
+                                 bool fold_cnots = false, int variants = 1) {
   std::vector<Group> groups;
   std::vector<int> remaining = todo;
-  while (!remaining.empty()) {
-    Group grp;
+  // One scan of `remaining`: variant v refuses the first v requests for new
+  // local qubits, so later (often better-packed) qubit sets get a chance.
+  // status 2 = taken by this scan, 3 = blocked; both reset by the caller.
+  auto scan = [&](int v, Group& grp) {
+    grp = Group();
     grp.mask = forced;
     int phase = 0;  // 0 leading CNOTs, 1 body, 2 trailing CNOTs
+    int refused = 0;
     for (int g : remaining) {
       bool ok = true;
       for (int p : info[g].preds)
@@ -128,7 +132,10 @@ std::vector<Group> greedy_groups(const std::vector<int>& todo, const std::vector
       if (ok && fold_cnots && phase == 2 && !info[g].cnot) ok = false;
       if (ok) {
         const uint32_t m = grp.mask | info[g].mix;
-        if (popc(m) <= cap) {
+        if (m != grp.mask && refused < v) {
+          ++refused;
+          ok = false;
+        } else if (popc(m) <= cap) {
           grp.mask = m;
           status[g] = 2;
           grp.gates.push_back(g);
@@ -140,12 +147,34 @@ std::vector<Group> greedy_groups(const std::vector<int>& todo, const std::vector
       }
       if (!ok) status[g] = 3;
     }
+  };
+  auto score = [&](const Group& grp) {
+    int sc = 0;
+    for (int g : grp.gates) sc += info[g].rot ? 4 : 1;
+    return sc;
+  };
+  while (!remaining.empty()) {
+    Group best;
+    int best_v = 0, best_score = -1;
+    for (int v = 0; v < variants; ++v) {
+      Group grp;
+      scan(v, grp);
+      const int sc = grp.gates.empty() ? -1 : score(grp);
+      if (sc > best_score) {
+        best_score = sc;
+        best_v = v;
+        best = grp;
+      }
+      for (int g : remaining) status[g] = 0;
+    }
+    if (best.gates.empty()) return {};  // cannot happen when cap >= popc(forced) + 1
+    Group grp;
+    scan(best_v, grp);
     std::vector<int> next;
     for (int g : remaining) {
       if (status[g] == 2) status[g] = 1;
       else { status[g] = 0; next.push_back(g); }
     }
-    if (grp.gates.empty()) return {};  // cannot happen when cap >= popc(forced) + 1
     groups.push_back(std::move(grp));
     remaining.swap(next);
   }
@@ -183,7 +212,7 @@ std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total
   std::vector<Group> passes;
   if (P->hbm) {
     const uint32_t forced = (1u << opt.forced_low) - 1u;
-    passes = greedy_groups(todo, info, k, forced, status);
+    passes = greedy_groups(todo, info, k, forced, status, false, opt.variants);
     if (G > 0 && passes.empty()) return "pass scheduling failed";
   } else {
     Group all;
@@ -218,9 +247,33 @@ std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total
     pd.av_begin = P->n_av;
 
     // ---- level 2: register segments inside the tile ----
-    std::vector<uint8_t> st2(G, 1);
-    for (int g : pg.gates) st2[g] = 0;
-    std::vector<Group> segs = greedy_groups(pg.gates, info, R, 0u, st2, true);
+    // Two policies, priced per pass: segments shaped [CNOTs][body][CNOTs]
+    // (every CNOT folds into address maps, but more segments), or free
+    // placement (interior CNOTs become register permutations). A segment
+    // boundary costs a shared-memory round trip of the tile; an interior
+    // CNOT a few dozen register moves/selects per thread.
+    auto interior_cnots = [&](const std::vector<Group>& gs) {
+      int cost = 0;
+      for (const Group& gr : gs) {
+        size_t a = 0, b = gr.gates.size();
+        while (a < b && info[gr.gates[a]].cnot) ++a;
+        while (b > a && info[gr.gates[b - 1]].cnot) --b;
+        for (size_t i = a; i < b; ++i) cost += info[gr.gates[i]].cnot ? 1 : 0;
+      }
+      return cost;
+    };
+    std::vector<Group> segs;
+    {
+      std::vector<uint8_t> st2(G, 1);
+      for (int g : pg.gates) st2[g] = 0;
+      std::vector<Group> folded = greedy_groups(pg.gates, info, R, 0u, st2, true, opt.variants);
+      for (int g : pg.gates) st2[g] = 0;
+      std::vector<Group> free_ = greedy_groups(pg.gates, info, R, 0u, st2, false, opt.variants);
+      const int seg_cost = opt.segment_cost, cnot_cost = 1;
+      const int c_fold = (int)folded.size() * seg_cost + interior_cnots(folded) * cnot_cost;
+      const int c_free = (int)free_.size() * seg_cost + interior_cnots(free_) * cnot_cost;
+      segs = (c_free < c_fold) ? std::move(free_) : std::move(folded);
+    }
     if (!pg.gates.empty() && segs.empty()) return "segment scheduling failed";
 
     struct Item {

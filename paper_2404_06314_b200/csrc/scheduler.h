@@ -22,6 +22,8 @@ struct ScheduleOptions {
   int reg_slots = 4;         // R
   int forced_low = 3;        // qubits 0..forced_low-1 always local in HBM passes
   int smem_max_qubits = kSmemMaxQubits;  // n above this streams tiles through HBM
+  int segment_cost = 4;      // price of a segment boundary in interior-CNOT units
+  int variants = 1;          // greedy restarts per group (refuse the first v new-qubit requests)
 };
 
 struct HostProgram {

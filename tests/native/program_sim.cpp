@@ -427,8 +427,26 @@ int sim_dump(int n, int64_t G, const int64_t* kinds, const int64_t* q0, const in
       printf("  fseg regs=");
       for (int s = 0; s < sd.nreg; ++s) printf("%d,", sd.reg_g[s]);
       printf(" ops:");
-      for (int o = sd.op_begin; o < sd.op_end; ++o) printf(" %s", names[op_code(P.ops[o].w0)]);
-      printf("\n");
+      for (int o = sd.op_begin; o < sd.op_end; ++o) {
+        const Op& op = P.ops[o];
+        printf(" %s", names[op_code(op.w0)]);
+        if (op_code(op.w0) == OP_U2SET) {
+          printf("[");
+          for (int s2 = 0; s2 < kMaxR; ++s2) {
+            const int id = P.setids[op.param * kMaxR + s2];
+            if (id >= 0) {
+              const BlockDesc& bd = P.blocks[pd.blk_begin + id];
+              printf("q%d:%d ", sd.reg_g[s2], bd.mem_end - bd.mem_begin);
+            }
+          }
+          printf("]");
+        } else if (op_code(op.w0) == OP_U2) {
+          const BlockDesc& bd = P.blocks[op.param];
+          printf("[q%d:%d]", (op_a(op.w0) & kSlotFlag) ? sd.reg_g[op_a(op.w0) & 7] : -1, bd.mem_end - bd.mem_begin);
+        }
+      }
+      printf("  ldmap=%s stmap=%s\n", (sd.ld_col[0] == 1 && sd.ld_col[1] == 2 && !sd.ld_k[0] && !sd.ld_k[1] && !sd.ld_k[2] && !sd.ld_k[3]) ? "id" : "cnot",
+             (sd.st_col[0] == 1 && sd.st_col[1] == 2 && !sd.st_k[0] && !sd.st_k[1] && !sd.st_k[2] && !sd.st_k[3]) ? "id" : "cnot");
     }
     for (int sg = pd.bseg_begin; sg < pd.bseg_end; ++sg) {
       const SegDesc& sd = P.segs[sg];
