@@ -19,64 +19,116 @@ namespace vqc {
 
 // ------------------------------------------------------------------ kernels
 
+// Observable terms staged in shared memory (Z strings only on this path).
+struct TermSm {
+  uint32_t mask;  // sign mask
+  int32_t obs;    // observable index
+  double coeff;
+};
+
+__device__ __forceinline__ void stage_terms(const DevProgram& D, TermSm* s_terms) {
+  for (int t = threadIdx.x; t < D.T; t += blockDim.x) {
+    TermSm ts;
+    ts.mask = D.t_smask[t];
+    ts.coeff = D.t_coeff[t];
+    int m = 0;
+    while (D.term_offs[m + 1] <= t) ++m;
+    ts.obs = m;
+    s_terms[t] = ts;
+  }
+}
+
+// Expectations (observables.py / _kernels.py:182-198, Z strings) and the
+// adjoint seed phi = w(j) psi with w = sum_m u_m O_m(j) (VJP) or O_bra(j)
+// (_kernels.py:209-217). Each thread owns `count` tile elements; a term's
+// sign over them is parity(base & s) ^ parity(i & h), h bit b =
+// parity(hi[b] & s), so no per-element index arithmetic is needed.
 template <bool DUAL>
 __device__ __forceinline__ void observe(const DevProgram& D, const RunArgs& A, const PassDesc* pd, double2* s_psi,
-                        double2* s_phi, const double* s_u_row, const Group& grp, double* s_red,
-                        uint32_t tile_base, int k, int64_t bl0, bool do_expect,
-                        int seed_mode, int bra, int tile, int n_tiles) {
-  const int Nt = 1 << k;
+                                        double2* s_phi, const double* s_u_row, const TermSm* s_terms,
+                                        const Group& grp, double* s_red, double* s_fin, uint32_t tile_base, int k,
+                                        int64_t bl0, bool do_expect, int seed_mode, int bra, int tile,
+                                        int n_tiles) {
+  constexpr int E = 1 << kMaxR;
+  const int lane = grp.lane_in_sample();
+  const TileWalk tw = tile_walk(pd, tile_base, k, lane, grp.TT);
+  const int count = tw.count;
+  auto term_bits = [&](uint32_t mask, uint32_t& p0, uint32_t& h) {
+    p0 = (uint32_t)__popc(tw.base & mask) & 1u;
+    h = 0;
+#pragma unroll
+    for (int b = 0; b < kMaxR; ++b) h |= ((uint32_t)__popc(tw.hi[b] & mask) & 1u) << b;
+  };
   if (do_expect) {
-    double* redbuf = s_red;
-    const int lane = grp.lane_in_sample();
-    const TileWalk tw = tile_walk(pd, tile_base, k, lane, grp.TT);
-    for (int m = 0; m < D.M; ++m) {
-      const int lo = D.term_offs[m], hi = D.term_offs[m + 1];
-      double acc = 0.0;
-      for_tile(tw, lane, grp.TT, [&](uint32_t l, uint32_t j) {
-        const double2 x = s_psi[swz(l)];
-        acc += zweight(D, j, lo, hi) * (x.x * x.x + x.y * x.y);
-      });
-      acc = grp.reduce(acc);
-      if (grp.leader()) redbuf[grp.red_index(m)] = acc;
+    double p2[E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      p2[i] = 0.0;
+      if (i < count) {
+        const double2 x = s_psi[swz((uint32_t)lane + (uint32_t)i * (uint32_t)grp.TT)];
+        p2[i] = x.x * x.x + x.y * x.y;
+      }
+    }
+    for (int m = 0; m < D.M; ++m) s_red[m * (int)blockDim.x + threadIdx.x] = 0.0;
+    for (int t = 0; t < D.T; ++t) {
+      const TermSm ts = s_terms[t];
+      uint32_t p0, h;
+      term_bits(ts.mask, p0, h);
+      double v = 0.0;
+#pragma unroll
+      for (int i = 0; i < E; ++i)
+        if (i < count) v += ((p0 ^ (uint32_t)__popc((uint32_t)i & h)) & 1u) ? -p2[i] : p2[i];
+      s_red[ts.obs * (int)blockDim.x + threadIdx.x] += ts.coeff * v;
     }
     __syncthreads();
-    const int total = D.M * grp.S;
-    for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-      const int m = idx / grp.S, s_ = idx - m * grp.S;
+    const int warp = threadIdx.x >> 5, lane32 = threadIdx.x & 31, nwarp = (blockDim.x + 31) >> 5;
+    const bool narrow = blockDim.x < 32;
+    for (int task = warp; task < D.M * grp.S; task += nwarp) {
+      const int m = task / grp.S, s_ = task - m * grp.S;
+      const double* base = s_red + m * (int)blockDim.x + s_ * grp.TT;
       double v = 0.0;
-      for (int w = 0; w < grp.W; ++w) v += redbuf[(m * grp.S + s_) * grp.W + w];
+      if (narrow) {
+        if (lane32 == 0)
+          for (int t = 0; t < grp.TT; ++t) v += base[t];
+      } else {
+        for (int t = lane32; t < grp.TT; t += 32) v += base[t];
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      }
       const int64_t bl = bl0 + s_;
-      if (bl < A.nb) A.expect[(bl * D.M + m) * n_tiles + tile] = v;
+      if (lane32 == 0 && bl < A.nb) A.expect[(bl * D.M + m) * n_tiles + tile] = v;
     }
     __syncthreads();
   }
   if constexpr (DUAL) {
     if (seed_mode != 0) {
-      const int lane = grp.lane_in_sample();
-      const TileWalk tw = tile_walk(pd, tile_base, k, lane, grp.TT);
-      for_tile(tw, lane, grp.TT, [&](uint32_t l, uint32_t j) {
-        double w = 0.0;
-        if (seed_mode == 1) {
-          for (int m = 0; m < D.M; ++m) {
-            const double u = s_u_row[m];
-            if (u != 0.0) w += u * zweight(D, j, D.term_offs[m], D.term_offs[m + 1]);
-          }
-        } else {
-          w = zweight(D, j, D.term_offs[bra], D.term_offs[bra + 1]);
-        }
-        const uint32_t p = swz(l);
+      double w[E];
+#pragma unroll
+      for (int i = 0; i < E; ++i) w[i] = 0.0;
+      for (int t = 0; t < D.T; ++t) {
+        const TermSm ts = s_terms[t];
+        const double e = seed_mode == 1 ? s_u_row[ts.obs] * ts.coeff : (ts.obs == bra ? ts.coeff : 0.0);
+        if (e == 0.0) continue;
+        uint32_t p0, h;
+        term_bits(ts.mask, p0, h);
+#pragma unroll
+        for (int i = 0; i < E; ++i) w[i] += ((p0 ^ (uint32_t)__popc((uint32_t)i & h)) & 1u) ? -e : e;
+      }
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        if (i >= count) break;
+        const uint32_t p = swz((uint32_t)lane + (uint32_t)i * (uint32_t)grp.TT);
         const double2 x = s_psi[p];
-        s_phi[p] = make_double2(w * x.x, w * x.y);
-      });
+        s_phi[p] = make_double2(w[i] * x.x, w[i] * x.y);
+      }
     }
   }
 }
 
 // Shared-memory carve-up (kernels and host sizing must agree).
 struct SmemLayout {
-  size_t psi, phi, cs, u, av, red, fin, up, total;  // byte offsets
+  size_t psi, phi, cs, u, av, red, fin, up, terms, total;  // byte offsets
   __host__ __device__ SmemLayout(int S, int n_amp, bool dual, int nrot, int nblk, int nav, int red_slots,
-                                 int threads, int M) {
+                                 int threads, int M, int n_terms) {
     size_t o = 0;
     psi = o; o += (size_t)S * n_amp * 16;
     phi = o; o += dual ? (size_t)S * n_amp * 16 : 0;
@@ -86,6 +138,7 @@ struct SmemLayout {
     red = o; o += (size_t)red_slots * threads * 8;
     fin = o; o += (size_t)red_slots * S * 8;
     up = o; o += (size_t)S * M * 8;
+    terms = o; o += (size_t)n_terms * sizeof(TermSm);
     total = o + 16;
   }
 };
@@ -126,7 +179,7 @@ __global__ void __launch_bounds__(R >= 5 ? 256 : (KM == KM_SPLIT ? 512 : (R >= 4
   const int64_t b = A.b0 + (valid ? bl : 0);
   const PassDesc* pd = D.passes;
   const int nrot = D.n_rot, nblk = D.n_blk, nav = D.n_av;
-  const SmemLayout L(A.S, N, ADJ, nrot, nblk, nav, A.red_slots, (int)blockDim.x, D.M);
+  const SmemLayout L(A.S, N, ADJ, nrot, nblk, nav, A.red_slots, (int)blockDim.x, D.M, D.T);
   double2* s_psi = reinterpret_cast<double2*>(smem_raw + L.psi) + (size_t)grp.sl * N;
   double2* s_phi = reinterpret_cast<double2*>(smem_raw + L.phi) + (size_t)grp.sl * N;
   double2* s_cs = reinterpret_cast<double2*>(smem_raw + L.cs) + (size_t)grp.sl * nrot;
@@ -135,6 +188,8 @@ __global__ void __launch_bounds__(R >= 5 ? 256 : (KM == KM_SPLIT ? 512 : (R >= 4
   double* s_red = reinterpret_cast<double*>(smem_raw + L.red);
   double* s_fin = reinterpret_cast<double*>(smem_raw + L.fin);
   double* s_up = reinterpret_cast<double*>(smem_raw + L.up);
+  TermSm* s_terms = reinterpret_cast<TermSm*>(smem_raw + L.terms);
+  stage_terms(D, s_terms);
 
   for (int l = lane; l < N; l += grp.TT) s_psi[swz((uint32_t)l)] = make_double2(l == 0 ? 1.0 : 0.0, 0.0);
   if (ADJ && A.upstream != nullptr)
@@ -145,16 +200,16 @@ __global__ void __launch_bounds__(R >= 5 ? 256 : (KM == KM_SPLIT ? 512 : (R >= 4
   run_segments<R, MODE_FWD>(D, A, pd->seg_begin, pd->seg_end, s_psi, s_psi, T, s_av_all, nav * 4, 0, s_red, s_fin,
                             grp, grp.role == 0, 0u, bl0, 0, 0, 1);
   if constexpr (!ADJ) {
-    observe<false>(D, A, nullptr, s_psi, s_psi, nullptr, grp, s_red, 0u, n, bl0, true, 0, 0, 0, 1);
+    observe<false>(D, A, nullptr, s_psi, s_psi, nullptr, s_terms, grp, s_red, s_fin, 0u, n, bl0, true, 0, 0, 0, 1);
   } else {
     if (!A.jacobian) {
-      observe<true>(D, A, nullptr, s_psi, s_phi, s_up + grp.sl * D.M, grp, s_red, 0u, n, bl0,
+      observe<true>(D, A, nullptr, s_psi, s_phi, s_up + grp.sl * D.M, s_terms, grp, s_red, s_fin, 0u, n, bl0,
                     A.expect != nullptr, 1, 0, 0, 1);
       __syncthreads();
       run_segments<R, BM>(D, A, pd->bseg_begin, pd->bseg_end, s_psi, s_phi, T, s_av_all, nav * 4, 0, s_red, s_fin,
                           grp, true, 0u, bl0, 0, 0, 1);
     } else {
-      observe<true>(D, A, nullptr, s_psi, s_phi, nullptr, grp, s_red, 0u, n, bl0,
+      observe<true>(D, A, nullptr, s_psi, s_phi, nullptr, s_terms, grp, s_red, s_fin, 0u, n, bl0,
                     A.expect != nullptr, 0, 0, 0, 1);
       double2* fin = A.psi_fin + (size_t)bl * N;
       if (D.M > 1 && valid)
@@ -165,7 +220,8 @@ __global__ void __launch_bounds__(R >= 5 ? 256 : (KM == KM_SPLIT ? 512 : (R >= 4
           if (valid)
             for (int l = lane; l < N; l += grp.TT) s_psi[swz((uint32_t)l)] = fin[l];
         }
-        observe<true>(D, A, nullptr, s_psi, s_phi, nullptr, grp, s_red, 0u, n, bl0, false, 2, m, 0, 1);
+        observe<true>(D, A, nullptr, s_psi, s_phi, nullptr, s_terms, grp, s_red, s_fin, 0u, n, bl0, false, 2, m,
+                      0, 1);
         __syncthreads();
         run_segments<R, BM>(D, A, pd->bseg_begin, pd->bseg_end, s_psi, s_phi, T, s_av_all, nav * 4, 0,
                             s_red, s_fin, grp, true, 0u, bl0, m, 0, 1);
@@ -201,7 +257,7 @@ __global__ void __launch_bounds__(R >= 5 ? 256 : 512, 1) k_pass(DevProgram D, Ru
       if (!((lm >> q) & 1u)) tile_base |= (((uint32_t)tile >> c++) & 1u) << q;
   }
   const SmemLayout L(1, Nt, ADJ, D.max_rot_pass, D.max_blk_pass, D.max_av_pass, A.red_slots, (int)blockDim.x,
-                     D.M);
+                     D.M, D.T);
   double2* s_psi = reinterpret_cast<double2*>(smem_raw + L.psi);
   double2* s_phi = reinterpret_cast<double2*>(smem_raw + L.phi);
   double2* s_cs = reinterpret_cast<double2*>(smem_raw + L.cs);
@@ -210,6 +266,8 @@ __global__ void __launch_bounds__(R >= 5 ? 256 : 512, 1) k_pass(DevProgram D, Ru
   double* s_red = reinterpret_cast<double*>(smem_raw + L.red);
   double* s_fin = reinterpret_cast<double*>(smem_raw + L.fin);
   double* s_up = reinterpret_cast<double*>(smem_raw + L.up);
+  TermSm* s_terms = reinterpret_cast<TermSm*>(smem_raw + L.terms);
+  if (flags & (F_OBSERVE | F_SEED)) stage_terms(D, s_terms);
 
   long long tdbg = A.dbg ? clock64() : 0;
   if (A.dbg && threadIdx.x == 0) atomicAdd(A.dbg + DBG_CTAS, 1ull);
@@ -260,7 +318,7 @@ __global__ void __launch_bounds__(R >= 5 ? 256 : 512, 1) k_pass(DevProgram D, Ru
     for_tile(tw, threadIdx.x, blockDim.x, [&](uint32_t l, uint32_t j) { dst[j] = s_psi[swz(l)]; });
   }
   if (flags & (F_OBSERVE | F_SEED)) {
-    observe<ADJ>(D, A, pd, s_psi, s_phi, s_up, grp, s_red, tile_base, k, bl, (flags & F_OBSERVE) != 0,
+    observe<ADJ>(D, A, pd, s_psi, s_phi, s_up, s_terms, grp, s_red, s_fin, tile_base, k, bl, (flags & F_OBSERVE) != 0,
                  (flags & F_SEED) ? (A.bra < 0 ? 1 : 2) : 0, A.bra, tile, n_tiles);
     __syncthreads();
   }
@@ -568,7 +626,8 @@ int smem_samples(const VqcPlan* p, int64_t B, bool dual, size_t* smem_bytes, int
   const int TT = split ? 2 * TPS : TPS;
   *threads_per_sample = TT;
   auto bytes_for = [&](int S) {
-    return SmemLayout(S, 1 << P.n, dual, P.n_rot, P.n_blk, P.n_av, red_slots(p), S * TT, p->M).total;
+    return SmemLayout(S, 1 << P.n, dual, P.n_rot, P.n_blk, P.n_av, red_slots(p), S * TT, p->M,
+                      (int)p->smask.size()).total;
   };
   const int max_threads = P.R >= 5 ? 256 : (split ? 512 : (P.R >= 4 ? 256 : 512));
   int smax = std::max(1, max_threads / TT);
@@ -583,7 +642,7 @@ size_t pass_smem(const VqcPlan* p, bool dual) {
   const HostProgram& P = p->prog;
   const int TPS = 1 << (P.k - P.R);
   return SmemLayout(1, 1 << P.k, dual, P.max_rot_per_pass, P.max_blk_per_pass, P.max_av_per_pass,
-                    red_slots(p), dual ? 2 * TPS : TPS, p->M).total;
+                    red_slots(p), dual ? 2 * TPS : TPS, p->M, (int)p->smask.size()).total;
 }
 
 int launch(const char* name, KFn fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
@@ -936,6 +995,7 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
   D.NG = P.NG;
   D.n_rot = P.n_rot;
   D.M = p->M;
+  D.T = (int)p->smask.size();
   D.n_pass = (int)P.passes.size();
   D.enc_off = p->enc_off;
   D.enc_size = p->enc_size;

@@ -34,6 +34,7 @@ struct DevProgram {
   const double* t_coeff;     // T (coeff * Re(phase); Z strings only)
   int n, k, R, NG, n_rot, M, n_pass;
   int n_blk, n_av, max_rot_pass, max_blk_pass, max_av_pass;
+  int T;  // observable terms
   int64_t enc_off, enc_size;
 };
 
