@@ -69,8 +69,9 @@ typedef struct {
 } VqcCircuit;
 
 /* observables.py:132-167 (ObservablePack): M observables, T terms total;
- * phases are (T, 2) re/im of i^{#Y}. This path supports Z strings
- * (x_mask == 0) and returns VQC_E_UNSUPPORTED otherwise. */
+ * phases are (T, 2) re/im of i^{#Y}. Z strings (x_mask == 0) run on every
+ * path; X/Y strings on the on-chip path (n <= 12) — vqc_plan_create returns
+ * VQC_E_UNSUPPORTED for them when n > 12. */
 typedef struct {
   int64_t n_obs;
   const int64_t* term_offs;  /* n_obs + 1 */

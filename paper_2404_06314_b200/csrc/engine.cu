@@ -21,8 +21,10 @@ namespace vqc {
 
 // Observable terms staged in shared memory (Z strings only on this path).
 struct TermSm {
-  uint32_t mask;  // sign mask
-  int32_t obs;    // observable index
+  uint32_t mask;   // sign mask (Y/Z letters)
+  int32_t obs;     // observable index
+  uint32_t xmask;  // flip mask (X/Y letters); 0 for Z strings
+  int32_t phase;   // i^phase = i^{#Y}
   double coeff;
 };
 
@@ -30,6 +32,8 @@ __device__ __forceinline__ void stage_terms(const DevProgram& D, TermSm* s_terms
   for (int t = threadIdx.x; t < D.T; t += blockDim.x) {
     TermSm ts;
     ts.mask = D.t_smask[t];
+    ts.xmask = D.t_xmask[t];
+    ts.phase = D.t_phase[t];
     ts.coeff = D.t_coeff[t];
     int m = 0;
     while (D.term_offs[m + 1] <= t) ++m;
@@ -72,6 +76,7 @@ __device__ __forceinline__ void observe(const DevProgram& D, const RunArgs& A, c
     for (int m = 0; m < D.M; ++m) s_red[m * (int)blockDim.x + threadIdx.x] = 0.0;
     for (int t = 0; t < D.T; ++t) {
       const TermSm ts = s_terms[t];
+      if (ts.xmask != 0u) continue;
       uint32_t p0, h;
       term_bits(ts.mask, p0, h);
       double v = 0.0;
@@ -79,6 +84,25 @@ __device__ __forceinline__ void observe(const DevProgram& D, const RunArgs& A, c
       for (int i = 0; i < E; ++i)
         if (i < count) v += ((p0 ^ (uint32_t)__popc((uint32_t)i & h)) & 1u) ? -p2[i] : p2[i];
       s_red[ts.obs * (int)blockDim.x + threadIdx.x] += ts.coeff * v;
+    }
+    if (D.has_xy) {
+      // X/Y strings (on-chip states only): Re sum_j conj(psi_j) i^k (-1)^{popc((j^x)&s)} psi_{j^x}
+      for (int t = 0; t < D.T; ++t) {
+        const TermSm ts = s_terms[t];
+        if (ts.xmask == 0u) continue;
+        double v = 0.0;
+        for (int i = 0; i < count; ++i) {
+          const uint32_t l = (uint32_t)lane + (uint32_t)i * (uint32_t)grp.TT;
+          const uint32_t kx = l ^ ts.xmask;
+          const double2 a = s_psi[swz(l)], bq = s_psi[swz(kx)];
+          // conj(a) * bq
+          double re = a.x * bq.x + a.y * bq.y, im = a.x * bq.y - a.y * bq.x;
+          const int ph = ts.phase & 3;  // multiply by i^ph, keep the real part
+          double r = ph == 0 ? re : ph == 1 ? -im : ph == 2 ? -re : im;
+          v += (__popc(kx & ts.mask) & 1) ? -r : r;
+        }
+        s_red[ts.obs * (int)blockDim.x + threadIdx.x] += ts.coeff * v;
+      }
     }
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane32 = threadIdx.x & 31, nwarp = (blockDim.x + 31) >> 5;
@@ -106,6 +130,7 @@ __device__ __forceinline__ void observe(const DevProgram& D, const RunArgs& A, c
       for (int i = 0; i < E; ++i) w[i] = 0.0;
       for (int t = 0; t < D.T; ++t) {
         const TermSm ts = s_terms[t];
+        if (ts.xmask != 0u) continue;
         const double e = seed_mode == 1 ? s_u_row[ts.obs] * ts.coeff : (ts.obs == bra ? ts.coeff : 0.0);
         if (e == 0.0) continue;
         uint32_t p0, h;
@@ -116,9 +141,28 @@ __device__ __forceinline__ void observe(const DevProgram& D, const RunArgs& A, c
 #pragma unroll
       for (int i = 0; i < E; ++i) {
         if (i >= count) break;
-        const uint32_t p = swz((uint32_t)lane + (uint32_t)i * (uint32_t)grp.TT);
+        const uint32_t l = (uint32_t)lane + (uint32_t)i * (uint32_t)grp.TT;
+        const uint32_t p = swz(l);
         const double2 x = s_psi[p];
-        s_phi[p] = make_double2(w[i] * x.x, w[i] * x.y);
+        double2 phi = make_double2(w[i] * x.x, w[i] * x.y);
+        if (D.has_xy) {
+          // pauli_sum_apply (_kernels.py:166-179) for the X/Y strings
+          for (int t = 0; t < D.T; ++t) {
+            const TermSm ts = s_terms[t];
+            if (ts.xmask == 0u) continue;
+            const double e = seed_mode == 1 ? s_u_row[ts.obs] * ts.coeff : (ts.obs == bra ? ts.coeff : 0.0);
+            if (e == 0.0) continue;
+            const uint32_t kx = l ^ ts.xmask;
+            const double2 bq = s_psi[swz(kx)];
+            const int ph = ts.phase & 3;
+            double2 v = ph == 0 ? bq : ph == 1 ? make_double2(-bq.y, bq.x)
+                      : ph == 2 ? make_double2(-bq.x, -bq.y) : make_double2(bq.y, -bq.x);
+            const double sg = (__popc(kx & ts.mask) & 1) ? -e : e;
+            phi.x += sg * v.x;
+            phi.y += sg * v.y;
+          }
+        }
+        s_phi[p] = phi;
       }
     }
   }
@@ -539,8 +583,10 @@ struct VqcPlan {
   int64_t total_params = 0, enc_off = 0, enc_size = 0;
   int M = 0;
   std::vector<int32_t> term_offs;
-  std::vector<uint32_t> smask;
+  std::vector<uint32_t> smask, xmask;
+  std::vector<int32_t> tphase;
   std::vector<double> tcoeff;
+  bool has_xy = false;
   // device tables
   Op* d_ops = nullptr;
   SegDesc* d_segs = nullptr;
@@ -553,6 +599,8 @@ struct VqcPlan {
   RotDesc* d_rots = nullptr;
   int32_t* d_term_offs = nullptr;
   uint32_t* d_smask = nullptr;
+  uint32_t* d_xmask = nullptr;
+  int32_t* d_tphase = nullptr;
   double* d_tcoeff = nullptr;
   int32_t* d_col_offs = nullptr;
   ChainEntry* d_chain = nullptr;
@@ -933,20 +981,33 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
     const int64_t lo = obs->term_offs[m], hi = obs->term_offs[m + 1];
     if (lo < 0 || hi < lo) { delete p; return fail(VQC_E_INVALID, "bad term_offs"); }
     for (int64_t t = lo; t < hi; ++t) {
-      if (obs->x_masks[t] != 0) {
+      if (obs->x_masks[t] != 0 && c->n_qubits > kSmemMaxQubits) {
         delete p;
         return fail(VQC_E_UNSUPPORTED,
-                    "observable " + std::to_string(m) + ": X/Y Pauli strings are not supported on the GPU path "
-                    "(Z strings only)");
+                    "observable " + std::to_string(m) + ": X/Y Pauli strings are supported for n <= 12 only "
+                    "(Z strings only on the HBM path)");
+      }
+      if (obs->x_masks[t] < 0 || ((uint64_t)obs->x_masks[t] & ~(uint64_t)nmask)) {
+        delete p;
+        return fail(VQC_E_INVALID, "observable x mask out of range");
       }
       if (obs->sign_masks[t] < 0 || ((uint64_t)obs->sign_masks[t] & ~(uint64_t)nmask)) {
         delete p;
         return fail(VQC_E_INVALID, "observable sign mask out of range");
       }
+      // phase = i^{#Y}: recover the power from the (re, im) pair
       const double pr = obs->phases ? obs->phases[2 * t] : 1.0, pim = obs->phases ? obs->phases[2 * t + 1] : 0.0;
-      if (pr != 1.0 || pim != 0.0) { delete p; return fail(VQC_E_UNSUPPORTED, "non-unit phase on a Z string"); }
+      int ph = -1;
+      if (pr == 1.0 && pim == 0.0) ph = 0;
+      else if (pr == 0.0 && pim == 1.0) ph = 1;
+      else if (pr == -1.0 && pim == 0.0) ph = 2;
+      else if (pr == 0.0 && pim == -1.0) ph = 3;
+      if (ph < 0) { delete p; return fail(VQC_E_INVALID, "Pauli phase must be a power of i"); }
       p->smask.push_back((uint32_t)obs->sign_masks[t]);
+      p->xmask.push_back((uint32_t)obs->x_masks[t]);
+      p->tphase.push_back(ph);
       p->tcoeff.push_back(obs->coeffs[t]);
+      if (obs->x_masks[t] != 0) p->has_xy = true;
     }
     p->term_offs[m + 1] = (int32_t)p->smask.size();
   }
@@ -964,6 +1025,8 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
   if (e == cudaSuccess) e = upload(P.rots, &p->d_rots);
   if (e == cudaSuccess) e = upload(p->term_offs, &p->d_term_offs);
   if (e == cudaSuccess) e = upload(p->smask, &p->d_smask);
+  if (e == cudaSuccess) e = upload(p->xmask, &p->d_xmask);
+  if (e == cudaSuccess) e = upload(p->tphase, &p->d_tphase);
   if (e == cudaSuccess) e = upload(p->tcoeff, &p->d_tcoeff);
   if (e == cudaSuccess) e = upload(P.col_offs, &p->d_col_offs);
   if (e == cudaSuccess) e = upload(P.chain, &p->d_chain);
@@ -988,6 +1051,9 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
   D.rots = p->d_rots;
   D.term_offs = p->d_term_offs;
   D.t_smask = p->d_smask;
+  D.t_xmask = p->d_xmask;
+  D.t_phase = p->d_tphase;
+  D.has_xy = p->has_xy ? 1 : 0;
   D.t_coeff = p->d_tcoeff;
   D.n = P.n;
   D.k = P.k;
@@ -1017,6 +1083,8 @@ void vqc_plan_destroy(VqcPlan* p) {
   cudaFree(p->d_rots);
   cudaFree(p->d_term_offs);
   cudaFree(p->d_smask);
+  cudaFree(p->d_xmask);
+  cudaFree(p->d_tphase);
   cudaFree(p->d_tcoeff);
   cudaFree(p->d_col_offs);
   cudaFree(p->d_chain);

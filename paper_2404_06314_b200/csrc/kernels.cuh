@@ -30,8 +30,11 @@ struct DevProgram {
   const DiagRun* diag;
   const int16_t* setids;
   const int32_t* term_offs;  // M + 1
-  const uint32_t* t_smask;   // T
-  const double* t_coeff;     // T (coeff * Re(phase); Z strings only)
+  const uint32_t* t_smask;   // T sign masks (Y/Z letters)
+  const uint32_t* t_xmask;   // T flip masks (X/Y letters; nonzero only when has_xy)
+  const int32_t* t_phase;    // T powers of i
+  const double* t_coeff;     // T
+  int has_xy;                // any X/Y string (on-chip states only)
   int n, k, R, NG, n_rot, M, n_pass;
   int n_blk, n_av, max_rot_pass, max_blk_pass, max_av_pass;
   int T;  // observable terms

@@ -96,12 +96,12 @@ def _random_cases():
     if not os.path.exists(path):
         return []
     g = np.load(path)
-    return [i for i in range(int(g["count"])) if not bool(g[f"c{i}_general"])]
+    return list(range(int(g["count"])))
 
 
 @pytest.mark.parametrize("idx", _random_cases())
 def test_random_circuits_vs_reference(torch_cuda, idx):
-    """Random circuits over RX RY RZ CNOT H X, shared/product parameters, Z-string sums."""
+    """Random circuits over RX RY RZ CNOT H X, shared/product parameters, Pauli sums."""
     from paper_2404_06314_b200 import ir
     from paper_2404_06314_b200.observables import Observable
     g = np.load(os.path.join(GOLDEN, "random.npz"))
@@ -209,13 +209,28 @@ def test_degenerate_shapes(torch_cuda):
     assert r.expectations.shape == (3, 0) and r.gradients["x"].shape == (3, 0, 4)
 
 
-def test_unsupported_observable_raises(torch_cuda):
+def test_xy_observables_on_chip(torch_cuda):
+    """General Pauli strings (observables.py:70-92) on the on-chip path."""
     from paper_2404_06314_b200 import configs, parse_observable
-    spec = configs.CONFIGS[1]
+    spec = configs.CONFIGS[2]
     circ, _, wrt = configs.build(spec, configs.native_api())
-    x, w = configs.inputs_and_weights(spec)
-    with pytest.raises(NotImplementedError, match="Z strings only"):
-        _engine().run_batch(_request(circ, [parse_observable("XZZZ")], {"w": w}, x[:2], wrt))
+    x, w = configs.inputs_and_weights(spec, batch=16)
+    obs = [parse_observable("0.5*XZYIIIII + -1.2*IIIIYYXZ + 0.3*ZIIIIIII"),
+           parse_observable("YIIIIIIY"), parse_observable("IIXIIIII + 2*IIIZIIII")]
+    e_ref, j_ref = oracle_batch(circ, obs, {"w": w}, x, wrt)
+    res = _engine().run_batch(_request(circ, obs, {"w": w}, x, wrt))
+    assert close(res.expectations, e_ref) < TOL
+    for k in wrt:
+        assert close(res.gradients[k], j_ref[k]) < TOL
+
+
+def test_xy_observables_rejected_on_hbm_path(torch_cuda):
+    from paper_2404_06314_b200 import configs, parse_observable
+    spec = configs.CONFIGS[4]
+    circ, _, wrt = configs.build(spec, configs.native_api())
+    x, w = configs.inputs_and_weights(spec, batch=2)
+    with pytest.raises(NotImplementedError, match="n <= 12"):
+        _engine().run_batch(_request(circ, [parse_observable("X" + "I" * 15)], {"w": w}, x, wrt))
 
 
 def test_no_gates_circuit(torch_cuda):
