@@ -18,7 +18,7 @@ __version__ = "0.1.0"
 
 def __getattr__(name):
     # torch-dependent pieces load lazily so the IR is importable without CUDA
-    if name in ("QuantumModule", "QuantumFunction", "Uniform", "Constant", "Normal"):
+    if name in ("QuantumModule", "QuantumFunction", "HybridModule", "Uniform", "Constant", "Normal"):
         from . import module
         return getattr(module, name)
     raise AttributeError(name)

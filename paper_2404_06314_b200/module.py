@@ -244,3 +244,63 @@ class QuantumModule(torch.nn.Module):
             out[n] = host[col:col + size].copy()
             col += size
         return out
+
+
+def _single_qubit(obs) -> bool:
+    return all(sum(ch != "I" for ch in string) <= 1 for _, string in obs.terms)
+
+
+class HybridModule(torch.nn.Module):
+    """Dense pre-layer -> pi*tanh squash -> QuantumModule -> dense post-layer.
+
+    Mirrors model.py:152-222 (same initialisation order and bounds from one
+    ``default_rng(seed)``; single-qubit observables required). Gradients flow
+    through QuantumFunction, i.e. the quantum core's input gradient comes from
+    the same VJP-seeded adjoint sweep as its weight gradient.
+    """
+
+    def __init__(self, input_dim: int, quantum: QuantumModule, output_dim: int, seed: int | None = None):
+        super().__init__()
+        for obs in quantum.observables:
+            if not _single_qubit(obs):
+                raise ValueError("hybrid quantum core must use single-qubit observables")
+        self.input_dim = int(input_dim)
+        self.output_dim = int(output_dim)
+        self.quantum = quantum
+        enc, m = quantum.encoding_size, quantum.num_outputs
+        rng = np.random.default_rng(seed)
+        bp = 1.0 / np.sqrt(max(1, input_dim))
+        bq = 1.0 / np.sqrt(max(1, m))
+        dev = quantum._engine.device
+
+        def param(a):
+            return torch.nn.Parameter(torch.from_numpy(np.ascontiguousarray(a, np.float64)).to(dev))
+
+        self.pre_weight = param(rng.uniform(-bp, bp, (enc, input_dim)))
+        self.pre_bias = param(rng.uniform(-bp, bp, enc))
+        self.post_weight = param(rng.uniform(-bq, bq, (output_dim, m)))
+        self.post_bias = param(rng.uniform(-bq, bq, output_dim))
+
+    def forward(self, inputs) -> torch.Tensor:
+        x = inputs if torch.is_tensor(inputs) else torch.from_numpy(np.atleast_2d(np.asarray(inputs, np.float64)))
+        x = x.to(device=self.pre_weight.device, dtype=torch.float64)
+        if x.dim() != 2 or x.shape[1] != self.input_dim:
+            raise ValueError(f"inputs must have shape (B, {self.input_dim}), got {tuple(x.shape)}")
+        angles = torch.pi * torch.tanh(x @ self.pre_weight.T + self.pre_bias)
+        return self.quantum(angles) @ self.post_weight.T + self.post_bias
+
+    def backward(self, inputs, upstream) -> dict:
+        """Gradients of sum(upstream * forward) per weight block (model.py:720-742)."""
+        up = torch.as_tensor(np.asarray(upstream.detach().cpu() if torch.is_tensor(upstream) else upstream,
+                                        dtype=np.float64), device=self.pre_weight.device)
+        n = np.atleast_2d(np.asarray(inputs.detach().cpu() if torch.is_tensor(inputs) else inputs)).shape[0]
+        if tuple(up.shape) != (n, self.output_dim):
+            raise ValueError(f"upstream shape {tuple(up.shape)} does not match (B, {self.output_dim})")
+        named = {"pre.weight": self.pre_weight, "pre.bias": self.pre_bias,
+                 "post.weight": self.post_weight, "post.bias": self.post_bias}
+        named.update(self.quantum.values)
+        for p in named.values():
+            p.grad = None
+        out = self.forward(inputs)
+        out.backward(up)
+        return {k: v.grad.detach().cpu().numpy().copy() for k, v in named.items()}

@@ -123,3 +123,35 @@ def test_nccl_world_size_1_allreduce(torch):
         assert torch.equal(before, mod.values["w"].grad)
     finally:
         dist.destroy_process_group()
+
+
+def test_hybrid_module_matches_reference_semantics(torch):
+    """HybridModule (model.py:152-222): oracle-built reference of its backward."""
+    from paper_2404_06314_b200 import configs
+    from paper_2404_06314_b200.module import HybridModule
+    spec, circ, obs, qmod = _module(2, seed=3)
+    hyb = HybridModule(5, qmod, 3, seed=9)
+    rng = np.random.default_rng(4)
+    x = rng.normal(size=(12, 5))
+    up = rng.normal(size=(12, 3))
+    g = hyb.backward(x, up)
+    # reference math (model.py:720-742) with oracle Jacobians
+    Wp = hyb.pre_weight.detach().cpu().numpy()
+    bp = hyb.pre_bias.detach().cpu().numpy()
+    Wq = hyb.post_weight.detach().cpu().numpy()
+    pre = x @ Wp.T + bp
+    ang = np.pi * np.tanh(pre)
+    w = qmod.parameter_values()["w"]
+    q, jac = oracle_batch(circ, obs, {"w": w}, ang, ("w", "x"))
+    d_q = up @ Wq
+    d_ang = np.einsum("bm,bmf->bf", d_q, jac["x"])
+    d_pre = d_ang * np.pi * (1.0 - np.tanh(pre) ** 2)
+    ref = {"post.weight": up.T @ q, "post.bias": up.sum(0), "w": np.einsum("bm,bmp->p", d_q, jac["w"]),
+           "pre.weight": d_pre.T @ x, "pre.bias": d_pre.sum(0)}
+    for k, v in ref.items():
+        assert close(g[k], v) < TOL, k
+    with pytest.raises(ValueError, match="single-qubit"):
+        from paper_2404_06314_b200 import parse_observable
+        from paper_2404_06314_b200.module import QuantumModule
+        bad = QuantumModule(circ, [parse_observable("ZZ" + "I" * 6)], "x", ["w"], device="cuda:0")
+        HybridModule(5, bad, 3)
