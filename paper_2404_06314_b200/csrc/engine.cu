@@ -576,6 +576,32 @@ int env_int(const char* name, int dflt) {
 
 }  // namespace
 
+// ThrEntry rows of every segment (program.h): for each thread group gi the
+// global bits its index contributes, and the swizzled load / store bases
+// with the folded CNOT translations controlled by thread bits applied.
+static std::vector<ThrEntry> build_thr_table(std::vector<SegDesc>& segs) {
+  std::vector<ThrEntry> tab;
+  for (SegDesc& sd : segs) {
+    sd.thr_off = (int32_t)tab.size();
+    const int nthr = sd.nthr;
+    for (uint32_t gi = 0; gi < (1u << nthr); ++gi) {
+      uint32_t j0 = 0, p0 = 0;
+      for (int i = 0; i < nthr; ++i)
+        if ((gi >> i) & 1u) {
+          p0 ^= sd.tsw[i];
+          j0 |= 1u << sd.thr_g[i];
+        }
+      uint32_t lp0 = p0, sp0 = p0;
+      for (int t = 0; t < kMaxR; ++t) {
+        if (__builtin_popcount(j0 & sd.ld_k[t]) & 1) lp0 ^= sd.ps[t];
+        if (__builtin_popcount(j0 & sd.st_k[t]) & 1) sp0 ^= sd.ps[t];
+      }
+      tab.push_back(ThrEntry{j0, lp0, sp0, 0u});
+    }
+  }
+  return tab;
+}
+
 struct VqcPlan {
   int device = 0;
   int sms = 148;
@@ -595,6 +621,7 @@ struct VqcPlan {
   MemberDesc* d_members = nullptr;
   DiagRun* d_diag = nullptr;
   int16_t* d_setids = nullptr;
+  ThrEntry* d_thr_tab = nullptr;
   PassDesc* d_passes = nullptr;
   RotDesc* d_rots = nullptr;
   int32_t* d_term_offs = nullptr;
@@ -1013,7 +1040,9 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
   }
   cudaError_t e = cudaGetDevice(&p->device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, p->device);
+  const std::vector<ThrEntry> thr_tab = build_thr_table(p->prog.segs);
   const HostProgram& P = p->prog;
+  if (e == cudaSuccess) e = upload(thr_tab, &p->d_thr_tab);
   if (e == cudaSuccess) e = upload(P.ops, &p->d_ops);
   if (e == cudaSuccess) e = upload(P.segs, &p->d_segs);
   if (e == cudaSuccess) e = upload(P.ipouts, &p->d_ipouts);
@@ -1042,6 +1071,7 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
   D.members = p->d_members;
   D.diag = p->d_diag;
   D.setids = p->d_setids;
+  D.thr_tab = p->d_thr_tab;
   D.n_blk = P.n_blk;
   D.n_av = P.n_av;
   D.max_rot_pass = P.max_rot_per_pass;
@@ -1079,6 +1109,7 @@ void vqc_plan_destroy(VqcPlan* p) {
   cudaFree(p->d_members);
   cudaFree(p->d_diag);
   cudaFree(p->d_setids);
+  cudaFree(p->d_thr_tab);
   cudaFree(p->d_passes);
   cudaFree(p->d_rots);
   cudaFree(p->d_term_offs);

@@ -29,6 +29,7 @@ struct DevProgram {
   const MemberDesc* members;
   const DiagRun* diag;
   const int16_t* setids;
+  const ThrEntry* thr_tab;
   const int32_t* term_offs;  // M + 1
   const uint32_t* t_smask;   // T sign masks (Y/Z letters)
   const uint32_t* t_xmask;   // T flip masks (X/Y letters; nonzero only when has_xy)
@@ -623,22 +624,18 @@ __device__ __forceinline__ void run_segments(const DevProgram& D, const RunArgs&
     SegCtx<R> C;
     C.own = own;
     C.partner = partner;
-    uint32_t p0 = 0;
-    C.J0 = tile_base;
+    const ThrEntry* te = D.thr_tab + sd->thr_off + (grp.gi & ((1 << nthr) - 1));
+    const uint2 e01 = *reinterpret_cast<const uint2*>(te);
+    C.J0 = tile_base | e01.x;
+    C.lp0 = e01.y;
+    // folded CNOT runs controlled by tile (non-local) bits
+    if (tile_base != 0) {
 #pragma unroll
-    for (int i = 0; i < kSmemMaxQubits; ++i)
-      if (i < nthr && ((grp.gi >> i) & 1)) {
-        p0 ^= sd->tsw[i];
-        C.J0 |= 1u << sd->thr_g[i];
-      }
-    // folded CNOT runs: register bit s loads from / stores to column col[s],
-    // translated by the J0-controlled slots (program.h SegDesc)
-    C.lp0 = p0;
-#pragma unroll
-    for (int t = 0; t < R; ++t) {
-      if (__popc(C.J0 & sd->ld_k[t]) & 1) C.lp0 ^= sd->ps[t];
-      C.lc[t] = sd->ldc[t];
+      for (int t = 0; t < R; ++t)
+        if (__popc(tile_base & sd->ld_k[t]) & 1) C.lp0 ^= sd->ps[t];
     }
+#pragma unroll
+    for (int t = 0; t < R; ++t) C.lc[t] = sd->ldc[t];
     double2 a[N], f[N];
     if (active) {
 #pragma unroll
@@ -677,13 +674,15 @@ __device__ __forceinline__ void run_segments(const DevProgram& D, const RunArgs&
     if (MODE == MODE_SPLIT && sd->ip_count > 0) __syncthreads();  // partners done reading
     asm volatile("" ::: "memory");  // keep the store map's loads and math after the op loop
     if (active) {
-      uint32_t sp0 = p0, sc[R];
+      uint32_t sp0 = te->sp0, sc[R];
+      if (tile_base != 0) {
+#pragma unroll
+        for (int t = 0; t < R; ++t)
+          if (__popc(tile_base & sd->st_k[t]) & 1) sp0 ^= sd->ps[t];
+      }
       asm volatile("" : "+r"(sp0));
 #pragma unroll
-      for (int t = 0; t < R; ++t) {
-        if (__popc(C.J0 & sd->st_k[t]) & 1) sp0 ^= sd->ps[t];
-        sc[t] = sd->stc[t];
-      }
+      for (int t = 0; t < R; ++t) sc[t] = sd->stc[t];
 #pragma unroll
       for (int i = 0; i < N; ++i) {
         uint32_t ad = sp0;

@@ -85,6 +85,7 @@ struct SegDesc {
   int32_t op_begin, op_end;
   int32_t ip_begin, ip_count;  // IpOut entries of this segment
   int32_t red_count;           // reduction slots used
+  int32_t thr_off;             // this segment's rows in the per-thread table (ThrEntry)
   // Leading / trailing CNOT runs folded into the shared-memory address maps:
   // register index bit s is stored at / loaded from the tile position whose
   // register bits are col[s] (an R-bit mask over slots) translated by the
@@ -100,6 +101,14 @@ struct SegDesc {
   int8_t reg_g[kMaxR];         // global qubit of each register slot
   int8_t thr_l[kMaxQubits];    // tile-local bit position of thread-index bit i
   int8_t thr_g[kMaxQubits];    // global qubit of thread-index bit i
+};
+
+// Per (segment, thread group) precomputed addressing: thread-bit part of
+// the group's global index and its swizzled load / store base addresses
+// (folded CNOT translations by thread bits applied; tile bits are added by
+// the kernel). Filled at plan creation (engine.cu build_thr_table).
+struct ThrEntry {
+  uint32_t j0, lp0, sp0, pad;
 };
 
 struct PassDesc {
