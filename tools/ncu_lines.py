@@ -17,6 +17,11 @@ sass = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-s
                       capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(sass)))
 hdr = rows[1]
+if column == "?":
+    print("\n".join(hdr))
+    sys.exit(0)
+if column not in hdr:  # substring match (e.g. "long_sb")
+    column = next(h for h in hdr if column.lower() in h.lower())
 samples = {}
 for r in rows[2:]:
     if len(r) != len(hdr):
