@@ -130,6 +130,14 @@ int vqc_run_batch_host(VqcPlan* plan, const double* h_inputs, const double* h_we
                        double* h_vjp_rows, double* h_vjp_sum);
 
 /* Number of kernels the last call on this thread launched (for bench claims). */
+/* Per-plan kernel specialisation (no reference counterpart: the reference's
+ * numba kernels are compiled once per gate kind, _kernels.py:32-141). The
+ * CUDA source that vqc_plan_create compiles with NVRTC for this circuit;
+ * with compile != 0 it is also compiled for sm_100a (no GPU needed) and the
+ * compile time stored in *compile_s. Returns the source length or < 0. */
+int64_t vqc_jit_source(const VqcCircuit* circuit, const int64_t* wrt_col, int compile, char* buf, int64_t cap,
+                       double* compile_s);
+
 int64_t vqc_last_launch_count(void);
 
 /* Per-kernel CUDA-event timing of this thread's launches (bench/profiling):

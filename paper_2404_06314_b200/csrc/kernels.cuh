@@ -9,15 +9,22 @@
 // round trip 32 B per amplitude (0.25 clk/amp/SM at 128 B/clk) — segments
 // amortise the round trip over every gate on their R qubits.
 #pragma once
+#ifndef __CUDACC_RTC__
 #include <cuda_runtime.h>
 #include <stdint.h>
-
-#include <type_traits>
+#endif
 
 #include "blockmath.h"
 #include "program.h"
 
 namespace vqc {
+
+// compile-time integer (std::integral_constant without <type_traits>, which
+// NVRTC cannot include)
+template <int V>
+struct IC {
+  static constexpr int value = V;
+};
 
 struct DevProgram {
   const Op* ops;
@@ -89,6 +96,7 @@ __device__ __forceinline__ void dbg_add(const RunArgs& A, int slot, long long& t
 __device__ __forceinline__ uint32_t swz(uint32_t l) { return swz_index(l); }
 
 __host__ __device__ constexpr int ctz_const(int i) { return (i & 1) ? 0 : 1 + ctz_const(i >> 1); }
+__host__ __device__ constexpr int popc_const(int i) { return i == 0 ? 0 : (i & 1) + popc_const(i >> 1); }
 
 __device__ __forceinline__ double neg_if(double x, bool c) {
   const int hi = __double2hiint(x) ^ (c ? (int)0x80000000 : 0);
@@ -115,11 +123,11 @@ __device__ __forceinline__ double2 rot_cs(const DevProgram& D, const RunArgs& A,
 template <int R, typename F>
 __device__ __forceinline__ void with_slot(uint32_t s, F&& f) {
   switch (s) {
-    case 0: f(std::integral_constant<int, 0>{}); break;
-    case 1: if constexpr (R > 1) f(std::integral_constant<int, 1>{}); break;
-    case 2: if constexpr (R > 2) f(std::integral_constant<int, 2>{}); break;
-    case 3: if constexpr (R > 3) f(std::integral_constant<int, 3>{}); break;
-    default: if constexpr (R > 4) f(std::integral_constant<int, 4>{}); break;
+    case 0: f(IC<0>{}); break;
+    case 1: if constexpr (R > 1) f(IC<1>{}); break;
+    case 2: if constexpr (R > 2) f(IC<2>{}); break;
+    case 3: if constexpr (R > 3) f(IC<3>{}); break;
+    default: if constexpr (R > 4) f(IC<4>{}); break;
   }
 }
 
@@ -353,11 +361,11 @@ __device__ __forceinline__ void put_partial(double* redbuf, int slot, double v) 
 // compile-time slot from an unrolled loop index (no branch after unrolling)
 template <int R, typename F>
 __device__ __forceinline__ void with_const_slot(int s, F&& f) {
-  if (s == 0) f(std::integral_constant<int, 0>{});
-  if constexpr (R > 1) if (s == 1) f(std::integral_constant<int, 1>{});
-  if constexpr (R > 2) if (s == 2) f(std::integral_constant<int, 2>{});
-  if constexpr (R > 3) if (s == 3) f(std::integral_constant<int, 3>{});
-  if constexpr (R > 4) if (s == 4) f(std::integral_constant<int, 4>{});
+  if (s == 0) f(IC<0>{});
+  if constexpr (R > 1) if (s == 1) f(IC<1>{});
+  if constexpr (R > 2) if (s == 2) f(IC<2>{});
+  if constexpr (R > 3) if (s == 3) f(IC<3>{});
+  if constexpr (R > 4) if (s == 4) f(IC<4>{});
 }
 
 // per-sample parameter tables in shared memory
@@ -396,7 +404,7 @@ __device__ __forceinline__ void ip_dispatch(const SegCtx<R>& C, const double2 (&
   auto ra = [&](int i) { return a[i]; };
   if constexpr (MODE == MODE_DUAL) {
     auto rf = [&](int i) { return f[i]; };
-    kernel(std::integral_constant<int, -1>{}, ra, rf);
+    kernel(IC<-1>{}, ra, rf);
   } else {
     // recompute partner addresses here (pinned by the empty asm) instead of
     // letting the compiler keep 2^R loop-invariant addresses live
@@ -409,336 +417,494 @@ __device__ __forceinline__ void ip_dispatch(const SegCtx<R>& C, const double2 (&
         if ((i >> s) & 1) ad ^= C.lc[s];
       return C.partner[ad];
     };
-    if (role == 0) kernel(std::integral_constant<int, 0>{}, ra, sm);
-    else kernel(std::integral_constant<int, 1>{}, sm, ra);
+    if (role == 0) kernel(IC<0>{}, ra, sm);
+    else kernel(IC<1>{}, sm, ra);
   }
 }
 
+// ---------------------------------------------------------------------------
+// Ops with compile-time operands. The interpreter (exec_op) dispatches to
+// these through with_slot; the per-plan JIT (jit.cpp) emits direct calls, so
+// both paths run the same arithmetic in the same order.
+template <int R>
+using Regs = double2[1 << R];
+
+template <int R, int MODE, int KIND, int S, bool ADJ>
+__device__ __forceinline__ void jop_rot(Regs<R>& a, Regs<R>& f, const SampleTables& T, int r) {
+  const double2 cs = T.cs[r];
+  const double sn = ADJ ? -cs.y : cs.y;
+  if constexpr (KIND == G_RX) {
+    g_rx<R, S>(a, cs.x, sn);
+    if constexpr (MODE == MODE_DUAL) g_rx<R, S>(f, cs.x, sn);
+  } else {
+    g_ry<R, S>(a, cs.x, sn);
+    if constexpr (MODE == MODE_DUAL) g_ry<R, S>(f, cs.x, sn);
+  }
+}
+
+// RZ on register slot mask m (power of two), or on a thread/tile bit cb (m = 0)
+template <int R, int MODE, bool ADJ>
+__device__ __forceinline__ void jop_rz(Regs<R>& a, Regs<R>& f, const SampleTables& T, int r, uint32_t m, bool cb) {
+  const double2 cs = T.cs[r];
+  const double sn = ADJ ? -cs.y : cs.y;
+  g_rz<R>(a, cs.x, sn, m, cb);
+  if constexpr (MODE == MODE_DUAL) g_rz<R>(f, cs.x, sn, m, cb);
+}
+
+// fused block (relative id blk) on slot S; ADJ applies U^dagger
+template <int R, int MODE, int S, bool ADJ>
+__device__ __forceinline__ void jop_u2(Regs<R>& a, Regs<R>& f, const SampleTables& T, int blk) {
+  const double2* u = T.u + 4 * blk;
+  double2 u00 = u[0], u01 = u[1], u10 = u[2], u11 = u[3];
+  if constexpr (ADJ) {
+    const double2 t = u01;
+    u00.y = -u00.y;
+    u11.y = -u11.y;
+    u01 = make_double2(u10.x, -u10.y);
+    u10 = make_double2(t.x, -t.y);
+  }
+  g_u2<R, S>(a, u00, u01, u10, u11);
+  if constexpr (MODE == MODE_DUAL) g_u2<R, S>(f, u00, u01, u10, u11);
+}
+
+template <int R, int MODE, int C, int T>
+__device__ __forceinline__ void jop_cnot_rr(Regs<R>& a, Regs<R>& f) {
+  g_cnot_rr<R, C, T>(a);
+  if constexpr (MODE == MODE_DUAL) g_cnot_rr<R, C, T>(f);
+}
+template <int R, int MODE, int T>
+__device__ __forceinline__ void jop_cnot_cr(Regs<R>& a, Regs<R>& f, bool cb) {
+  g_cnot_cr<R, T>(a, cb);
+  if constexpr (MODE == MODE_DUAL) g_cnot_cr<R, T>(f, cb);
+}
+template <int R, int MODE, int S>
+__device__ __forceinline__ void jop_h(Regs<R>& a, Regs<R>& f) {
+  g_h<R, S>(a);
+  if constexpr (MODE == MODE_DUAL) g_h<R, S>(f);
+}
+template <int R, int MODE, int S>
+__device__ __forceinline__ void jop_x(Regs<R>& a, Regs<R>& f) {
+  g_x<R, S>(a);
+  if constexpr (MODE == MODE_DUAL) g_x<R, S>(f);
+}
 template <int R, int MODE>
-__device__ __forceinline__ void exec_op(const DevProgram& D, const Op op, double2 (&a)[1 << R],
-                                        double2 (&f)[1 << R], const SegCtx<R>& C, int role,
-                                        const SampleTables& T, double* s_redbuf) {
-  constexpr bool DUAL = MODE == MODE_DUAL;
+__device__ __forceinline__ void jop_cz(Regs<R>& a, Regs<R>& f, uint32_t m, bool cond) {
+  g_cz<R>(a, m, cond);
+  if constexpr (MODE == MODE_DUAL) g_cz<R>(f, m, cond);
+}
+template <int R, int MODE>
+__device__ __forceinline__ void jop_czrun(Regs<R>& a, Regs<R>& f, const DiagRun* dr, uint32_t J0) {
+  uint32_t qc = 0, m = 0;
+  for (uint32_t rest = J0; rest != 0; rest &= rest - 1) qc ^= (uint32_t)__popc(J0 & dr->upper[__ffs(rest) - 1]);
+#pragma unroll
+  for (int s = 0; s < R; ++s) m |= ((uint32_t)__popc(J0 & dr->part[s]) & 1u) << s;
+  const uint32_t qreg = dr->qreg;
+  g_czrun<R>(a, qreg, m, qc);
+  if constexpr (MODE == MODE_DUAL) g_czrun<R>(f, qreg, m, qc);
+}
+
+// inner products: partial sums into reduction slots (adjoint modes only)
+template <int R, int MODE, int S>
+__device__ __forceinline__ void jop_ip3(const SegCtx<R>& C, const Regs<R>& a, const Regs<R>& f, int role,
+                                        double* s_red, int r0) {
+  if constexpr (MODE != MODE_FWD) {
+    double ix = 0.0, iy = 0.0, iz = 0.0;
+    ip_dispatch<R, MODE>(C, a, f, role, [&](auto PART, auto&& p, auto&& q) {
+      ip_xyz<R, S, PART.value>(p, q, ix, iy, iz);
+    });
+    put_partial(s_red, r0, ix);
+    put_partial(s_red, r0 + 1, iy);
+    put_partial(s_red, r0 + 2, iz);
+  }
+}
+// KIND: 0 = X, 1 = Y on slot S
+template <int R, int MODE, int KIND, int S>
+__device__ __forceinline__ void jop_ipxy(const SegCtx<R>& C, const Regs<R>& a, const Regs<R>& f, int role,
+                                         double* s_red, int r) {
+  if constexpr (MODE != MODE_FWD) {
+    double v = 0.0;
+    ip_dispatch<R, MODE>(C, a, f, role, [&](auto PART, auto&& p, auto&& q) {
+      if constexpr (KIND == 0) v = ip_x<R, S, PART.value>(p, q);
+      else v = ip_y<R, S, PART.value>(p, q);
+    });
+    put_partial(s_red, r, v);
+  }
+}
+template <int R, int MODE>
+__device__ __forceinline__ void jop_ipz(const SegCtx<R>& C, const Regs<R>& a, const Regs<R>& f, int role,
+                                        double* s_red, int r, uint32_t m, bool cb) {
+  if constexpr (MODE != MODE_FWD) {
+    double v = 0.0;
+    ip_dispatch<R, MODE>(C, a, f, role, [&](auto PART, auto&& p, auto&& q) {
+      v = ip_z<R, PART.value>(p, q, m, cb);
+    });
+    put_partial(s_red, r, v);
+  }
+}
+
+// Fused blocks on the register slots of compile-time MASK (one op of the
+// program): straight-line code, so the block results only need to reach the
+// loop-carried registers once per set instead of once per block.
+template <int R, int MODE, bool ADJ, int MASK>
+__device__ __forceinline__ void jop_u2set(Regs<R>& a, Regs<R>& f, const SampleTables& T, const int16_t* ids) {
+  if constexpr ((MASK & 1) != 0) jop_u2<R, MODE, 0, ADJ>(a, f, T, ids[0]);
+  if constexpr (R > 1 && (MASK & 2) != 0) jop_u2<R, MODE, 1, ADJ>(a, f, T, ids[1]);
+  if constexpr (R > 2 && (MASK & 4) != 0) jop_u2<R, MODE, 2, ADJ>(a, f, T, ids[2]);
+  if constexpr (R > 3 && (MASK & 8) != 0) jop_u2<R, MODE, 3, ADJ>(a, f, T, ids[3]);
+  if constexpr (R > 4 && (MASK & 16) != 0) jop_u2<R, MODE, 4, ADJ>(a, f, T, ids[4]);
+}
+
+// Im<phi|X,Y,Z|psi> on every slot of MASK; reduction slots r0, r0 + 3, ... in
+// slot order. The split-role branch is taken once for the whole set.
+template <int R, int PART, int MASK, class P, class F>
+__device__ __forceinline__ void ip3set_part(P&& p, F&& q, double* s_red, int r0) {
+  auto one = [&](auto SL, int r) {
+    if constexpr (SL.value < R && ((MASK >> SL.value) & 1) != 0) {
+      double ix = 0.0, iy = 0.0, iz = 0.0;
+      ip_xyz<R, SL.value, PART>(p, q, ix, iy, iz);
+      put_partial(s_red, r, ix);
+      put_partial(s_red, r + 1, iy);
+      put_partial(s_red, r + 2, iz);
+    }
+  };
+  one(IC<0>{}, r0);
+  one(IC<1>{}, r0 + 3 * popc_const(MASK & 1));
+  one(IC<2>{}, r0 + 3 * popc_const(MASK & 3));
+  one(IC<3>{}, r0 + 3 * popc_const(MASK & 7));
+  one(IC<4>{}, r0 + 3 * popc_const(MASK & 15));
+}
+template <int R, int MODE, int MASK>
+__device__ __forceinline__ void jop_ip3set(const SegCtx<R>& C, const Regs<R>& a, const Regs<R>& f, int role,
+                                           double* s_red, int r0) {
+  if constexpr (MODE != MODE_FWD) {
+    ip_dispatch<R, MODE>(C, a, f, role, [&](auto PART, auto&& p, auto&& q) {
+      ip3set_part<R, PART.value, MASK>(p, q, s_red, r0);
+    });
+  }
+}
+
+// run-time mask -> compile-time MASK for the common wide sets (R = 4, three
+// or four slots); other masks take the per-slot path. Kept narrow: every
+// specialisation is ~1-2k FP64 instructions per kernel instantiation.
+template <int R, class F, class G>
+__device__ __forceinline__ void with_wide_mask(uint32_t mask, F&& f, G&& generic) {
+  if constexpr (R == 4) {
+    switch (mask) {
+      case 15: f(IC<15>{}); return;
+      case 7: f(IC<7>{}); return;
+      case 11: f(IC<11>{}); return;
+      case 13: f(IC<13>{}); return;
+      case 14: f(IC<14>{}); return;
+      default: break;
+    }
+  }
+  generic();
+}
+
+// interpreter: one op of the device program, operands decoded at run time
+template <int R, int MODE>
+__device__ __forceinline__ void exec_op(const DevProgram& D, const Op op, Regs<R>& a, Regs<R>& f,
+                                        const SegCtx<R>& C, int role, const SampleTables& T, double* s_redbuf) {
   const uint32_t w0 = op.w0;
   const uint32_t A = op_a(w0), Bq = op_b(w0);
   const uint32_t J0 = C.J0;
+  const bool adj = op_adj(w0);
   switch (op_code(w0)) {
-    case OP_RX: {
-      const double2 cs = T.cs[(int)op.param - T.rot_base];
-      const double sn = op_adj(w0) ? -cs.y : cs.y;
-      with_slot<R>(A & 7u, [&](auto SL) {
-        g_rx<R, SL.value>(a, cs.x, sn);
-        if constexpr (DUAL) g_rx<R, SL.value>(f, cs.x, sn);
-      });
-    } break;
+    case OP_RX:
     case OP_RY: {
-      const double2 cs = T.cs[(int)op.param - T.rot_base];
-      const double sn = op_adj(w0) ? -cs.y : cs.y;
+      const int r = (int)op.param - T.rot_base;
+      const bool rx = op_code(w0) == OP_RX;
       with_slot<R>(A & 7u, [&](auto SL) {
-        g_ry<R, SL.value>(a, cs.x, sn);
-        if constexpr (DUAL) g_ry<R, SL.value>(f, cs.x, sn);
+        if (rx) {
+          if (adj) jop_rot<R, MODE, G_RX, SL.value, true>(a, f, T, r);
+          else jop_rot<R, MODE, G_RX, SL.value, false>(a, f, T, r);
+        } else {
+          if (adj) jop_rot<R, MODE, G_RY, SL.value, true>(a, f, T, r);
+          else jop_rot<R, MODE, G_RY, SL.value, false>(a, f, T, r);
+        }
       });
     } break;
     case OP_RZ: {
-      const double2 cs = T.cs[(int)op.param - T.rot_base];
-      const double sn = op_adj(w0) ? -cs.y : cs.y;
       const uint32_t m = (A & kSlotFlag) ? (1u << (A & 7u)) : 0u;
       const bool cb = (A & kSlotFlag) ? false : ((J0 >> A) & 1u);
-      g_rz<R>(a, cs.x, sn, m, cb);
-      if constexpr (DUAL) g_rz<R>(f, cs.x, sn, m, cb);
+      const int r = (int)op.param - T.rot_base;
+      if (adj) jop_rz<R, MODE, true>(a, f, T, r, m, cb);
+      else jop_rz<R, MODE, false>(a, f, T, r, m, cb);
     } break;
     case OP_U2: {
-      const double2* u = T.u + 4 * ((int)op.param - T.blk_base);
-      double2 u00 = u[0], u01 = u[1], u10 = u[2], u11 = u[3];
-      if (op_adj(w0)) {  // U^dagger
-        const double2 t = u01;
-        u00.y = -u00.y;
-        u11.y = -u11.y;
-        u01 = make_double2(u10.x, -u10.y);
-        u10 = make_double2(t.x, -t.y);
-      }
+      const int blk = (int)op.param - T.blk_base;
       with_slot<R>(A & 7u, [&](auto SL) {
-        g_u2<R, SL.value>(a, u00, u01, u10, u11);
-        if constexpr (DUAL) g_u2<R, SL.value>(f, u00, u01, u10, u11);
+        if (adj) jop_u2<R, MODE, SL.value, true>(a, f, T, blk);
+        else jop_u2<R, MODE, SL.value, false>(a, f, T, blk);
       });
     } break;
     case OP_U2SET: {
-      const bool adj = op_adj(w0);
+      // forward segments apply blocks, adjoint segments un-apply them
+      constexpr bool ADJ = MODE != MODE_FWD;
+      const int16_t* ids = D.setids + op.param * kMaxR;
+      with_wide_mask<R>(
+          Bq, [&](auto MK) { jop_u2set<R, MODE, ADJ, MK.value>(a, f, T, ids); },
+          [&]() {
 #pragma unroll
-      for (int sl = 0; sl < R; ++sl) {
-        const int id = D.setids[op.param * kMaxR + sl];
-        if (id < 0) continue;
-        const double2* u = T.u + 4 * id;
-        double2 u00 = u[0], u01 = u[1], u10 = u[2], u11 = u[3];
-        if (adj) {
-          const double2 t = u01;
-          u00.y = -u00.y;
-          u11.y = -u11.y;
-          u01 = make_double2(u10.x, -u10.y);
-          u10 = make_double2(t.x, -t.y);
-        }
-        with_const_slot<R>(sl, [&](auto SL) {
-          g_u2<R, SL.value>(a, u00, u01, u10, u11);
-          if constexpr (DUAL) g_u2<R, SL.value>(f, u00, u01, u10, u11);
-        });
-      }
+            for (int sl = 0; sl < R; ++sl) {
+              const int id = ids[sl];
+              if (id < 0) continue;
+              with_const_slot<R>(sl, [&](auto SL) {
+                if (adj) jop_u2<R, MODE, SL.value, true>(a, f, T, id);
+                else jop_u2<R, MODE, SL.value, false>(a, f, T, id);
+              });
+            }
+          });
     } break;
     case OP_CNOT: {
       if (A & kSlotFlag) {
         with_slot<R>(A & 7u, [&](auto Cc) {
-          with_slot<R>(Bq & 7u, [&](auto Tt) {
-            g_cnot_rr<R, Cc.value, Tt.value>(a);
-            if constexpr (DUAL) g_cnot_rr<R, Cc.value, Tt.value>(f);
-          });
+          with_slot<R>(Bq & 7u, [&](auto Tt) { jop_cnot_rr<R, MODE, Cc.value, Tt.value>(a, f); });
         });
       } else {
         const bool cb = (J0 >> A) & 1u;
-        with_slot<R>(Bq & 7u, [&](auto Tt) {
-          g_cnot_cr<R, Tt.value>(a, cb);
-          if constexpr (DUAL) g_cnot_cr<R, Tt.value>(f, cb);
-        });
+        with_slot<R>(Bq & 7u, [&](auto Tt) { jop_cnot_cr<R, MODE, Tt.value>(a, f, cb); });
       }
     } break;
     case OP_H:
-      with_slot<R>(A & 7u, [&](auto SL) {
-        g_h<R, SL.value>(a);
-        if constexpr (DUAL) g_h<R, SL.value>(f);
-      });
+      with_slot<R>(A & 7u, [&](auto SL) { jop_h<R, MODE, SL.value>(a, f); });
       break;
     case OP_X:
-      with_slot<R>(A & 7u, [&](auto SL) {
-        g_x<R, SL.value>(a);
-        if constexpr (DUAL) g_x<R, SL.value>(f);
-      });
+      with_slot<R>(A & 7u, [&](auto SL) { jop_x<R, MODE, SL.value>(a, f); });
       break;
     case OP_CZ: {
       uint32_t m = 0;
       bool cond = true;
       if (A & kSlotFlag) m |= 1u << (A & 7u); else cond = cond && ((J0 >> A) & 1u);
       if (Bq & kSlotFlag) m |= 1u << (Bq & 7u); else cond = cond && ((J0 >> Bq) & 1u);
-      g_cz<R>(a, m, cond);
-      if constexpr (DUAL) g_cz<R>(f, m, cond);
+      jop_cz<R, MODE>(a, f, m, cond);
     } break;
-    case OP_CZRUN: {
-      const DiagRun* dr = D.diag + op.param;
-      uint32_t qc = 0, m = 0;
-      for (uint32_t rest = J0; rest != 0; rest &= rest - 1) qc ^= (uint32_t)__popc(J0 & dr->upper[__ffs(rest) - 1]);
-#pragma unroll
-      for (int s = 0; s < R; ++s) m |= ((uint32_t)__popc(J0 & dr->part[s]) & 1u) << s;
-      const uint32_t qreg = dr->qreg;
-      g_czrun<R>(a, qreg, m, qc);
-      if constexpr (DUAL) g_czrun<R>(f, qreg, m, qc);
-    } break;
-    case OP_PUBLISH:
-      if constexpr (MODE == MODE_SPLIT) {
-        __syncthreads();  // partners finished reading the previous copy
-#pragma unroll
-        for (int i = 0; i < (1 << R); ++i) C.own[C.addr(i)] = a[i];
-        __syncthreads();
-      }
+    case OP_CZRUN:
+      jop_czrun<R, MODE>(a, f, D.diag + op.param, J0);
       break;
+    case OP_PUBLISH:
+      break;  // handled by the segment loop (needs the CTA barrier)
     case OP_IP3:
-      if constexpr (MODE != MODE_FWD) {
-        double ix = 0.0, iy = 0.0, iz = 0.0;
-        with_slot<R>(A & 7u, [&](auto SL) {
-          ip_dispatch<R, MODE>(C, a, f, role, [&](auto PART, auto&& p, auto&& q) {
-            ip_xyz<R, SL.value, PART.value>(p, q, ix, iy, iz);
-          });
-        });
-        const int r0 = (int)op_ip(w0);
-        put_partial(s_redbuf, r0, ix);
-        put_partial(s_redbuf, r0 + 1, iy);
-        put_partial(s_redbuf, r0 + 2, iz);
-      }
+      with_slot<R>(A & 7u, [&](auto SL) { jop_ip3<R, MODE, SL.value>(C, a, f, role, s_redbuf, (int)op_ip(w0)); });
       break;
     case OP_IP3SET:
       if constexpr (MODE != MODE_FWD) {
-        const uint32_t mask = Bq;
-        int r0 = (int)op_ip(w0);
+        with_wide_mask<R>(
+            Bq, [&](auto MK) { jop_ip3set<R, MODE, MK.value>(C, a, f, role, s_redbuf, (int)op_ip(w0)); },
+            [&]() {
+              int r0 = (int)op_ip(w0);
 #pragma unroll
-        for (int sl = 0; sl < R; ++sl) {
-          if (!((mask >> sl) & 1u)) continue;
-          double ix = 0.0, iy = 0.0, iz = 0.0;
-          with_const_slot<R>(sl, [&](auto SL) {
-            ip_dispatch<R, MODE>(C, a, f, role, [&](auto PART, auto&& p, auto&& q) {
-              ip_xyz<R, SL.value, PART.value>(p, q, ix, iy, iz);
+              for (int sl = 0; sl < R; ++sl) {
+                if (!((Bq >> sl) & 1u)) continue;
+                with_const_slot<R>(sl, [&](auto SL) { jop_ip3<R, MODE, SL.value>(C, a, f, role, s_redbuf, r0); });
+                r0 += 3;
+              }
             });
-          });
-          put_partial(s_redbuf, r0, ix);
-          put_partial(s_redbuf, r0 + 1, iy);
-          put_partial(s_redbuf, r0 + 2, iz);
-          r0 += 3;
-        }
       }
       break;
-    default:
-      if constexpr (MODE != MODE_FWD) {
-        double v = 0.0;
-        const uint32_t code = op_code(w0);
-        if (code == OP_IPX) {
-          with_slot<R>(A & 7u, [&](auto SL) {
-            ip_dispatch<R, MODE>(C, a, f, role, [&](auto PART, auto&& p, auto&& q) {
-              v = ip_x<R, SL.value, PART.value>(p, q);
-            });
-          });
-        } else if (code == OP_IPY) {
-          with_slot<R>(A & 7u, [&](auto SL) {
-            ip_dispatch<R, MODE>(C, a, f, role, [&](auto PART, auto&& p, auto&& q) {
-              v = ip_y<R, SL.value, PART.value>(p, q);
-            });
-          });
-        } else {
-          const uint32_t m = (A & kSlotFlag) ? (1u << (A & 7u)) : 0u;
-          const bool cb = (A & kSlotFlag) ? false : ((J0 >> A) & 1u);
-          ip_dispatch<R, MODE>(C, a, f, role, [&](auto PART, auto&& p, auto&& q) {
-            v = ip_z<R, PART.value>(p, q, m, cb);
-          });
-        }
-        put_partial(s_redbuf, (int)op_ip(w0), v);
-      }
+    case OP_IPX:
+      with_slot<R>(A & 7u, [&](auto SL) { jop_ipxy<R, MODE, 0, SL.value>(C, a, f, role, s_redbuf, (int)op_ip(w0)); });
       break;
+    case OP_IPY:
+      with_slot<R>(A & 7u, [&](auto SL) { jop_ipxy<R, MODE, 1, SL.value>(C, a, f, role, s_redbuf, (int)op_ip(w0)); });
+      break;
+    default: {  // OP_IPZ
+      const uint32_t m = (A & kSlotFlag) ? (1u << (A & 7u)) : 0u;
+      const bool cb = (A & kSlotFlag) ? false : ((J0 >> A) & 1u);
+      jop_ipz<R, MODE>(C, a, f, role, s_redbuf, (int)op_ip(w0), m, cb);
+    } break;
   }
 }
 
-// Run segments [sb, se) on the tile(s) in shared memory. MODE_FWD: psi only;
-// MODE_DUAL: each thread holds psi and phi of its register group; MODE_SPLIT:
-// role-0 threads hold psi, role-1 threads phi. s_psi / s_phi point at this
-// thread's sample block; T / s_av are this thread's sample tables. Gradient
-// outputs go to A.ip (rows relative to A.b0, times n_tiles). Threads with
-// active == false only take part in the barriers.
-template <int R, int MODE>
-__device__ __forceinline__ void run_segments(const DevProgram& D, const RunArgs& A, int sb, int se,
-                                             double2* s_psi, double2* s_phi, const SampleTables& T,
-                                             const double* s_av_all, int av_stride, int av_base,
-                                             double* s_red, double* s_fin, const Group& grp, bool active,
-                                             uint32_t tile_base, int64_t bl0, int bra, int tile,
-                                             int n_tiles) {
-  constexpr int N = 1 << R;
-  constexpr bool DUAL = MODE == MODE_DUAL;
-  long long tdbg = A.dbg ? clock64() : 0;
+// ---------------------------------------------------------------------------
+// Segment frame shared by the interpreter and the JIT: everything a segment
+// needs besides its ops (the caller's run_segments arguments).
+struct SegEnv {
+  const DevProgram& D;
+  const RunArgs& A;
+  double2* s_psi;
+  double2* s_phi;
+  const double* s_av_all;
+  int av_stride, av_base;
+  double* s_red;
+  double* s_fin;
+  const Group& grp;
+  bool active;
+  uint32_t tile_base;
+  int64_t bl0;
+  int bra, tile, n_tiles;
+  double2* own;
+  const double2* partner;
+};
+
+template <int MODE>
+__device__ __forceinline__ SegEnv make_env(const DevProgram& D, const RunArgs& A, double2* s_psi, double2* s_phi,
+                                           const double* s_av_all, int av_stride, int av_base, double* s_red,
+                                           double* s_fin, const Group& grp, bool active, uint32_t tile_base,
+                                           int64_t bl0, int bra, int tile, int n_tiles) {
   double2* own = (MODE == MODE_SPLIT && grp.role) ? s_phi : s_psi;
   const double2* partner = (MODE == MODE_SPLIT && grp.role) ? s_psi : s_phi;
-  for (int sg = sb; sg < se; ++sg) {
-    const SegDesc* sd = D.segs + sg;
-    const int nthr = sd->nthr;
-    SegCtx<R> C;
-    C.own = own;
-    C.partner = partner;
-    const ThrEntry* te = D.thr_tab + sd->thr_off + (grp.gi & ((1 << nthr) - 1));
-    const uint2 e01 = *reinterpret_cast<const uint2*>(te);
-    C.J0 = tile_base | e01.x;
-    C.lp0 = e01.y;
-    // folded CNOT runs controlled by tile (non-local) bits
-    if (tile_base != 0) {
+  return SegEnv{D, A, s_psi, s_phi, s_av_all, av_stride, av_base, s_red, s_fin, grp, active, tile_base,
+                bl0, bra, tile, n_tiles, own, partner};
+}
+
+// segment start: address maps and the register load (shared-memory transpose)
+template <int R, int MODE>
+__device__ __forceinline__ void seg_begin(const SegEnv& E, const SegDesc* sd, SegCtx<R>& C, Regs<R>& a, Regs<R>& f) {
+  constexpr int N = 1 << R;
+  const int nthr = sd->nthr;
+  C.own = E.own;
+  C.partner = E.partner;
+  const ThrEntry* te = E.D.thr_tab + sd->thr_off + (E.grp.gi & ((1 << nthr) - 1));
+  const uint2 e01 = *reinterpret_cast<const uint2*>(te);
+  C.J0 = E.tile_base | e01.x;
+  C.lp0 = e01.y;
+  // folded CNOT runs controlled by tile (non-local) bits
+  if (E.tile_base != 0) {
 #pragma unroll
-      for (int t = 0; t < R; ++t)
-        if (__popc(tile_base & sd->ld_k[t]) & 1) C.lp0 ^= sd->ps[t];
+    for (int t = 0; t < R; ++t)
+      if (__popc(E.tile_base & sd->ld_k[t]) & 1) C.lp0 ^= sd->ps[t];
+  }
+#pragma unroll
+  for (int t = 0; t < R; ++t) C.lc[t] = sd->ldc[t];
+  if (E.active) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const uint32_t ad = C.addr(i);
+      a[i] = E.own[ad];
+      if constexpr (MODE == MODE_DUAL) f[i] = E.s_phi[ad];
     }
+  }
+}
+
+// split adjoint: write this thread's registers back for the partner's inner products
+template <int R, int MODE>
+__device__ __forceinline__ void seg_publish(const SegEnv& E, const SegCtx<R>& C, const Regs<R>& a) {
+  if constexpr (MODE == MODE_SPLIT) {
+    __syncthreads();
+    if (E.active) {
+      uint32_t base = C.lp0;
+      asm volatile("" : "+r"(base));
 #pragma unroll
-    for (int t = 0; t < R; ++t) C.lc[t] = sd->ldc[t];
-    double2 a[N], f[N];
-    if (active) {
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        const uint32_t ad = C.addr(i);
-        a[i] = own[ad];
-        if constexpr (DUAL) f[i] = s_phi[ad];
-      }
-    }
-    dbg_add(A, DBG_SEG_LOAD, tdbg);
-    const int ob = sd->op_begin, oe = sd->op_end;
-    Op nxt = ob < oe ? D.ops[ob] : Op{0u, 0u};
-    for (int o = ob; o < oe; ++o) {
-      const Op op = nxt;
-      if (o + 1 < oe) nxt = D.ops[o + 1];
-      if (MODE == MODE_SPLIT && op_code(op.w0) == OP_PUBLISH) {
-        __syncthreads();
-        if (active) {
-          uint32_t base = C.lp0;
-          asm volatile("" : "+r"(base));
-#pragma unroll
-          for (int i = 0; i < N; ++i) {
-            uint32_t ad = base;
-#pragma unroll
-            for (int s = 0; s < R; ++s)
-              if ((i >> s) & 1) ad ^= C.lc[s];
-            own[ad] = a[i];
-          }
-        }
-        __syncthreads();
-        continue;
-      }
-      if (active) exec_op<R, MODE>(D, op, a, f, C, grp.role, T, s_red);
-    }
-    dbg_add(A, DBG_SEG_OPS, tdbg);
-    if (MODE == MODE_SPLIT && sd->ip_count > 0) __syncthreads();  // partners done reading
-    asm volatile("" ::: "memory");  // keep the store map's loads and math after the op loop
-    if (active) {
-      uint32_t sp0 = te->sp0, sc[R];
-      if (tile_base != 0) {
-#pragma unroll
-        for (int t = 0; t < R; ++t)
-          if (__popc(tile_base & sd->st_k[t]) & 1) sp0 ^= sd->ps[t];
-      }
-      asm volatile("" : "+r"(sp0));
-#pragma unroll
-      for (int t = 0; t < R; ++t) sc[t] = sd->stc[t];
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        uint32_t ad = sp0;
+      for (int i = 0; i < (1 << R); ++i) {
+        uint32_t ad = base;
 #pragma unroll
         for (int s = 0; s < R; ++s)
-          if ((i >> s) & 1) ad ^= sc[s];
-        own[ad] = a[i];
-        if constexpr (DUAL) s_phi[ad] = f[i];
+          if ((i >> s) & 1) ad ^= C.lc[s];
+        E.own[ad] = a[i];
       }
     }
     __syncthreads();
-    dbg_add(A, DBG_SEG_STORE, tdbg);
-    if constexpr (MODE != MODE_FWD) {
-      const int nout = sd->ip_count;
-      if (nout > 0) {
-        // phase 1: one warp per (reduction slot, sample) sums the sample's
-        // per-thread partials in a fixed order; phase 2: one thread per
-        // (output, sample) applies the block gradient vector. Blocks narrower
-        // than a warp (tiny n) reduce serially on thread 0.
-        const int nred = sd->red_count;
-        const bool narrow = blockDim.x < 32;
-        const int lane = narrow ? 0 : (threadIdx.x & 31);
-        const int warp = narrow ? (threadIdx.x == 0 ? 0 : 1 << 30) : (threadIdx.x >> 5);
-        const int nwarp = narrow ? 1 : (blockDim.x >> 5);
-        for (int task = warp; task < nred * grp.S; task += nwarp) {
-          const int slot = task / grp.S, s_ = task - slot * grp.S;
-          const double* base = s_red + slot * (int)blockDim.x + s_ * grp.TT;
-          double v = 0.0;
-          if (narrow) {
-            for (int t = 0; t < grp.TT; ++t) v += base[t];
-          } else {
-            for (int t = lane; t < grp.TT; t += 32) v += base[t];
-            for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-          }
-          if (lane == 0) s_fin[slot * grp.S + s_] = v;
-        }
-        __syncthreads();
-        for (int task = threadIdx.x; task < nout * grp.S; task += blockDim.x) {
-          const int oi = task / grp.S, s_ = task - oi * grp.S;
-          const IpOut io = D.ipouts[sd->ip_begin + oi];
-          const double* r = s_fin + s_;
-          double v;
-          if (io.avec < 0) {
-            v = r[io.red * grp.S];
-          } else {
-            const double* av = s_av_all + (size_t)s_ * av_stride + 4 * (io.avec - av_base);
-            v = av[0] * r[io.red * grp.S] + av[1] * r[(io.red + 1) * grp.S] + av[2] * r[(io.red + 2) * grp.S];
-          }
-          const int64_t bl = bl0 + s_;
-          if (bl < A.nb) A.ip[(((bl * A.K) + bra) * D.NG + io.gslot) * n_tiles + tile] = v;
-        }
-      }
-    }
-    dbg_add(A, DBG_SEG_FINAL, tdbg);
   }
 }
+
+// segment end: register store (through the folded store map), barrier, and the
+// segment's gradient outputs
+template <int R, int MODE>
+__device__ __forceinline__ void seg_end(const SegEnv& E, const SegDesc* sd, const Regs<R>& a, const Regs<R>& f) {
+  constexpr int N = 1 << R;
+  const Group& grp = E.grp;
+  const RunArgs& A = E.A;
+  if (MODE == MODE_SPLIT && sd->ip_count > 0) __syncthreads();  // partners done reading
+  asm volatile("" ::: "memory");  // keep the store map's loads and math after the op loop
+  if (E.active) {
+    const ThrEntry* te = E.D.thr_tab + sd->thr_off + (grp.gi & ((1 << sd->nthr) - 1));
+    uint32_t sp0 = te->sp0, sc[R];
+    if (E.tile_base != 0) {
+#pragma unroll
+      for (int t = 0; t < R; ++t)
+        if (__popc(E.tile_base & sd->st_k[t]) & 1) sp0 ^= sd->ps[t];
+    }
+    asm volatile("" : "+r"(sp0));
+#pragma unroll
+    for (int t = 0; t < R; ++t) sc[t] = sd->stc[t];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      uint32_t ad = sp0;
+#pragma unroll
+      for (int s = 0; s < R; ++s)
+        if ((i >> s) & 1) ad ^= sc[s];
+      E.own[ad] = a[i];
+      if constexpr (MODE == MODE_DUAL) E.s_phi[ad] = f[i];
+    }
+  }
+  __syncthreads();
+  if constexpr (MODE != MODE_FWD) {
+    const int nout = sd->ip_count;
+    if (nout > 0) {
+      // phase 1: one warp per (reduction slot, sample) sums the sample's
+      // per-thread partials in a fixed order; phase 2: one thread per
+      // (output, sample) applies the block gradient vector. Blocks narrower
+      // than a warp (tiny n) reduce serially on thread 0.
+      const int nred = sd->red_count;
+      const bool narrow = blockDim.x < 32;
+      const int lane = narrow ? 0 : (threadIdx.x & 31);
+      const int warp = narrow ? (threadIdx.x == 0 ? 0 : 1 << 30) : (threadIdx.x >> 5);
+      const int nwarp = narrow ? 1 : (blockDim.x >> 5);
+      for (int task = warp; task < nred * grp.S; task += nwarp) {
+        const int slot = task / grp.S, s_ = task - slot * grp.S;
+        const double* base = E.s_red + slot * (int)blockDim.x + s_ * grp.TT;
+        double v = 0.0;
+        if (narrow) {
+          for (int t = 0; t < grp.TT; ++t) v += base[t];
+        } else {
+          for (int t = lane; t < grp.TT; t += 32) v += base[t];
+          for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        }
+        if (lane == 0) E.s_fin[slot * grp.S + s_] = v;
+      }
+      __syncthreads();
+      for (int task = threadIdx.x; task < nout * grp.S; task += blockDim.x) {
+        const int oi = task / grp.S, s_ = task - oi * grp.S;
+        const IpOut io = E.D.ipouts[sd->ip_begin + oi];
+        const double* r = E.s_fin + s_;
+        double v;
+        if (io.avec < 0) {
+          v = r[io.red * grp.S];
+        } else {
+          const double* av = E.s_av_all + (size_t)s_ * E.av_stride + 4 * (io.avec - E.av_base);
+          v = av[0] * r[io.red * grp.S] + av[1] * r[(io.red + 1) * grp.S] + av[2] * r[(io.red + 2) * grp.S];
+        }
+        const int64_t bl = E.bl0 + s_;
+        if (bl < A.nb) A.ip[(((bl * A.K) + E.bra) * E.D.NG + io.gslot) * E.n_tiles + E.tile] = v;
+      }
+    }
+  }
+}
+
+// Interpreter: run segments [sb, se) on the tile(s) in shared memory.
+// MODE_FWD: psi only; MODE_DUAL: each thread holds psi and phi of its register
+// group; MODE_SPLIT: role-0 threads hold psi, role-1 threads phi. Gradient
+// outputs go to A.ip (rows relative to A.b0, times n_tiles). Threads with
+// active == false only take part in the barriers.
+struct InterpSegs {
+  template <int R, int MODE>
+  __device__ __forceinline__ static void run(const SegEnv& E, const SampleTables& T, int sb, int se) {
+    const DevProgram& D = E.D;
+    long long tdbg = E.A.dbg ? clock64() : 0;
+    for (int sg = sb; sg < se; ++sg) {
+      const SegDesc* sd = D.segs + sg;
+      SegCtx<R> C;
+      Regs<R> a, f;
+      seg_begin<R, MODE>(E, sd, C, a, f);
+      dbg_add(E.A, DBG_SEG_LOAD, tdbg);
+      const int ob = sd->op_begin, oe = sd->op_end;
+      Op nxt = ob < oe ? D.ops[ob] : Op{0u, 0u};
+      for (int o = ob; o < oe; ++o) {
+        const Op op = nxt;
+        if (o + 1 < oe) nxt = D.ops[o + 1];
+        if (MODE == MODE_SPLIT && op_code(op.w0) == OP_PUBLISH) {
+          seg_publish<R, MODE>(E, C, a);
+          continue;
+        }
+        if (E.active) exec_op<R, MODE>(D, op, a, f, C, E.grp.role, T, E.s_red);
+      }
+      dbg_add(E.A, DBG_SEG_OPS, tdbg);
+      seg_end<R, MODE>(E, sd, a, f);
+      dbg_add(E.A, DBG_SEG_FINAL, tdbg);
+    }
+  }
+};
 
 // Per-sample tables for one pass: (cos, sin) of every rotation, then each
 // fused block's unitary and gradient vectors (blockmath.h). Ends synchronised.

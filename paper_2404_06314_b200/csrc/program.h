@@ -14,7 +14,19 @@
 // in registers; diagonal gates (RZ, CZ) and CNOT controls may sit on any qubit
 // (their effect on non-register bits is a per-thread constant).
 #pragma once
+#ifdef __CUDACC_RTC__
+// NVRTC (jit.cpp) has no system include path: the fixed-width types it needs
+typedef unsigned int uint32_t;
+typedef int int32_t;
+typedef long long int64_t;
+typedef unsigned long long uint64_t;
+typedef short int16_t;
+typedef unsigned short uint16_t;
+typedef signed char int8_t;
+typedef unsigned char uint8_t;
+#else
 #include <stdint.h>
+#endif
 
 #ifdef __CUDACC__
 #define VQC_HD __host__ __device__

@@ -456,7 +456,9 @@ std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total
           }
           it.id = set_id;
           const uint32_t ids = (uint32_t)set_id;
-          op.w0 = enc(OP_U2SET, 0, 0, 0, false);
+          uint32_t smask = 0;  // slots of the set (operand b): compile-time dispatch in the kernels
+          for (const Item& sub : it.sub) smask |= 1u << slot_of[gates[sub.gates[0]].q0];
+          op.w0 = enc(OP_U2SET, 0, smask, 0, false);
           op.param = ids;
           P->ops.push_back(op);
           continue;
@@ -578,7 +580,9 @@ std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total
             }
             nred += 3 * __builtin_popcount(gmask);
           }
-          op.w0 = enc(OP_U2SET, 0, 0, 0, true);
+          uint32_t smask = 0;
+          for (const Item& sub : it.sub) smask |= 1u << slot_of[gates[sub.gates[0]].q0];
+          op.w0 = enc(OP_U2SET, 0, smask, 0, true);
           op.param = (uint32_t)it.id;
           P->ops.push_back(op);
           continue;

@@ -1,0 +1,386 @@
+// Kernel skeletons shared by the prebuilt interpreter kernels (engine.cu) and
+// the per-plan JIT kernels (jit.cpp): staging, expectations / adjoint seed,
+// tile load / store. The segment work is a policy (SEGS::run<R, MODE>):
+// InterpSegs decodes the device program at run time, a JIT policy is
+// straight-line code with every operand a compile-time constant.
+#pragma once
+#include "kernels.cuh"
+
+namespace vqc {
+
+// Observable terms staged in shared memory (Z strings only on this path).
+struct TermSm {
+  uint32_t mask;   // sign mask (Y/Z letters)
+  int32_t obs;     // observable index
+  uint32_t xmask;  // flip mask (X/Y letters); 0 for Z strings
+  int32_t phase;   // i^phase = i^{#Y}
+  double coeff;
+};
+
+__device__ __forceinline__ void stage_terms(const DevProgram& D, TermSm* s_terms) {
+  for (int t = threadIdx.x; t < D.T; t += blockDim.x) {
+    TermSm ts;
+    ts.mask = D.t_smask[t];
+    ts.xmask = D.t_xmask[t];
+    ts.phase = D.t_phase[t];
+    ts.coeff = D.t_coeff[t];
+    int m = 0;
+    while (D.term_offs[m + 1] <= t) ++m;
+    ts.obs = m;
+    s_terms[t] = ts;
+  }
+}
+
+// Expectations (observables.py / _kernels.py:182-198, Z strings) and the
+// adjoint seed phi = w(j) psi with w = sum_m u_m O_m(j) (VJP) or O_bra(j)
+// (_kernels.py:209-217). Each thread owns `count` tile elements; a term's
+// sign over them is parity(base & s) ^ parity(i & h), h bit b =
+// parity(hi[b] & s), so no per-element index arithmetic is needed.
+template <bool DUAL>
+__device__ __forceinline__ void observe(const DevProgram& D, const RunArgs& A, const PassDesc* pd, double2* s_psi,
+                                        double2* s_phi, const double* s_u_row, const TermSm* s_terms,
+                                        const Group& grp, double* s_red, double* s_fin, uint32_t tile_base, int k,
+                                        int64_t bl0, bool do_expect, int seed_mode, int bra, int tile,
+                                        int n_tiles) {
+  constexpr int E = 1 << kMaxR;
+  const int lane = grp.lane_in_sample();
+  const TileWalk tw = tile_walk(pd, tile_base, k, lane, grp.TT);
+  const int count = tw.count;
+  auto term_bits = [&](uint32_t mask, uint32_t& p0, uint32_t& h) {
+    p0 = (uint32_t)__popc(tw.base & mask) & 1u;
+    h = 0;
+#pragma unroll
+    for (int b = 0; b < kMaxR; ++b) h |= ((uint32_t)__popc(tw.hi[b] & mask) & 1u) << b;
+  };
+  if (do_expect) {
+    double p2[E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      p2[i] = 0.0;
+      if (i < count) {
+        const double2 x = s_psi[swz((uint32_t)lane + (uint32_t)i * (uint32_t)grp.TT)];
+        p2[i] = x.x * x.x + x.y * x.y;
+      }
+    }
+    for (int m = 0; m < D.M; ++m) s_red[m * (int)blockDim.x + threadIdx.x] = 0.0;
+    for (int t = 0; t < D.T; ++t) {
+      const TermSm ts = s_terms[t];
+      if (ts.xmask != 0u) continue;
+      uint32_t p0, h;
+      term_bits(ts.mask, p0, h);
+      double v = 0.0;
+#pragma unroll
+      for (int i = 0; i < E; ++i)
+        if (i < count) v += ((p0 ^ (uint32_t)__popc((uint32_t)i & h)) & 1u) ? -p2[i] : p2[i];
+      s_red[ts.obs * (int)blockDim.x + threadIdx.x] += ts.coeff * v;
+    }
+    if (D.has_xy) {
+      // X/Y strings (on-chip states only): Re sum_j conj(psi_j) i^k (-1)^{popc((j^x)&s)} psi_{j^x}
+      for (int t = 0; t < D.T; ++t) {
+        const TermSm ts = s_terms[t];
+        if (ts.xmask == 0u) continue;
+        double v = 0.0;
+        for (int i = 0; i < count; ++i) {
+          const uint32_t l = (uint32_t)lane + (uint32_t)i * (uint32_t)grp.TT;
+          const uint32_t kx = l ^ ts.xmask;
+          const double2 a = s_psi[swz(l)], bq = s_psi[swz(kx)];
+          // conj(a) * bq
+          double re = a.x * bq.x + a.y * bq.y, im = a.x * bq.y - a.y * bq.x;
+          const int ph = ts.phase & 3;  // multiply by i^ph, keep the real part
+          double r = ph == 0 ? re : ph == 1 ? -im : ph == 2 ? -re : im;
+          v += (__popc(kx & ts.mask) & 1) ? -r : r;
+        }
+        s_red[ts.obs * (int)blockDim.x + threadIdx.x] += ts.coeff * v;
+      }
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane32 = threadIdx.x & 31, nwarp = (blockDim.x + 31) >> 5;
+    const bool narrow = blockDim.x < 32;
+    for (int task = warp; task < D.M * grp.S; task += nwarp) {
+      const int m = task / grp.S, s_ = task - m * grp.S;
+      const double* base = s_red + m * (int)blockDim.x + s_ * grp.TT;
+      double v = 0.0;
+      if (narrow) {
+        if (lane32 == 0)
+          for (int t = 0; t < grp.TT; ++t) v += base[t];
+      } else {
+        for (int t = lane32; t < grp.TT; t += 32) v += base[t];
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      }
+      const int64_t bl = bl0 + s_;
+      if (lane32 == 0 && bl < A.nb) A.expect[(bl * D.M + m) * n_tiles + tile] = v;
+    }
+    __syncthreads();
+  }
+  if constexpr (DUAL) {
+    if (seed_mode != 0) {
+      double w[E];
+#pragma unroll
+      for (int i = 0; i < E; ++i) w[i] = 0.0;
+      for (int t = 0; t < D.T; ++t) {
+        const TermSm ts = s_terms[t];
+        if (ts.xmask != 0u) continue;
+        const double e = seed_mode == 1 ? s_u_row[ts.obs] * ts.coeff : (ts.obs == bra ? ts.coeff : 0.0);
+        if (e == 0.0) continue;
+        uint32_t p0, h;
+        term_bits(ts.mask, p0, h);
+#pragma unroll
+        for (int i = 0; i < E; ++i) w[i] += ((p0 ^ (uint32_t)__popc((uint32_t)i & h)) & 1u) ? -e : e;
+      }
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        if (i >= count) break;
+        const uint32_t l = (uint32_t)lane + (uint32_t)i * (uint32_t)grp.TT;
+        const uint32_t p = swz(l);
+        const double2 x = s_psi[p];
+        double2 phi = make_double2(w[i] * x.x, w[i] * x.y);
+        if (D.has_xy) {
+          // pauli_sum_apply (_kernels.py:166-179) for the X/Y strings
+          for (int t = 0; t < D.T; ++t) {
+            const TermSm ts = s_terms[t];
+            if (ts.xmask == 0u) continue;
+            const double e = seed_mode == 1 ? s_u_row[ts.obs] * ts.coeff : (ts.obs == bra ? ts.coeff : 0.0);
+            if (e == 0.0) continue;
+            const uint32_t kx = l ^ ts.xmask;
+            const double2 bq = s_psi[swz(kx)];
+            const int ph = ts.phase & 3;
+            double2 v = ph == 0 ? bq : ph == 1 ? make_double2(-bq.y, bq.x)
+                      : ph == 2 ? make_double2(-bq.x, -bq.y) : make_double2(bq.y, -bq.x);
+            const double sg = (__popc(kx & ts.mask) & 1) ? -e : e;
+            phi.x += sg * v.x;
+            phi.y += sg * v.y;
+          }
+        }
+        s_phi[p] = phi;
+      }
+    }
+  }
+}
+
+// Shared-memory carve-up (kernels and host sizing must agree).
+struct SmemLayout {
+  size_t psi, phi, cs, u, av, red, fin, up, terms, total;  // byte offsets
+  __host__ __device__ SmemLayout(int S, int n_amp, bool dual, int nrot, int nblk, int nav, int red_slots,
+                                 int threads, int M, int n_terms) {
+    size_t o = 0;
+    psi = o; o += (size_t)S * n_amp * 16;
+    phi = o; o += dual ? (size_t)S * n_amp * 16 : 0;
+    cs = o; o += (size_t)S * nrot * 16;
+    u = o; o += (size_t)S * nblk * 64;
+    av = o; o += (size_t)S * nav * 32;
+    red = o; o += (size_t)red_slots * threads * 8;
+    fin = o; o += (size_t)red_slots * S * 8;
+    up = o; o += (size_t)S * M * 8;
+    terms = o; o += (size_t)n_terms * sizeof(TermSm);
+    total = o + 16;
+  }
+};
+
+// kernel modes: forward only / adjoint with both states per thread (small n) /
+// adjoint split over (psi, phi) thread pairs
+enum { KM_FWD = 0, KM_DUAL = 1, KM_SPLIT = 2 };
+
+template <int R, int KM>
+__device__ __forceinline__ Group make_group(int threads_per_role, int samples) {
+  Group g;
+  g.tid = threadIdx.x;
+  g.TPS = threads_per_role;
+  g.TT = KM == KM_SPLIT ? 2 * threads_per_role : threads_per_role;
+  g.S = samples;
+  const int lane = threadIdx.x % g.TT;
+  g.sl = threadIdx.x / g.TT;
+  g.role = lane / g.TPS;
+  g.gi = lane % g.TPS;
+  g.W = g.TT >= 32 ? g.TT >> 5 : 1;
+  return g;
+}
+
+// Whole state on chip: one CTA owns S samples of n <= 12 qubits and runs
+// forward, expectations, seed and the adjoint sweep without touching HBM.
+__host__ __device__ constexpr int smem_max_threads(int R, int KM) {
+  return R >= 5 ? 256 : (KM == KM_SPLIT ? 512 : (R >= 4 ? 256 : 512));
+}
+__host__ __device__ constexpr int pass_max_threads(int R) { return R >= 5 ? 256 : 512; }
+
+template <int R, int KM, class SEGS>
+__device__ __forceinline__ void smem_body(const DevProgram& D, const RunArgs& A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr bool ADJ = KM != KM_FWD;
+  constexpr int BM = KM == KM_SPLIT ? MODE_SPLIT : MODE_DUAL;
+  const int n = D.n, N = 1 << n;
+  const Group grp = make_group<R, KM>(1 << (n - R), A.S);
+  const int lane = grp.lane_in_sample();
+  const int64_t bl0 = (int64_t)blockIdx.x * A.S;
+  const int64_t bl = bl0 + grp.sl;
+  const bool valid = bl < A.nb;
+  const int64_t b = A.b0 + (valid ? bl : 0);
+  const PassDesc* pd = D.passes;
+  const int nrot = D.n_rot, nblk = D.n_blk, nav = D.n_av;
+  const SmemLayout L(A.S, N, ADJ, nrot, nblk, nav, A.red_slots, (int)blockDim.x, D.M, D.T);
+  double2* s_psi = reinterpret_cast<double2*>(smem_raw + L.psi) + (size_t)grp.sl * N;
+  double2* s_phi = reinterpret_cast<double2*>(smem_raw + L.phi) + (size_t)grp.sl * N;
+  double2* s_cs = reinterpret_cast<double2*>(smem_raw + L.cs) + (size_t)grp.sl * nrot;
+  double2* s_u = reinterpret_cast<double2*>(smem_raw + L.u) + (size_t)grp.sl * nblk * 4;
+  double* s_av_all = reinterpret_cast<double*>(smem_raw + L.av);
+  double* s_red = reinterpret_cast<double*>(smem_raw + L.red);
+  double* s_fin = reinterpret_cast<double*>(smem_raw + L.fin);
+  double* s_up = reinterpret_cast<double*>(smem_raw + L.up);
+  TermSm* s_terms = reinterpret_cast<TermSm*>(smem_raw + L.terms);
+  stage_terms(D, s_terms);
+
+  for (int l = lane; l < N; l += grp.TT) s_psi[swz((uint32_t)l)] = make_double2(l == 0 ? 1.0 : 0.0, 0.0);
+  if (ADJ && A.upstream != nullptr)
+    for (int m = lane; m < D.M; m += grp.TT) s_up[grp.sl * D.M + m] = valid ? A.upstream[b * D.M + m] : 0.0;
+  build_tables(D, A, pd, b, valid, s_cs, s_u, s_av_all + (size_t)grp.sl * nav * 4, lane, grp.TT);
+  const SampleTables T{s_cs, s_u, 0, 0};
+
+  SEGS::template run<R, MODE_FWD>(make_env<MODE_FWD>(D, A, s_psi, s_psi, s_av_all, nav * 4, 0, s_red, s_fin,
+                            grp, grp.role == 0, 0u, bl0, 0, 0, 1), T, pd->seg_begin, pd->seg_end);
+  if constexpr (!ADJ) {
+    observe<false>(D, A, nullptr, s_psi, s_psi, nullptr, s_terms, grp, s_red, s_fin, 0u, n, bl0, true, 0, 0, 0, 1);
+  } else {
+    if (!A.jacobian) {
+      observe<true>(D, A, nullptr, s_psi, s_phi, s_up + grp.sl * D.M, s_terms, grp, s_red, s_fin, 0u, n, bl0,
+                    A.expect != nullptr, 1, 0, 0, 1);
+      __syncthreads();
+      SEGS::template run<R, BM>(make_env<BM>(D, A, s_psi, s_phi, s_av_all, nav * 4, 0, s_red, s_fin,
+                          grp, true, 0u, bl0, 0, 0, 1), T, pd->bseg_begin, pd->bseg_end);
+    } else {
+      observe<true>(D, A, nullptr, s_psi, s_phi, nullptr, s_terms, grp, s_red, s_fin, 0u, n, bl0,
+                    A.expect != nullptr, 0, 0, 0, 1);
+      double2* fin = A.psi_fin + (size_t)bl * N;
+      if (D.M > 1 && valid)
+        for (int l = lane; l < N; l += grp.TT) fin[l] = s_psi[swz((uint32_t)l)];
+      for (int m = 0; m < D.M; ++m) {
+        if (m > 0) {
+          __syncthreads();
+          if (valid)
+            for (int l = lane; l < N; l += grp.TT) s_psi[swz((uint32_t)l)] = fin[l];
+        }
+        observe<true>(D, A, nullptr, s_psi, s_phi, nullptr, s_terms, grp, s_red, s_fin, 0u, n, bl0, false, 2, m,
+                      0, 1);
+        __syncthreads();
+        SEGS::template run<R, BM>(make_env<BM>(D, A, s_psi, s_phi, s_av_all, nav * 4, 0,
+                            s_red, s_fin, grp, true, 0u, bl0, m, 0, 1), T, pd->bseg_begin, pd->bseg_end);
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// One pass over HBM-resident states: CTA (tile, row) stages 2^k amplitudes.
+template <int R, int KM, class SEGS>
+__device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr bool ADJ = KM != KM_FWD;
+  const PassDesc* pd = D.passes + A.pass;
+  const int k = pd->k, Nt = 1 << k;
+  const uint32_t flags = A.flags;
+  const Group grp = make_group<R, KM>(1 << (k - R), 1);
+  const int tile = blockIdx.x, n_tiles = gridDim.x;
+  const int64_t bl = blockIdx.y;
+  const int64_t b = A.b0 + bl;
+  const size_t N = (size_t)1 << D.n;
+  uint32_t tile_base = 0;
+  {
+    const uint32_t lm = pd->local_mask;
+    int c = 0;
+    for (int q = 0; q < D.n; ++q)
+      if (!((lm >> q) & 1u)) tile_base |= (((uint32_t)tile >> c++) & 1u) << q;
+  }
+  const SmemLayout L(1, Nt, ADJ, D.max_rot_pass, D.max_blk_pass, D.max_av_pass, A.red_slots, (int)blockDim.x,
+                     D.M, D.T);
+  double2* s_psi = reinterpret_cast<double2*>(smem_raw + L.psi);
+  double2* s_phi = reinterpret_cast<double2*>(smem_raw + L.phi);
+  double2* s_cs = reinterpret_cast<double2*>(smem_raw + L.cs);
+  double2* s_u = reinterpret_cast<double2*>(smem_raw + L.u);
+  double* s_av = reinterpret_cast<double*>(smem_raw + L.av);
+  double* s_red = reinterpret_cast<double*>(smem_raw + L.red);
+  double* s_fin = reinterpret_cast<double*>(smem_raw + L.fin);
+  double* s_up = reinterpret_cast<double*>(smem_raw + L.up);
+  TermSm* s_terms = reinterpret_cast<TermSm*>(smem_raw + L.terms);
+  if (flags & (F_OBSERVE | F_SEED)) stage_terms(D, s_terms);
+
+  long long tdbg = A.dbg ? clock64() : 0;
+  if (A.dbg && threadIdx.x == 0) atomicAdd(A.dbg + DBG_CTAS, 1ull);
+  if (ADJ && (flags & F_SEED) && A.bra < 0)
+    for (int m = threadIdx.x; m < D.M; m += blockDim.x) s_up[m] = A.upstream[b * D.M + m];
+  if (flags & F_INIT) {
+    for (int l = threadIdx.x; l < Nt; l += blockDim.x)
+      s_psi[swz((uint32_t)l)] = make_double2((tile_base == 0 && l == 0) ? 1.0 : 0.0, 0.0);
+  } else {
+    // asynchronous 16-byte copies straight into the swizzled tile; they land
+    // while the per-sample tables are built
+    const double2* src = ((flags & F_LOAD_FIN) ? A.psi_fin : A.psi) + (size_t)bl * N;
+    const double2* srcf = A.phi + (size_t)bl * N;
+    const bool lphi = ADJ && (flags & F_LOAD_PHI);
+    const TileWalk tw = tile_walk(pd, tile_base, k, threadIdx.x, blockDim.x);
+    for_tile(tw, threadIdx.x, blockDim.x, [&](uint32_t l, uint32_t j) {
+      cp_async16(s_psi + swz(l), src + j);
+      if (lphi) cp_async16(s_phi + swz(l), srcf + j);
+    });
+  }
+  if (A.tables != nullptr) {
+    // per-sample tables precomputed by k_tables: copy this pass's slices
+    const double* t = A.tables + (size_t)bl * A.table_stride;
+    const int nrot = pd->rot_end - pd->rot_begin, nblk = pd->blk_end - pd->blk_begin,
+              nav = pd->av_end - pd->av_begin;
+    const double* tcs = t + 2 * pd->rot_begin;
+    const double* tu = t + 2 * (size_t)D.n_rot + 8 * (size_t)pd->blk_begin;
+    const double* tav = t + 2 * (size_t)D.n_rot + 8 * (size_t)D.n_blk + 4 * (size_t)pd->av_begin;
+    for (int i = threadIdx.x; i < nrot; i += blockDim.x) cp_async16(s_cs + i, tcs + 2 * i);
+    for (int i = threadIdx.x; i < 4 * nblk; i += blockDim.x) cp_async16(s_u + i, tu + 2 * i);
+    for (int i = threadIdx.x; i < 2 * nav; i += blockDim.x) cp_async16(s_av + 2 * i, tav + 2 * i);
+  } else {
+    build_tables(D, A, pd, b, true, s_cs, s_u, s_av, threadIdx.x, blockDim.x);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  dbg_add(A, DBG_PROLOGUE, tdbg);
+  const SampleTables T{s_cs, s_u, pd->rot_begin, pd->blk_begin};
+  if (flags & F_FWD)
+    SEGS::template run<R, MODE_FWD>(make_env<MODE_FWD>(D, A, s_psi, s_psi, s_av, 0, pd->av_begin, s_red, s_fin,
+                              grp, grp.role == 0, tile_base, bl, 0, tile, n_tiles), T, pd->seg_begin, pd->seg_end);
+  dbg_add(A, DBG_FWD, tdbg);
+  if (flags & F_STORE_FIN) {
+    uint32_t tb = tile_base;
+    asm volatile("" : "+r"(tb));
+    const TileWalk tw = tile_walk(pd, tb, k, threadIdx.x, blockDim.x);
+    double2* dst = A.psi_fin + (size_t)bl * N;
+    for_tile(tw, threadIdx.x, blockDim.x, [&](uint32_t l, uint32_t j) { dst[j] = s_psi[swz(l)]; });
+  }
+  if (flags & (F_OBSERVE | F_SEED)) {
+    observe<ADJ>(D, A, pd, s_psi, s_phi, s_up, s_terms, grp, s_red, s_fin, tile_base, k, bl, (flags & F_OBSERVE) != 0,
+                 (flags & F_SEED) ? (A.bra < 0 ? 1 : 2) : 0, A.bra, tile, n_tiles);
+    __syncthreads();
+  }
+  dbg_add(A, DBG_OBSERVE, tdbg);
+  if constexpr (ADJ) {
+    if (flags & F_BWD)
+      SEGS::template run<R, MODE_SPLIT>(make_env<MODE_SPLIT>(D, A, s_psi, s_phi, s_av, 0, pd->av_begin,
+                                  s_red, s_fin, grp, true, tile_base, bl, A.bra < 0 ? 0 : A.bra, tile, n_tiles), T, pd->bseg_begin, pd->bseg_end);
+  }
+  dbg_add(A, DBG_BWD, tdbg);
+  const bool sphi = ADJ && (flags & F_STORE_PHI);
+  if ((flags & F_STORE_PSI) || sphi) {
+    asm volatile("" ::: "memory");
+    uint32_t tb = tile_base;
+    asm volatile("" : "+r"(tb));  // rebuild the tile walk here rather than keep it live
+    const TileWalk tw = tile_walk(pd, tb, k, threadIdx.x, blockDim.x);
+    const bool spsi = (flags & F_STORE_PSI) != 0;
+    double2* dst = A.psi + (size_t)bl * N;
+    double2* dstf = A.phi + (size_t)bl * N;
+    for_tile(tw, threadIdx.x, blockDim.x, [&](uint32_t l, uint32_t j) {
+      if (spsi) dst[j] = s_psi[swz(l)];
+      if (sphi) dstf[j] = s_phi[swz(l)];
+    });
+  }
+  dbg_add(A, DBG_STORE, tdbg);
+}
+
+}  // namespace vqc

@@ -29,7 +29,7 @@ EXPORTED_SYMBOLS = (
     "vqc_plan_create", "vqc_plan_destroy", "vqc_plan_num_cols", "vqc_plan_num_obs",
     "vqc_plan_mode", "vqc_plan_describe", "vqc_workspace_bytes", "vqc_forward", "vqc_adjoint",
     "vqc_run_batch_host", "vqc_last_launch_count", "vqc_profile_enable", "vqc_profile_report",
-    "vqc_last_error", "vqc_abi_version",
+    "vqc_last_error", "vqc_abi_version", "vqc_jit_source",
 )
 
 
@@ -82,6 +82,9 @@ def load_library(path: str | None = None):
         lib.vqc_run_batch_host.restype = ctypes.c_int
         lib.vqc_run_batch_host.argtypes = [_VP, _F64P, _F64P, ctypes.c_int64, _F64P, _F64P, _F64P,
                                            _F64P, _F64P]
+        lib.vqc_jit_source.restype = ctypes.c_int64
+        lib.vqc_jit_source.argtypes = [ctypes.POINTER(VqcCircuit), _I64P, ctypes.c_int, ctypes.c_char_p,
+                                       ctypes.c_int64, ctypes.POINTER(ctypes.c_double)]
         lib.vqc_last_launch_count.restype = ctypes.c_int64
         lib.vqc_last_launch_count.argtypes = []
         lib.vqc_profile_enable.restype = None
@@ -206,6 +209,26 @@ class Plan:
         _check(self._lib.vqc_run_batch_host(self._h, p(inputs), p(weights), B, p(up), p(expect),
                                             p(jac), p(rows), p(vsum)), "vqc_run_batch_host")
         return expect, jac, rows, vsum
+
+
+def jit_source(compiled, wrt_col, enc_offset: int, enc_size: int, compile: bool = False):
+    """(CUDA source, NVRTC compile seconds or None) of the kernels a plan for
+    this circuit would JIT-compile; runs on the CPU (no device needed)."""
+    lib = load_library()
+    keep = [_i64(compiled.kinds), _i64(compiled.q0), _i64(compiled.q1), _f64(compiled.coeff),
+            _i64(compiled.f_offs), _i64(compiled.f_idx if len(compiled.f_idx) else np.zeros(1, np.int64)),
+            _i64(wrt_col if len(wrt_col) else np.zeros(1, np.int64))]
+    circ = VqcCircuit(compiled.num_qubits, len(compiled.kinds), keep[0].ctypes.data_as(_I64P),
+                      keep[1].ctypes.data_as(_I64P), keep[2].ctypes.data_as(_I64P),
+                      keep[3].ctypes.data_as(_F64P), keep[4].ctypes.data_as(_I64P),
+                      keep[5].ctypes.data_as(_I64P), compiled.total_params, enc_offset, enc_size)
+    secs = ctypes.c_double(0.0)
+    n = lib.vqc_jit_source(ctypes.byref(circ), keep[6].ctypes.data_as(_I64P), 1 if compile else 0, None, 0,
+                           ctypes.byref(secs))
+    _check(int(n) if n < 0 else 0, "vqc_jit_source")
+    buf = ctypes.create_string_buffer(int(n) + 1)
+    lib.vqc_jit_source(ctypes.byref(circ), keep[6].ctypes.data_as(_I64P), 0, buf, int(n) + 1, None)
+    return buf.value.decode(), (secs.value if compile else None)
 
 
 def last_launch_count() -> int:

@@ -123,6 +123,12 @@ std::string check_program(const HostProgram& P, const ScheduleOptions& opt) {
               if (id >= pd.blk_end - pd.blk_begin) return "set block id out of range";
             }
             if (code == OP_IP3SET && (b & ~((1u << sd.nreg) - 1u))) return "IP3SET mask beyond slots";
+            if (code == OP_U2SET) {
+              uint32_t m = 0;
+              for (int sl = 0; sl < kMaxR; ++sl)
+                if (P.setids[op.param * kMaxR + sl] >= 0) m |= 1u << sl;
+              if (m != b) return "U2SET slot mask (operand b) disagrees with its block ids";
+            }
             break;
           case OP_U2: case OP_IP3:
             if ((int)op.param < pd.blk_begin || (int)op.param >= pd.blk_end) return "block id outside pass range";
