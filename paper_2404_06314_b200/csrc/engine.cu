@@ -571,7 +571,8 @@ int check_common(const VqcPlan* p, const double* d_in, const double* d_w, int64_
 
 // flat gate list -> scheduled device program (shared by plan creation and
 // the CPU-side JIT source dump)
-int schedule_circuit(const VqcCircuit* c, const int64_t* wrt_col, HostProgram* prog) {
+int schedule_circuit(const VqcCircuit* c, const int64_t* wrt_col, HostProgram* prog,
+                     std::vector<uint32_t>* zmask = nullptr, std::vector<double>* zcoeff = nullptr) {
   std::vector<GateIn> gates((size_t)c->n_gates);
   for (int64_t g = 0; g < c->n_gates; ++g) {
     GateIn& gi = gates[g];
@@ -589,13 +590,16 @@ int schedule_circuit(const VqcCircuit* c, const int64_t* wrt_col, HostProgram* p
   }
   std::vector<int64_t> wcol((size_t)c->total_params, -1);
   for (int64_t i = 0; i < c->total_params; ++i) wcol[i] = wrt_col[i];
+  if (zmask) prog->absorbed = absorb_trailing_gates(&gates, c->n_qubits, zmask, zcoeff);
   ScheduleOptions opt;
   opt.tile_qubits = env_int("VQC_TILE_QUBITS", 11);
   opt.segment_cost = env_int("VQC_SEGMENT_COST", 4);
   // four register slots (16 amplitudes per thread); the scheduler and its
   // CPU checker also handle 3 and 5 (tests/test_scheduler_sim.py)
   opt.reg_slots = 4;
+  const int absorbed = prog->absorbed;
   std::string err = build_program(gates, c->n_qubits, c->total_params, wcol, opt, prog);
+  prog->absorbed = absorbed;
   if (!err.empty())
     return fail(err.find("out of range") != std::string::npos || err.find("duplicate") != std::string::npos
                     ? VQC_E_INVALID
@@ -618,7 +622,9 @@ int64_t vqc_jit_source(const VqcCircuit* c, const int64_t* wrt_col, int compile,
   if (!c || (c->total_params > 0 && !wrt_col)) return fail(VQC_E_INVALID, "NULL argument");
   if (c->n_qubits < 1 || c->n_qubits > kMaxQubits) return fail(VQC_E_INVALID, "num_qubits must be in [1, 24]");
   HostProgram prog;
-  if (int rc = schedule_circuit(c, wrt_col, &prog)) return rc;
+  std::vector<uint32_t> zm;  // as for Z-string observables (trailing gates absorbed)
+  std::vector<double> zc;
+  if (int rc = schedule_circuit(c, wrt_col, &prog, &zm, &zc)) return rc;
   const std::string src = jit_source(prog, use_split(prog.n, prog.R));
   if (compile) {
     std::string err = jit_compile_only(prog, use_split(prog.n, prog.R), compile_s);
@@ -687,11 +693,6 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
   if (c->total_params > 0 && !wrt_col) return fail(VQC_E_INVALID, "wrt_col is NULL");
 
   VqcPlan* p = new VqcPlan();
-  if (int rc = schedule_circuit(c, wrt_col, &p->prog)) {
-    delete p;
-    return rc;
-  }
-  std::string err;
   p->total_params = c->total_params;
   p->enc_off = c->enc_offset;
   p->enc_size = c->enc_size;
@@ -732,6 +733,14 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
     }
     p->term_offs[m + 1] = (int32_t)p->smask.size();
   }
+  // Z-only observables absorb the circuit's trailing CNOT / CZ / X gates
+  // (G^dagger O G is again a Z string): fewer state passes, same results
+  if (int rc = schedule_circuit(c, wrt_col, &p->prog, p->has_xy ? nullptr : &p->smask,
+                                p->has_xy ? nullptr : &p->tcoeff)) {
+    delete p;
+    return rc;
+  }
+  std::string err;
   cudaError_t e = cudaGetDevice(&p->device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, p->device);
   const std::vector<ThrEntry> thr_tab = build_thr_table(p->prog.segs);
@@ -845,10 +854,10 @@ int64_t vqc_plan_describe(const VqcPlan* p, char* buf, int64_t cap) {
                            "{\"n\": %d, \"mode\": \"%s\", \"tile_qubits\": %d, \"reg_slots\": %d, "
                            "\"passes\": %d, \"segments\": %d, \"rotations\": %d, \"grad_slots\": %d, "
                            "\"fwd_ops\": %d, \"bwd_ops\": %d, \"cols\": %d, \"obs\": %d, \"jit\": %s, "
-                           "\"jit_compile_s\": %.3f, \"jit_cubin_bytes\": %zu}",
+                           "\"jit_compile_s\": %.3f, \"jit_cubin_bytes\": %zu, \"absorbed_gates\": %d}",
                            P.n, P.hbm ? "hbm" : "smem", P.k, P.R, (int)P.passes.size(), nseg, P.n_rot,
                            P.NG, P.n_fwd_ops, P.n_bwd_ops, P.n_cols, p->M, p->use_jit ? "true" : "false",
-                           p->jit.compile_s, p->jit.cubin_bytes);
+                           p->jit.compile_s, p->jit.cubin_bytes, P.absorbed);
   if (buf && cap > 0) {
     const int64_t c = std::min<int64_t>(cap - 1, len);
     memcpy(buf, tmp, (size_t)c);

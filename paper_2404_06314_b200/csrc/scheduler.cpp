@@ -187,6 +187,29 @@ uint32_t enc(uint32_t code, uint32_t a, uint32_t b, uint32_t ipl, bool adj) {
 
 }  // namespace
 
+int absorb_trailing_gates(std::vector<GateIn>* gates, int n, std::vector<uint32_t>* zmask,
+                          std::vector<double>* zcoeff) {
+  int count = 0;
+  auto ok_q = [&](int q) { return q >= 0 && q < n; };
+  while (!gates->empty()) {
+    const GateIn& g = gates->back();
+    if (g.kind == G_CNOT || g.kind == G_CZ) {
+      if (!ok_q(g.q0) || !ok_q(g.q1) || g.q0 == g.q1) break;
+      if (g.kind == G_CNOT)
+        for (uint32_t& s : *zmask) s ^= ((s >> g.q1) & 1u) << g.q0;  // CNOT Z_t CNOT = Z_c Z_t
+    } else if (g.kind == G_X) {
+      if (!ok_q(g.q0)) break;
+      for (size_t t = 0; t < zmask->size(); ++t)
+        if (((*zmask)[t] >> g.q0) & 1u) (*zcoeff)[t] = -(*zcoeff)[t];  // X Z X = -Z
+    } else {
+      break;
+    }
+    gates->pop_back();
+    ++count;
+  }
+  return count;
+}
+
 std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total_params,
                           const std::vector<int64_t>& wrt_col, const ScheduleOptions& opt,
                           HostProgram* P) {

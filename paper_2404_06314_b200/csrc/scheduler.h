@@ -49,7 +49,17 @@ struct HostProgram {
   std::vector<ChainEntry> chain;
   // stats
   int n_fwd_ops = 0, n_bwd_ops = 0;
+  int absorbed = 0;  // trailing gates folded into the observables (absorb_trailing_gates)
 };
+
+// Fold the circuit's trailing parameter-free gates that map Z strings to Z
+// strings into the observables: <psi|G^dagger O G|psi> with O a weighted Z
+// string stays a Z string (CNOT: Z_t -> Z_c Z_t; CZ: commutes; X: Z -> -Z).
+// Pops them from `gates` (last gate first) and rewrites each term's sign mask
+// / coefficient. Stops at the first gate that is not such a gate or has
+// invalid qubits (left for build_program to report). Returns the count.
+int absorb_trailing_gates(std::vector<GateIn>* gates, int n_qubits, std::vector<uint32_t>* zmask,
+                          std::vector<double>* zcoeff);
 
 // Returns "" on success, else an error message. wrt_col: flat index -> column or -1.
 std::string build_program(const std::vector<GateIn>& gates, int n_qubits, int64_t total_params,
