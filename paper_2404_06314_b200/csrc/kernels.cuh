@@ -291,20 +291,36 @@ __device__ __forceinline__ double ip_z(P&& p, F&& f, uint32_t slot_mask, bool cb
   }
   return acc;
 }
+// All three Pauli inner products of slot S in one sweep, as explicit FMA
+// chains (12 DFMA per pair) split over two accumulator sets (alternate pairs)
+// so the dependent chains are half as long.
 template <int R, int S, int PART, class P, class F>
 __device__ __forceinline__ void ip_xyz(P&& p, F&& f, double& ix, double& iy, double& iz) {
+  double ax[2] = {0.0, 0.0}, ay[2] = {0.0, 0.0}, az[2] = {0.0, 0.0};
+  int k = 0;
 #pragma unroll
   for (int i = 0; i < (1 << R); ++i)
     if (!((i >> S) & 1) && take_pair<R, S, PART>(i)) {
       const int j = i | (1 << S);
+      const int c = k & 1;
+      ++k;
       const double2 f0 = f(i), f1 = f(j), p0 = p(i), p1 = p(j);
-      ix += f0.x * p1.y - f0.y * p1.x;
-      ix += f1.x * p0.y - f1.y * p0.x;
-      iy -= f0.x * p1.x + f0.y * p1.y;
-      iy += f1.x * p0.x + f1.y * p0.y;
-      iz += f0.x * p0.y - f0.y * p0.x;
-      iz -= f1.x * p1.y - f1.y * p1.x;
+      ax[c] = fma(f0.x, p1.y, ax[c]);
+      ax[c] = fma(-f0.y, p1.x, ax[c]);
+      ax[c] = fma(f1.x, p0.y, ax[c]);
+      ax[c] = fma(-f1.y, p0.x, ax[c]);
+      ay[c] = fma(-f0.x, p1.x, ay[c]);
+      ay[c] = fma(-f0.y, p1.y, ay[c]);
+      ay[c] = fma(f1.x, p0.x, ay[c]);
+      ay[c] = fma(f1.y, p0.y, ay[c]);
+      az[c] = fma(f0.x, p0.y, az[c]);
+      az[c] = fma(-f0.y, p0.x, az[c]);
+      az[c] = fma(-f1.x, p1.y, az[c]);
+      az[c] = fma(f1.y, p1.x, az[c]);
     }
+  ix += ax[0] + ax[1];
+  iy += ay[0] + ay[1];
+  iz += az[0] + az[1];
 }
 
 // ---------------------------------------------------------------------------
@@ -748,14 +764,31 @@ __device__ __forceinline__ SegEnv make_env(const DevProgram& D, const RunArgs& A
                 bl0, bra, tile, n_tiles, own, partner};
 }
 
+// Segment descriptor access: RtSeg reads the device table at run time (the
+// interpreter); the JIT emits a struct with the same static members as
+// compile-time constants, so unused folds and address maps disappear.
+struct RtSeg {
+  const SegDesc* sd;
+  __device__ __forceinline__ int nthr() const { return sd->nthr; }
+  __device__ __forceinline__ int thr_off() const { return sd->thr_off; }
+  __device__ __forceinline__ uint32_t ld_k(int t) const { return sd->ld_k[t]; }
+  __device__ __forceinline__ uint32_t st_k(int t) const { return sd->st_k[t]; }
+  __device__ __forceinline__ uint32_t ps(int t) const { return sd->ps[t]; }
+  __device__ __forceinline__ uint32_t ldc(int t) const { return sd->ldc[t]; }
+  __device__ __forceinline__ uint32_t stc(int t) const { return sd->stc[t]; }
+  __device__ __forceinline__ int ip_count() const { return sd->ip_count; }
+  __device__ __forceinline__ int red_count() const { return sd->red_count; }
+  __device__ __forceinline__ int ip_begin() const { return sd->ip_begin; }
+};
+
 // segment start: address maps and the register load (shared-memory transpose)
-template <int R, int MODE>
-__device__ __forceinline__ void seg_begin(const SegEnv& E, const SegDesc* sd, SegCtx<R>& C, Regs<R>& a, Regs<R>& f) {
+template <int R, int MODE, class SD>
+__device__ __forceinline__ void seg_begin(const SegEnv& E, const SD& sd, SegCtx<R>& C, Regs<R>& a, Regs<R>& f) {
   constexpr int N = 1 << R;
-  const int nthr = sd->nthr;
+  const int nthr = sd.nthr();
   C.own = E.own;
   C.partner = E.partner;
-  const ThrEntry* te = E.D.thr_tab + sd->thr_off + (E.grp.gi & ((1 << nthr) - 1));
+  const ThrEntry* te = E.D.thr_tab + sd.thr_off() + (E.grp.gi & ((1 << nthr) - 1));
   const uint2 e01 = *reinterpret_cast<const uint2*>(te);
   C.J0 = E.tile_base | e01.x;
   C.lp0 = e01.y;
@@ -763,10 +796,10 @@ __device__ __forceinline__ void seg_begin(const SegEnv& E, const SegDesc* sd, Se
   if (E.tile_base != 0) {
 #pragma unroll
     for (int t = 0; t < R; ++t)
-      if (__popc(E.tile_base & sd->ld_k[t]) & 1) C.lp0 ^= sd->ps[t];
+      if (__popc(E.tile_base & sd.ld_k(t)) & 1) C.lp0 ^= sd.ps(t);
   }
 #pragma unroll
-  for (int t = 0; t < R; ++t) C.lc[t] = sd->ldc[t];
+  for (int t = 0; t < R; ++t) C.lc[t] = sd.ldc(t);
   if (E.active) {
 #pragma unroll
     for (int i = 0; i < N; ++i) {
@@ -800,24 +833,24 @@ __device__ __forceinline__ void seg_publish(const SegEnv& E, const SegCtx<R>& C,
 
 // segment end: register store (through the folded store map), barrier, and the
 // segment's gradient outputs
-template <int R, int MODE>
-__device__ __forceinline__ void seg_end(const SegEnv& E, const SegDesc* sd, const Regs<R>& a, const Regs<R>& f) {
+template <int R, int MODE, class SD>
+__device__ __forceinline__ void seg_end(const SegEnv& E, const SD& sd, const Regs<R>& a, const Regs<R>& f) {
   constexpr int N = 1 << R;
   const Group& grp = E.grp;
   const RunArgs& A = E.A;
-  if (MODE == MODE_SPLIT && sd->ip_count > 0) __syncthreads();  // partners done reading
+  if (MODE == MODE_SPLIT && sd.ip_count() > 0) __syncthreads();  // partners done reading
   asm volatile("" ::: "memory");  // keep the store map's loads and math after the op loop
   if (E.active) {
-    const ThrEntry* te = E.D.thr_tab + sd->thr_off + (grp.gi & ((1 << sd->nthr) - 1));
+    const ThrEntry* te = E.D.thr_tab + sd.thr_off() + (grp.gi & ((1 << sd.nthr()) - 1));
     uint32_t sp0 = te->sp0, sc[R];
     if (E.tile_base != 0) {
 #pragma unroll
       for (int t = 0; t < R; ++t)
-        if (__popc(E.tile_base & sd->st_k[t]) & 1) sp0 ^= sd->ps[t];
+        if (__popc(E.tile_base & sd.st_k(t)) & 1) sp0 ^= sd.ps(t);
     }
     asm volatile("" : "+r"(sp0));
 #pragma unroll
-    for (int t = 0; t < R; ++t) sc[t] = sd->stc[t];
+    for (int t = 0; t < R; ++t) sc[t] = sd.stc(t);
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       uint32_t ad = sp0;
@@ -830,13 +863,13 @@ __device__ __forceinline__ void seg_end(const SegEnv& E, const SegDesc* sd, cons
   }
   __syncthreads();
   if constexpr (MODE != MODE_FWD) {
-    const int nout = sd->ip_count;
+    const int nout = sd.ip_count();
     if (nout > 0) {
       // phase 1: one warp per (reduction slot, sample) sums the sample's
       // per-thread partials in a fixed order; phase 2: one thread per
       // (output, sample) applies the block gradient vector. Blocks narrower
       // than a warp (tiny n) reduce serially on thread 0.
-      const int nred = sd->red_count;
+      const int nred = sd.red_count();
       const bool narrow = blockDim.x < 32;
       const int lane = narrow ? 0 : (threadIdx.x & 31);
       const int warp = narrow ? (threadIdx.x == 0 ? 0 : 1 << 30) : (threadIdx.x >> 5);
@@ -856,7 +889,7 @@ __device__ __forceinline__ void seg_end(const SegEnv& E, const SegDesc* sd, cons
       __syncthreads();
       for (int task = threadIdx.x; task < nout * grp.S; task += blockDim.x) {
         const int oi = task / grp.S, s_ = task - oi * grp.S;
-        const IpOut io = E.D.ipouts[sd->ip_begin + oi];
+        const IpOut io = E.D.ipouts[sd.ip_begin() + oi];
         const double* r = E.s_fin + s_;
         double v;
         if (io.avec < 0) {
@@ -883,12 +916,13 @@ struct InterpSegs {
     const DevProgram& D = E.D;
     long long tdbg = E.A.dbg ? clock64() : 0;
     for (int sg = sb; sg < se; ++sg) {
-      const SegDesc* sd = D.segs + sg;
+      const SegDesc* sdp = D.segs + sg;
+      const RtSeg sd{sdp};
       SegCtx<R> C;
       Regs<R> a, f;
       seg_begin<R, MODE>(E, sd, C, a, f);
       dbg_add(E.A, DBG_SEG_LOAD, tdbg);
-      const int ob = sd->op_begin, oe = sd->op_end;
+      const int ob = sdp->op_begin, oe = sdp->op_end;
       Op nxt = ob < oe ? D.ops[ob] : Op{0u, 0u};
       for (int o = ob; o < oe; ++o) {
         const Op op = nxt;
@@ -942,18 +976,21 @@ __device__ __forceinline__ void build_tables(const DevProgram& D, const RunArgs&
 // j(i) = base ^ XOR_{b in i} hi[b]; visiting i in Gray-code order costs one
 // XOR per element.
 struct TileWalk {
-  uint32_t base;
-  uint32_t hi[kMaxR];
+  uint32_t base;           // global index of this thread's first element
+  uint32_t hi[kMaxR];      // global index bit of element-index bit b
+  uint32_t sbase;          // swizzled tile address of the first element
+  uint32_t shi[kMaxR];     // swizzled address bit of element-index bit b
   int count;  // elements per thread: 2^k / stride = 2^R <= 16
 };
 
-// pdep of tile-local index bits into the pass's global qubit positions
-// (visits only the set bits of l)
-__device__ __forceinline__ uint32_t dep_local(const PassDesc& pd, uint32_t l) {
+// pdep: the bits of l deposited into the set bits of m (ascending); the
+// pass's local qubits are local_mask's set bits in ascending order
+__device__ __forceinline__ uint32_t pdep32(uint32_t l, uint32_t m) {
   uint32_t j = 0;
-  while (l) {
-    j |= 1u << pd.local_q[__ffs(l) - 1];
-    l &= l - 1;
+  for (uint32_t bb = 1; m != 0; bb <<= 1) {
+    const uint32_t low = m & (0u - m);
+    if (l & bb) j |= low;
+    m ^= low;
   }
   return j;
 }
@@ -963,33 +1000,37 @@ __device__ __forceinline__ TileWalk tile_walk(const PassDesc* pd, uint32_t tile_
   TileWalk w;
   const int Nt = 1 << k;
   w.count = Nt / stride;
-  w.base = tile_base | (pd ? dep_local(*pd, (uint32_t)lane) : (uint32_t)lane);
+  const uint32_t lm = pd ? pd->local_mask : 0u;
+  w.base = tile_base | (pd ? pdep32((uint32_t)lane, lm) : (uint32_t)lane);
+  w.sbase = swz((uint32_t)lane);
   const int s0 = __ffs(stride) - 1;  // stride is a power of two: hi[b] is one local bit
 #pragma unroll
   for (int b = 0; b < kMaxR; ++b) {
     const int p = s0 + b;
-    w.hi[b] = p < k ? (pd ? (1u << pd->local_q[p]) : (1u << p)) : 0u;
+    w.hi[b] = p < k ? (pd ? pdep32(1u << p, lm) : (1u << p)) : 0u;
+    w.shi[b] = p < k ? swz(1u << p) : 0u;
   }
   return w;
 }
 
-// calls f(l, j) for every element of this thread: l tile-local, j global.
-// Kept as a rolled loop (the element index bits select hi[] entries with
-// constant indices) so call sites stay small in the instruction cache.
+// calls f(sw, j) for every element of this thread: sw its swizzled tile
+// address, j its global index (both GF(2)-linear in the element index, so
+// one XOR per set bit). Kept as a rolled loop so call sites stay small in
+// the instruction cache.
 template <class F>
 __device__ __forceinline__ void for_tile(const TileWalk& w, int lane, int stride, F&& f) {
 #pragma unroll 1
   for (int i = 0; i < w.count; ++i) {
-    uint32_t j = w.base;
+    uint32_t j = w.base, sw = w.sbase;
 #pragma unroll
     for (int b = 0; b < kMaxR; ++b)
-      if ((i >> b) & 1) j ^= w.hi[b];
-    f((uint32_t)lane + (uint32_t)i * (uint32_t)stride, j);
+      if ((i >> b) & 1) {
+        j ^= w.hi[b];
+        sw ^= w.shi[b];
+      }
+    f(sw, j);
   }
 }
-
-// global index of tile-local element l (pdep of l into the pass's local qubits)
-
 
 // Z-string signs and weights for global index j over terms [lo, hi)
 __device__ __forceinline__ double zweight(const DevProgram& D, uint32_t j, int lo, int hi) {

@@ -36,13 +36,13 @@ __device__ __forceinline__ void stage_terms(const DevProgram& D, TermSm* s_terms
 // (_kernels.py:209-217). Each thread owns `count` tile elements; a term's
 // sign over them is parity(base & s) ^ parity(i & h), h bit b =
 // parity(hi[b] & s), so no per-element index arithmetic is needed.
-template <bool DUAL>
+// E: elements per thread (compile time; equals the tile walk's count)
+template <bool DUAL, int E>
 __device__ __forceinline__ void observe(const DevProgram& D, const RunArgs& A, const PassDesc* pd, double2* s_psi,
                                         double2* s_phi, const double* s_u_row, const TermSm* s_terms,
                                         const Group& grp, double* s_red, double* s_fin, uint32_t tile_base, int k,
                                         int64_t bl0, bool do_expect, int seed_mode, int bra, int tile,
                                         int n_tiles) {
-  constexpr int E = 1 << kMaxR;
   const int lane = grp.lane_in_sample();
   const TileWalk tw = tile_walk(pd, tile_base, k, lane, grp.TT);
   const int count = tw.count;
@@ -204,6 +204,7 @@ __host__ __device__ constexpr int pass_max_threads(int R) { return R >= 5 ? 256 
 
 template <int R, int KM, class SEGS>
 __device__ __forceinline__ void smem_body(const DevProgram& D, const RunArgs& A) {
+  constexpr int OBS_E = KM == KM_SPLIT ? (1 << (R - 1)) : (1 << R);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr bool ADJ = KM != KM_FWD;
   constexpr int BM = KM == KM_SPLIT ? MODE_SPLIT : MODE_DUAL;
@@ -237,16 +238,16 @@ __device__ __forceinline__ void smem_body(const DevProgram& D, const RunArgs& A)
   SEGS::template run<R, MODE_FWD>(make_env<MODE_FWD>(D, A, s_psi, s_psi, s_av_all, nav * 4, 0, s_red, s_fin,
                             grp, grp.role == 0, 0u, bl0, 0, 0, 1), T, pd->seg_begin, pd->seg_end);
   if constexpr (!ADJ) {
-    observe<false>(D, A, nullptr, s_psi, s_psi, nullptr, s_terms, grp, s_red, s_fin, 0u, n, bl0, true, 0, 0, 0, 1);
+    observe<false, OBS_E>(D, A, nullptr, s_psi, s_psi, nullptr, s_terms, grp, s_red, s_fin, 0u, n, bl0, true, 0, 0, 0, 1);
   } else {
     if (!A.jacobian) {
-      observe<true>(D, A, nullptr, s_psi, s_phi, s_up + grp.sl * D.M, s_terms, grp, s_red, s_fin, 0u, n, bl0,
+      observe<true, OBS_E>(D, A, nullptr, s_psi, s_phi, s_up + grp.sl * D.M, s_terms, grp, s_red, s_fin, 0u, n, bl0,
                     A.expect != nullptr, 1, 0, 0, 1);
       __syncthreads();
       SEGS::template run<R, BM>(make_env<BM>(D, A, s_psi, s_phi, s_av_all, nav * 4, 0, s_red, s_fin,
                           grp, true, 0u, bl0, 0, 0, 1), T, pd->bseg_begin, pd->bseg_end);
     } else {
-      observe<true>(D, A, nullptr, s_psi, s_phi, nullptr, s_terms, grp, s_red, s_fin, 0u, n, bl0,
+      observe<true, OBS_E>(D, A, nullptr, s_psi, s_phi, nullptr, s_terms, grp, s_red, s_fin, 0u, n, bl0,
                     A.expect != nullptr, 0, 0, 0, 1);
       double2* fin = A.psi_fin + (size_t)bl * N;
       if (D.M > 1 && valid)
@@ -257,7 +258,7 @@ __device__ __forceinline__ void smem_body(const DevProgram& D, const RunArgs& A)
           if (valid)
             for (int l = lane; l < N; l += grp.TT) s_psi[swz((uint32_t)l)] = fin[l];
         }
-        observe<true>(D, A, nullptr, s_psi, s_phi, nullptr, s_terms, grp, s_red, s_fin, 0u, n, bl0, false, 2, m,
+        observe<true, OBS_E>(D, A, nullptr, s_psi, s_phi, nullptr, s_terms, grp, s_red, s_fin, 0u, n, bl0, false, 2, m,
                       0, 1);
         __syncthreads();
         SEGS::template run<R, BM>(make_env<BM>(D, A, s_psi, s_phi, s_av_all, nav * 4, 0,
@@ -276,6 +277,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // One pass over HBM-resident states: CTA (tile, row) stages 2^k amplitudes.
 template <int R, int KM, class SEGS>
 __device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A) {
+  constexpr int OBS_E = KM == KM_SPLIT ? (1 << (R - 1)) : (1 << R);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr bool ADJ = KM != KM_FWD;
   const PassDesc* pd = D.passes + A.pass;
@@ -320,9 +322,9 @@ __device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A)
     const double2* srcf = A.phi + (size_t)bl * N;
     const bool lphi = ADJ && (flags & F_LOAD_PHI);
     const TileWalk tw = tile_walk(pd, tile_base, k, threadIdx.x, blockDim.x);
-    for_tile(tw, threadIdx.x, blockDim.x, [&](uint32_t l, uint32_t j) {
-      cp_async16(s_psi + swz(l), src + j);
-      if (lphi) cp_async16(s_phi + swz(l), srcf + j);
+    for_tile(tw, threadIdx.x, blockDim.x, [&](uint32_t sw, uint32_t j) {
+      cp_async16(s_psi + sw, src + j);
+      if (lphi) cp_async16(s_phi + sw, srcf + j);
     });
   }
   if (A.tables != nullptr) {
@@ -352,10 +354,10 @@ __device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A)
     asm volatile("" : "+r"(tb));
     const TileWalk tw = tile_walk(pd, tb, k, threadIdx.x, blockDim.x);
     double2* dst = A.psi_fin + (size_t)bl * N;
-    for_tile(tw, threadIdx.x, blockDim.x, [&](uint32_t l, uint32_t j) { dst[j] = s_psi[swz(l)]; });
+    for_tile(tw, threadIdx.x, blockDim.x, [&](uint32_t sw, uint32_t j) { dst[j] = s_psi[sw]; });
   }
   if (flags & (F_OBSERVE | F_SEED)) {
-    observe<ADJ>(D, A, pd, s_psi, s_phi, s_up, s_terms, grp, s_red, s_fin, tile_base, k, bl, (flags & F_OBSERVE) != 0,
+    observe<ADJ, OBS_E>(D, A, pd, s_psi, s_phi, s_up, s_terms, grp, s_red, s_fin, tile_base, k, bl, (flags & F_OBSERVE) != 0,
                  (flags & F_SEED) ? (A.bra < 0 ? 1 : 2) : 0, A.bra, tile, n_tiles);
     __syncthreads();
   }
@@ -375,9 +377,9 @@ __device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A)
     const bool spsi = (flags & F_STORE_PSI) != 0;
     double2* dst = A.psi + (size_t)bl * N;
     double2* dstf = A.phi + (size_t)bl * N;
-    for_tile(tw, threadIdx.x, blockDim.x, [&](uint32_t l, uint32_t j) {
-      if (spsi) dst[j] = s_psi[swz(l)];
-      if (sphi) dstf[j] = s_phi[swz(l)];
+    for_tile(tw, threadIdx.x, blockDim.x, [&](uint32_t sw, uint32_t j) {
+      if (spsi) dst[j] = s_psi[sw];
+      if (sphi) dstf[j] = s_phi[sw];
     });
   }
   dbg_add(A, DBG_STORE, tdbg);
