@@ -278,6 +278,7 @@ struct VqcPlan {
   size_t state_budget = 0;
   bool use_jit = false;
   JitKernels jit;
+  std::vector<std::pair<const void*, int64_t>> resident;  // kernel -> resident CTAs (L2 prefetch distance)
   // host-call cache
   std::mutex mu;
   cudaStream_t stream = nullptr;
@@ -394,6 +395,18 @@ int launch(const char* name, Kern k, dim3 grid, dim3 block, size_t smem, cudaStr
   return VQC_OK;
 }
 
+// CTAs of kernel k resident at once on the device (the L2 prefetch distance)
+int64_t resident_ctas(const VqcPlan* p, Kern k, int block, size_t smem) {
+  int occ = 1;
+  if (k.cu) {
+    occ = jit_occupancy(k.cu, block, smem);
+  } else {
+    cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k.fn, block, smem) != cudaSuccess || occ < 1) occ = 1;
+  }
+  return (int64_t)occ * p->sms;
+}
+
 Kern smem_k(const VqcPlan* p, bool adj) {
   Kern k;
   if (p->use_jit) k.cu = adj ? p->jit.smem_adj : p->jit.smem_fwd;
@@ -501,36 +514,54 @@ int run_core(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, const
     }
     const dim3 grid((unsigned)L.n_tiles, (unsigned)nb), block((unsigned)TPS), block2((unsigned)(2 * TPS));
     int rc;
+    // pass launches: L2 prefetch one wave of CTAs ahead (VQC_PF=0 disables)
+    const bool pf_on = env_int("VQC_PF", 0) != 0;  // measured slower on cfg4/5 (r01): off by default
+    auto launch_pass = [&](const char* name, Kern k, dim3 blk, size_t smem) {
+      RunArgs A2 = A;
+      A2.pf_dist = 0;
+      if (pf_on) {
+        const void* key = k.cu ? (const void*)k.cu : (const void*)k.fn;
+        int64_t res = -1;
+        for (auto& kv : p->resident)
+          if (kv.first == key) res = kv.second;
+        if (res < 0) {
+          res = resident_ctas(p, k, (int)blk.x, smem);
+          p->resident.push_back({key, res});
+        }
+        A2.pf_dist = res;
+      }
+      return launch(name, k, grid, blk, smem, st, D, A2);
+    };
     for (int pi = 0; pi < NP - 1; ++pi) {
       A.pass = pi;
       A.flags = (pi == 0 ? F_INIT : F_LOAD_PSI) | F_FWD | F_STORE_PSI;
-      if ((rc = launch("pass_forward", pass_k(p, false, A.pass), grid, block, sm1, st, D, A))) return rc;
+      if ((rc = launch_pass("pass_forward", pass_k(p, false, A.pass), block, sm1))) return rc;
     }
     const uint32_t first = NP == 1 ? F_INIT : F_LOAD_PSI;
     A.pass = NP - 1;
     if (mode == VQC_MODE_FORWARD) {
       A.flags = first | F_FWD | F_OBSERVE;
-      if ((rc = launch("pass_forward", pass_k(p, false, A.pass), grid, block, sm1, st, D, A))) return rc;
+      if ((rc = launch_pass("pass_forward", pass_k(p, false, A.pass), block, sm1))) return rc;
     } else if (mode == VQC_MODE_VJP) {
       A.flags = first | F_FWD | F_OBSERVE | F_SEED | F_BWD | (NP > 1 ? (F_STORE_PSI | F_STORE_PHI) : 0);
-      if ((rc = launch("pass_adjoint", pass_k(p, true, A.pass), grid, block2, sm2, st, D, A))) return rc;
+      if ((rc = launch_pass("pass_adjoint", pass_k(p, true, A.pass), block2, sm2))) return rc;
       for (int pi = NP - 2; pi >= 0; --pi) {
         A.pass = pi;
         A.flags = F_LOAD_PSI | F_LOAD_PHI | F_BWD | (pi > 0 ? (F_STORE_PSI | F_STORE_PHI) : 0);
-        if ((rc = launch("pass_adjoint", pass_k(p, true, A.pass), grid, block2, sm2, st, D, A))) return rc;
+        if ((rc = launch_pass("pass_adjoint", pass_k(p, true, A.pass), block2, sm2))) return rc;
       }
     } else {
       A.flags = first | F_FWD | F_OBSERVE | F_STORE_FIN;
-      if ((rc = launch("pass_forward", pass_k(p, false, A.pass), grid, block, sm1, st, D, A))) return rc;
+      if ((rc = launch_pass("pass_forward", pass_k(p, false, A.pass), block, sm1))) return rc;
       for (int m = 0; m < p->M; ++m) {
         A.bra = m;
         A.pass = NP - 1;
         A.flags = F_LOAD_FIN | F_SEED | F_BWD | (NP > 1 ? (F_STORE_PSI | F_STORE_PHI) : 0);
-        if ((rc = launch("pass_adjoint", pass_k(p, true, A.pass), grid, block2, sm2, st, D, A))) return rc;
+        if ((rc = launch_pass("pass_adjoint", pass_k(p, true, A.pass), block2, sm2))) return rc;
         for (int pi = NP - 2; pi >= 0; --pi) {
           A.pass = pi;
           A.flags = F_LOAD_PSI | F_LOAD_PHI | F_BWD | (pi > 0 ? (F_STORE_PSI | F_STORE_PHI) : 0);
-          if ((rc = launch("pass_adjoint", pass_k(p, true, A.pass), grid, block2, sm2, st, D, A))) return rc;
+          if ((rc = launch_pass("pass_adjoint", pass_k(p, true, A.pass), block2, sm2))) return rc;
         }
       }
     }

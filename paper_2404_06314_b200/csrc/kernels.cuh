@@ -76,6 +76,7 @@ struct RunArgs {
   unsigned long long* dbg; // VQC_DEBUG_TIMING: per-phase clock64 totals (thread 0 of each CTA)
   const double* tables;    // HBM mode: per-sample tables from k_tables (rows relative to b0)
   int64_t table_stride;    // doubles per sample
+  int64_t pf_dist;         // HBM passes: prefetch into L2 the tile of the CTA this many launch slots ahead (0 = off)
 };
 
 // phase timing (debug only): dbg[slot] += clock64 delta, slots fixed below
@@ -1014,22 +1015,24 @@ __device__ __forceinline__ TileWalk tile_walk(const PassDesc* pd, uint32_t tile_
 }
 
 // calls f(sw, j) for every element of this thread: sw its swizzled tile
-// address, j its global index (both GF(2)-linear in the element index, so
-// one XOR per set bit). Kept as a rolled loop so call sites stay small in
-// the instruction cache.
-template <class F>
-__device__ __forceinline__ void for_tile(const TileWalk& w, int lane, int stride, F&& f) {
-#pragma unroll 1
-  for (int i = 0; i < w.count; ++i) {
-    uint32_t j = w.base, sw = w.sbase;
-#pragma unroll
-    for (int b = 0; b < kMaxR; ++b)
-      if ((i >> b) & 1) {
-        j ^= w.hi[b];
-        sw ^= w.shi[b];
-      }
+// address, j its global index (both GF(2)-linear in the element index).
+// E = elements per thread (compile time): unrolled in Gray-code order, so each
+// element costs one XOR per index (the walk used to be a rolled loop with a
+// per-element bit scan, ~20 integer instructions per element).
+template <int G, int E, class F>
+__device__ __forceinline__ void for_tile_step(const TileWalk& w, uint32_t j, uint32_t sw, F&& f) {
+  if constexpr (G < E) {
+    constexpr int b = ctz_const(G);  // Gray code: element G differs from element G - 1 in bit b
+    j ^= w.hi[b];
+    sw ^= w.shi[b];
     f(sw, j);
+    for_tile_step<G + 1, E>(w, j, sw, f);
   }
+}
+template <int E, class F>
+__device__ __forceinline__ void for_tile(const TileWalk& w, F&& f) {
+  f(w.sbase, w.base);
+  for_tile_step<1, E>(w, w.base, w.sbase, f);
 }
 
 // Z-string signs and weights for global index j over terms [lo, hi)

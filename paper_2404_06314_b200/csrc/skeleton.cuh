@@ -272,6 +272,9 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src)
   const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src) : "memory");
 }
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // One pass over HBM-resident states: CTA (tile, row) stages 2^k amplitudes.
@@ -288,13 +291,8 @@ __device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A)
   const int64_t bl = blockIdx.y;
   const int64_t b = A.b0 + bl;
   const size_t N = (size_t)1 << D.n;
-  uint32_t tile_base = 0;
-  {
-    const uint32_t lm = pd->local_mask;
-    int c = 0;
-    for (int q = 0; q < D.n; ++q)
-      if (!((lm >> q) & 1u)) tile_base |= (((uint32_t)tile >> c++) & 1u) << q;
-  }
+  const uint32_t nonlocal = ~pd->local_mask & ((1u << D.n) - 1u);
+  const uint32_t tile_base = pdep32((uint32_t)tile, nonlocal);
   const SmemLayout L(1, Nt, ADJ, D.max_rot_pass, D.max_blk_pass, D.max_av_pass, A.red_slots, (int)blockDim.x,
                      D.M, D.T);
   double2* s_psi = reinterpret_cast<double2*>(smem_raw + L.psi);
@@ -322,10 +320,24 @@ __device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A)
     const double2* srcf = A.phi + (size_t)bl * N;
     const bool lphi = ADJ && (flags & F_LOAD_PHI);
     const TileWalk tw = tile_walk(pd, tile_base, k, threadIdx.x, blockDim.x);
-    for_tile(tw, threadIdx.x, blockDim.x, [&](uint32_t sw, uint32_t j) {
+    for_tile<OBS_E>(tw, [&](uint32_t sw, uint32_t j) {
       cp_async16(s_psi + sw, src + j);
       if (lphi) cp_async16(s_phi + sw, srcf + j);
     });
+    // warm L2 with the tile of the CTA that starts about one wave later (its
+    // loads then come from L2 while this CTA computes)
+    const int64_t nxt = ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) + A.pf_dist;
+    if (A.pf_dist > 0 && nxt < (int64_t)gridDim.x * gridDim.y) {
+      const uint32_t tb2 = pdep32((uint32_t)(nxt % gridDim.x), nonlocal);
+      const int64_t row2 = nxt / gridDim.x;
+      const double2* src2 = ((flags & F_LOAD_FIN) ? A.psi_fin : A.psi) + (size_t)row2 * N;
+      const double2* srcf2 = A.phi + (size_t)row2 * N;
+      const uint32_t dj = tile_base ^ tb2;
+      for_tile<OBS_E>(tw, [&](uint32_t sw, uint32_t j) {
+        prefetch_l2(src2 + (j ^ dj));
+        if (lphi) prefetch_l2(srcf2 + (j ^ dj));
+      });
+    }
   }
   if (A.tables != nullptr) {
     // per-sample tables precomputed by k_tables: copy this pass's slices
@@ -354,7 +366,7 @@ __device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A)
     asm volatile("" : "+r"(tb));
     const TileWalk tw = tile_walk(pd, tb, k, threadIdx.x, blockDim.x);
     double2* dst = A.psi_fin + (size_t)bl * N;
-    for_tile(tw, threadIdx.x, blockDim.x, [&](uint32_t sw, uint32_t j) { dst[j] = s_psi[sw]; });
+    for_tile<OBS_E>(tw, [&](uint32_t sw, uint32_t j) { dst[j] = s_psi[sw]; });
   }
   if (flags & (F_OBSERVE | F_SEED)) {
     observe<ADJ, OBS_E>(D, A, pd, s_psi, s_phi, s_up, s_terms, grp, s_red, s_fin, tile_base, k, bl, (flags & F_OBSERVE) != 0,
@@ -377,7 +389,7 @@ __device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A)
     const bool spsi = (flags & F_STORE_PSI) != 0;
     double2* dst = A.psi + (size_t)bl * N;
     double2* dstf = A.phi + (size_t)bl * N;
-    for_tile(tw, threadIdx.x, blockDim.x, [&](uint32_t sw, uint32_t j) {
+    for_tile<OBS_E>(tw, [&](uint32_t sw, uint32_t j) {
       if (spsi) dst[j] = s_psi[sw];
       if (sphi) dstf[j] = s_phi[sw];
     });
