@@ -626,8 +626,12 @@ int schedule_circuit(const VqcCircuit* c, const int64_t* wrt_col, HostProgram* p
   opt.tile_qubits = env_int("VQC_TILE_QUBITS", 11);
   opt.segment_cost = env_int("VQC_SEGMENT_COST", 4);
   // four register slots (16 amplitudes per thread); the scheduler and its
-  // CPU checker also handle 3 and 5 (tests/test_scheduler_sim.py)
+  // CPU checker also handle 3 and 5 (tests/test_scheduler_sim.py). Other
+  // values (VQC_REG_SLOTS) only for JIT-compiled HBM plans: the prebuilt
+  // interpreter kernels exist for R = 4 passes only.
   opt.reg_slots = 4;
+  if (c->n_qubits > opt.smem_max_qubits && env_int("VQC_JIT", -1) != 0)
+    opt.reg_slots = std::max(3, std::min(4, env_int("VQC_REG_SLOTS", 4)));
   const int absorbed = prog->absorbed;
   std::string err = build_program(gates, c->n_qubits, c->total_params, wcol, opt, prog);
   prog->absorbed = absorbed;
