@@ -835,10 +835,11 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
   D.enc_size = p->enc_size;
   p->state_budget = (size_t)env_int("VQC_STATE_BUDGET_MB", 16384) << 20;
   // JIT policy (VQC_JIT): unset = specialise HBM-pass plans (per-pass units
-  // compile in parallel in seconds), 1 = every plan, 0 = interpreter only. The
-  // on-chip kernel is one unit holding the whole circuit and compiles slowly.
+  // compile in parallel) and on-chip plans of n >= 8 qubits (shape-shared
+  // segment code, one unit); 1 = every plan, 0 = interpreter only. Small
+  // circuits are launch-bound and stay on the prebuilt interpreter.
   const int jit_mode = env_int("VQC_JIT", -1);
-  const bool want_jit = jit_mode > 0 || (jit_mode < 0 && P.hbm);
+  const bool want_jit = jit_mode > 0 || (jit_mode < 0 && (P.hbm || P.n >= 8));
   if (want_jit && P.n_fwd_ops + P.n_bwd_ops > 0) {
     err = jit_build(P, use_split(P.n, P.R), &p->jit);
     if (!err.empty()) {

@@ -37,3 +37,14 @@ def test_random_hbm_circuit_compiles_for_sm100a():
     assert secs is not None and secs > 0
     for op in ("jop_cnot", "jop_u2", "jop_ip"):
         assert op in src, op
+
+
+def test_on_chip_plan_shares_code_per_segment_shape():
+    """cfg3 (on-chip): 48 segments of two shapes -> two switch cases, and the
+    unit compiles in seconds (it took minutes as one copy per segment)."""
+    spec = configs.CONFIGS[3]
+    circ, obs, wrt = configs.build(spec, configs.native_api())
+    src, secs = _src(circ, wrt, compile=True)
+    assert src.count("case 0:") == 2 and "case 1:" not in src
+    assert "__constant__ int jf0_opnd" in src and "vqc_jit_sa" in src
+    assert secs < 120
