@@ -106,6 +106,13 @@ using KFn = void (*)(DevProgram, RunArgs);
 // split the adjoint over (psi, phi) thread pairs
 bool use_split(int n, int R) { return (n - R) >= 5; }
 
+// JIT-compiled HBM plans: the adjoint sweep runs 3 register slots with both
+// states per thread (KM_DUAL: no partner reads, one barrier less per
+// segment), the forward sweep its own 4-slot schedule (measured on cfg4:
+// adjoint 630 -> 559 ms, forward 191 ms kept; r01 knob sweep in DESIGN.md)
+constexpr int kHbmAdjointRegs = 3;
+constexpr int kHbmForwardRegs = 4;
+
 // Plans use R = min(4, n) register slots (schedule_circuit), so only these
 // interpreter instantiations exist (each is a large unrolled kernel).
 KFn smem_kernel(int R, bool dual, bool split) {
@@ -245,6 +252,55 @@ static std::vector<ThrEntry> build_thr_table(std::vector<SegDesc>& segs) {
   return tab;
 }
 
+// device copies of one scheduled program's tables
+struct ProgTabs {
+  Op* ops = nullptr;
+  SegDesc* segs = nullptr;
+  IpOut* ipouts = nullptr;
+  BlockDesc* blocks = nullptr;
+  MemberDesc* members = nullptr;
+  DiagRun* diag = nullptr;
+  int16_t* setids = nullptr;
+  ThrEntry* thr_tab = nullptr;
+  PassDesc* passes = nullptr;
+  RotDesc* rots = nullptr;
+  cudaError_t upload_all(std::vector<SegDesc>& segs_h, const HostProgram& P) {
+    const std::vector<ThrEntry> thr = build_thr_table(segs_h);
+    cudaError_t e = upload(thr, &thr_tab);
+    if (e == cudaSuccess) e = upload(P.ops, &ops);
+    if (e == cudaSuccess) e = upload(P.segs, &segs);
+    if (e == cudaSuccess) e = upload(P.ipouts, &ipouts);
+    if (e == cudaSuccess) e = upload(P.blocks, &blocks);
+    if (e == cudaSuccess) e = upload(P.members, &members);
+    if (e == cudaSuccess) e = upload(P.diag, &diag);
+    if (e == cudaSuccess) e = upload(P.setids, &setids);
+    if (e == cudaSuccess) e = upload(P.passes, &passes);
+    if (e == cudaSuccess) e = upload(P.rots, &rots);
+    return e;
+  }
+  void free_all() {
+    cudaFree(ops);
+    cudaFree(segs);
+    cudaFree(ipouts);
+    cudaFree(blocks);
+    cudaFree(members);
+    cudaFree(diag);
+    cudaFree(setids);
+    cudaFree(thr_tab);
+    cudaFree(passes);
+    cudaFree(rots);
+    *this = ProgTabs();
+  }
+};
+
+// a second scheduled program (forward sweep) with its tables and kernels
+struct ProgDev {
+  HostProgram prog;
+  ProgTabs tabs;
+  DevProgram D{};
+  JitKernels jit;
+};
+
 struct VqcPlan {
   int device = 0;
   int sms = 148;
@@ -257,16 +313,7 @@ struct VqcPlan {
   std::vector<double> tcoeff;
   bool has_xy = false;
   // device tables
-  Op* d_ops = nullptr;
-  SegDesc* d_segs = nullptr;
-  IpOut* d_ipouts = nullptr;
-  BlockDesc* d_blocks = nullptr;
-  MemberDesc* d_members = nullptr;
-  DiagRun* d_diag = nullptr;
-  int16_t* d_setids = nullptr;
-  ThrEntry* d_thr_tab = nullptr;
-  PassDesc* d_passes = nullptr;
-  RotDesc* d_rots = nullptr;
+  ProgTabs tabs;  // device tables of `prog`
   int32_t* d_term_offs = nullptr;
   uint32_t* d_smask = nullptr;
   uint32_t* d_xmask = nullptr;
@@ -278,7 +325,9 @@ struct VqcPlan {
   size_t state_budget = 0;
   bool use_jit = false;
   JitKernels jit;
-  std::vector<std::pair<const void*, int64_t>> resident;  // kernel -> resident CTAs (L2 prefetch distance)
+  // Separate forward schedule for HBM plans (its own tile size / register
+  // slots, VQC_FWD_TILE / VQC_FWD_REG); null = `prog` runs forward and adjoint
+  ProgDev* fwd = nullptr;
   // host-call cache
   std::mutex mu;
   cudaStream_t stream = nullptr;
@@ -289,8 +338,9 @@ struct VqcPlan {
 namespace {
 
 struct Layout {
-  size_t ip = 0, rows = 0, psi = 0, phi = 0, fin = 0, ipart = 0, epart = 0, tables = 0, total = 0;
-  int64_t table_stride = 0;  // doubles per sample (0: tables rebuilt per CTA)
+  size_t ip = 0, rows = 0, psi = 0, phi = 0, fin = 0, ipart = 0, epart = 0, tables = 0, ftables = 0, total = 0;
+  int64_t table_stride = 0;   // doubles per sample (0: tables rebuilt per CTA)
+  int64_t ftable_stride = 0;  // same for the separate forward program
   int64_t chunk = 0;
   int n_tiles = 1;
   int K = 1;
@@ -326,12 +376,15 @@ Layout make_layout(const VqcPlan* p, int64_t B, int mode) {
     L.phi = take(adj ? (size_t)chunk * N * 16 : 0);
     L.fin = take(mode == VQC_MODE_JACOBIAN ? (size_t)chunk * N * 16 : 0);
     L.ipart = take(adj ? (size_t)chunk * L.K * P.NG * L.n_tiles * 8 : 0);
-    L.epart = take((size_t)chunk * M * L.n_tiles * 8);
-    const int64_t stride = 2 * (int64_t)P.n_rot + 8 * (int64_t)P.n_blk + 4 * (int64_t)P.n_av;
-    if (stride > 0 && stride * 8 <= 160 * 1024) {
-      L.table_stride = stride;
-      L.tables = take((size_t)chunk * stride * 8);
-    }
+    const int ftiles = p->fwd ? 1 << (p->fwd->prog.n - p->fwd->prog.k) : L.n_tiles;
+    L.epart = take((size_t)chunk * M * std::max(L.n_tiles, ftiles) * 8);
+    auto stride_of = [](const HostProgram& Q) {
+      const int64_t st = 2 * (int64_t)Q.n_rot + 8 * (int64_t)Q.n_blk + 4 * (int64_t)Q.n_av;
+      return (st > 0 && st * 8 <= 160 * 1024) ? st : (int64_t)0;
+    };
+    if ((L.table_stride = stride_of(P)) > 0) L.tables = take((size_t)chunk * L.table_stride * 8);
+    if (p->fwd && (L.ftable_stride = stride_of(p->fwd->prog)) > 0)
+      L.ftables = take((size_t)chunk * L.ftable_stride * 8);
   }
   L.total = off + 256;
   return L;
@@ -359,11 +412,10 @@ int smem_samples(const VqcPlan* p, int64_t B, bool dual, size_t* smem_bytes, int
   return S;
 }
 
-size_t pass_smem(const VqcPlan* p, bool dual) {
-  const HostProgram& P = p->prog;
+size_t pass_smem(const VqcPlan* p, const HostProgram& P, bool dual) {
   const int TPS = 1 << (P.k - P.R);
   return SmemLayout(1, 1 << P.k, dual, P.max_rot_per_pass, P.max_blk_per_pass, P.max_av_per_pass,
-                    red_slots(p), dual ? 2 * TPS : TPS, p->M, (int)p->smask.size()).total;
+                    red_slots(p), (dual && !P.adj_dual) ? 2 * TPS : TPS, p->M, (int)p->smask.size()).total;
 }
 
 int launch(const char* name, Kern k, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
@@ -393,18 +445,6 @@ int launch(const char* name, Kern k, dim3 grid, dim3 block, size_t smem, cudaStr
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   return VQC_OK;
-}
-
-// CTAs of kernel k resident at once on the device (the L2 prefetch distance)
-int64_t resident_ctas(const VqcPlan* p, Kern k, int block, size_t smem) {
-  int occ = 1;
-  if (k.cu) {
-    occ = jit_occupancy(k.cu, block, smem);
-  } else {
-    cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k.fn, block, smem) != cudaSuccess || occ < 1) occ = 1;
-  }
-  return (int64_t)occ * p->sms;
 }
 
 Kern smem_k(const VqcPlan* p, bool adj) {
@@ -483,15 +523,22 @@ int run_core(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, const
     return launch(adj ? "smem_fwd_adjoint" : "smem_forward", smem_k(p, adj), grid,
                   block, smem, st, D, A);
   }
-  // HBM passes, chunked over rows
+  // HBM passes, chunked over rows. The forward sweep runs the forward program
+  // (p->fwd when the plan has a separate forward schedule, else `prog`); the
+  // adjoint sweep always runs `prog`. With one program the last pass fuses
+  // forward + observe + seed + the first adjoint pass.
   double2* psi = reinterpret_cast<double2*>(ws + L.psi);
   double2* phi = reinterpret_cast<double2*>(ws + L.phi);
   double2* fin = reinterpret_cast<double2*>(ws + L.fin);
   double* ipart = reinterpret_cast<double*>(ws + L.ipart);
   double* epart = reinterpret_cast<double*>(ws + L.epart);
-  const int TPS = 1 << (P.k - P.R);
-  const int NP = (int)P.passes.size();
-  const size_t sm1 = pass_smem(p, false), sm2 = pass_smem(p, true);
+  const bool sep = p->fwd != nullptr;
+  const HostProgram& PF = sep ? p->fwd->prog : P;
+  const DevProgram& DF = sep ? p->fwd->D : D;
+  const int TPS = 1 << (P.k - P.R), TPSF = 1 << (PF.k - PF.R);
+  const int NP = (int)P.passes.size(), NPF = (int)PF.passes.size();
+  const int tiles_f = 1 << (PF.n - PF.k);
+  const size_t smF = pass_smem(p, PF, false), smB = pass_smem(p, P, true);
   for (int64_t b0 = 0; b0 < B; b0 += L.chunk) {
     const int64_t nb = std::min<int64_t>(L.chunk, B - b0);
     A.b0 = b0;
@@ -503,71 +550,76 @@ int run_core(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, const
     A.expect = epart;
     A.ip = ipart;
     A.bra = -1;
+    A.pf_dist = 0;
+    int rc;
+    // per-sample angle / block tables of each program that runs
+    RunArgs AF = A;  // forward sweep arguments
     A.tables = nullptr;
     A.table_stride = 0;
-    if (L.table_stride > 0) {
+    AF.tables = nullptr;
+    AF.table_stride = 0;
+    if (L.table_stride > 0 && (!sep || mode != VQC_MODE_FORWARD)) {
       A.tables = reinterpret_cast<double*>(ws + L.tables);
       A.table_stride = L.table_stride;
-      int rc0;
-      if ((rc0 = launch("tables", Kern{k_tables, nullptr}, dim3((unsigned)nb), dim3(256), (size_t)L.table_stride * 8, st, D, A)))
-        return rc0;
+      if ((rc = launch("tables", Kern{k_tables, nullptr}, dim3((unsigned)nb), dim3(256),
+                       (size_t)L.table_stride * 8, st, D, A)))
+        return rc;
     }
-    const dim3 grid((unsigned)L.n_tiles, (unsigned)nb), block((unsigned)TPS), block2((unsigned)(2 * TPS));
-    int rc;
-    // pass launches: L2 prefetch one wave of CTAs ahead (VQC_PF=0 disables)
-    const bool pf_on = env_int("VQC_PF", 0) != 0;  // measured slower on cfg4/5 (r01): off by default
-    auto launch_pass = [&](const char* name, Kern k, dim3 blk, size_t smem) {
-      RunArgs A2 = A;
-      A2.pf_dist = 0;
-      if (pf_on) {
-        const void* key = k.cu ? (const void*)k.cu : (const void*)k.fn;
-        int64_t res = -1;
-        for (auto& kv : p->resident)
-          if (kv.first == key) res = kv.second;
-        if (res < 0) {
-          res = resident_ctas(p, k, (int)blk.x, smem);
-          p->resident.push_back({key, res});
-        }
-        A2.pf_dist = res;
-      }
-      return launch(name, k, grid, blk, smem, st, D, A2);
+    if (!sep) {
+      AF.tables = A.tables;
+      AF.table_stride = A.table_stride;
+    } else if (L.ftable_stride > 0) {
+      AF.tables = reinterpret_cast<double*>(ws + L.ftables);
+      AF.table_stride = L.ftable_stride;
+      if ((rc = launch("tables", Kern{k_tables, nullptr}, dim3((unsigned)nb), dim3(256),
+                       (size_t)L.ftable_stride * 8, st, DF, AF)))
+        return rc;
+    }
+    const dim3 grid((unsigned)L.n_tiles, (unsigned)nb), grid_f((unsigned)tiles_f, (unsigned)nb);
+    const dim3 block_f((unsigned)TPSF), block2((unsigned)(P.adj_dual ? TPS : 2 * TPS));
+    auto fwd_pass = [&](int pi, uint32_t flags) {
+      AF.pass = pi;
+      AF.flags = flags;
+      Kern k;
+      if (sep) k.cu = p->fwd->jit.pass_fwd[pi];
+      else k = pass_k(p, false, pi);
+      return launch("pass_forward", k, grid_f, block_f, smF, st, DF, AF);
     };
-    for (int pi = 0; pi < NP - 1; ++pi) {
+    auto adj_pass = [&](int pi, uint32_t flags) {
       A.pass = pi;
-      A.flags = (pi == 0 ? F_INIT : F_LOAD_PSI) | F_FWD | F_STORE_PSI;
-      if ((rc = launch_pass("pass_forward", pass_k(p, false, A.pass), block, sm1))) return rc;
-    }
-    const uint32_t first = NP == 1 ? F_INIT : F_LOAD_PSI;
-    A.pass = NP - 1;
+      A.flags = flags;
+      return launch("pass_adjoint", pass_k(p, true, pi), grid, block2, smB, st, D, A);
+    };
+    const uint32_t stores = F_STORE_PSI | F_STORE_PHI;
+    // forward sweep: all but the last forward pass
+    for (int pi = 0; pi < NPF - 1; ++pi)
+      if ((rc = fwd_pass(pi, (pi == 0 ? F_INIT : F_LOAD_PSI) | F_FWD | F_STORE_PSI))) return rc;
+    const uint32_t first = NPF == 1 ? F_INIT : F_LOAD_PSI;
+    int exp_tiles = tiles_f;  // tiles of the kernel that observes (expectation partials)
     if (mode == VQC_MODE_FORWARD) {
-      A.flags = first | F_FWD | F_OBSERVE;
-      if ((rc = launch_pass("pass_forward", pass_k(p, false, A.pass), block, sm1))) return rc;
+      if ((rc = fwd_pass(NPF - 1, first | F_FWD | F_OBSERVE))) return rc;
     } else if (mode == VQC_MODE_VJP) {
-      A.flags = first | F_FWD | F_OBSERVE | F_SEED | F_BWD | (NP > 1 ? (F_STORE_PSI | F_STORE_PHI) : 0);
-      if ((rc = launch_pass("pass_adjoint", pass_k(p, true, A.pass), block2, sm2))) return rc;
-      for (int pi = NP - 2; pi >= 0; --pi) {
-        A.pass = pi;
-        A.flags = F_LOAD_PSI | F_LOAD_PHI | F_BWD | (pi > 0 ? (F_STORE_PSI | F_STORE_PHI) : 0);
-        if ((rc = launch_pass("pass_adjoint", pass_k(p, true, A.pass), block2, sm2))) return rc;
+      if (!sep) {
+        if ((rc = adj_pass(NP - 1, first | F_FWD | F_OBSERVE | F_SEED | F_BWD | (NP > 1 ? stores : 0)))) return rc;
+      } else {
+        if ((rc = fwd_pass(NPF - 1, first | F_FWD | F_STORE_PSI))) return rc;
+        if ((rc = adj_pass(NP - 1, F_LOAD_PSI | F_OBSERVE | F_SEED | F_BWD | (NP > 1 ? stores : 0)))) return rc;
       }
+      exp_tiles = L.n_tiles;
+      for (int pi = NP - 2; pi >= 0; --pi)
+        if ((rc = adj_pass(pi, F_LOAD_PSI | F_LOAD_PHI | F_BWD | (pi > 0 ? stores : 0)))) return rc;
     } else {
-      A.flags = first | F_FWD | F_OBSERVE | F_STORE_FIN;
-      if ((rc = launch_pass("pass_forward", pass_k(p, false, A.pass), block, sm1))) return rc;
+      if ((rc = fwd_pass(NPF - 1, first | F_FWD | F_OBSERVE | F_STORE_FIN))) return rc;
       for (int m = 0; m < p->M; ++m) {
         A.bra = m;
-        A.pass = NP - 1;
-        A.flags = F_LOAD_FIN | F_SEED | F_BWD | (NP > 1 ? (F_STORE_PSI | F_STORE_PHI) : 0);
-        if ((rc = launch_pass("pass_adjoint", pass_k(p, true, A.pass), block2, sm2))) return rc;
-        for (int pi = NP - 2; pi >= 0; --pi) {
-          A.pass = pi;
-          A.flags = F_LOAD_PSI | F_LOAD_PHI | F_BWD | (pi > 0 ? (F_STORE_PSI | F_STORE_PHI) : 0);
-          if ((rc = launch_pass("pass_adjoint", pass_k(p, true, A.pass), block2, sm2))) return rc;
-        }
+        if ((rc = adj_pass(NP - 1, F_LOAD_FIN | F_SEED | F_BWD | (NP > 1 ? stores : 0)))) return rc;
+        for (int pi = NP - 2; pi >= 0; --pi)
+          if ((rc = adj_pass(pi, F_LOAD_PSI | F_LOAD_PHI | F_BWD | (pi > 0 ? stores : 0)))) return rc;
       }
     }
     if (adj && (rc = run_tile_reduce(ipart, ip + (size_t)b0 * L.K * P.NG, nb * L.K * P.NG, L.n_tiles, st)))
       return rc;
-    if (d_expect && (rc = run_tile_reduce(epart, d_expect + (size_t)b0 * p->M, nb * p->M, L.n_tiles, st)))
+    if (d_expect && (rc = run_tile_reduce(epart, d_expect + (size_t)b0 * p->M, nb * p->M, exp_tiles, st)))
       return rc;
   }
   return VQC_OK;
@@ -603,7 +655,8 @@ int check_common(const VqcPlan* p, const double* d_in, const double* d_w, int64_
 // flat gate list -> scheduled device program (shared by plan creation and
 // the CPU-side JIT source dump)
 int schedule_circuit(const VqcCircuit* c, const int64_t* wrt_col, HostProgram* prog,
-                     std::vector<uint32_t>* zmask = nullptr, std::vector<double>* zcoeff = nullptr) {
+                     std::vector<uint32_t>* zmask = nullptr, std::vector<double>* zcoeff = nullptr,
+                     int tile_override = 0, int regs_override = 0) {
   std::vector<GateIn> gates((size_t)c->n_gates);
   for (int64_t g = 0; g < c->n_gates; ++g) {
     GateIn& gi = gates[g];
@@ -631,7 +684,9 @@ int schedule_circuit(const VqcCircuit* c, const int64_t* wrt_col, HostProgram* p
   // interpreter kernels exist for R = 4 passes only.
   opt.reg_slots = 4;
   if (c->n_qubits > opt.smem_max_qubits && env_int("VQC_JIT", -1) != 0)
-    opt.reg_slots = std::max(3, std::min(4, env_int("VQC_REG_SLOTS", 4)));
+    opt.reg_slots = std::max(3, std::min(4, env_int("VQC_REG_SLOTS", kHbmAdjointRegs)));
+  if (tile_override > 0) opt.tile_qubits = tile_override;
+  if (regs_override > 0) opt.reg_slots = regs_override;
   const int absorbed = prog->absorbed;
   std::string err = build_program(gates, c->n_qubits, c->total_params, wcol, opt, prog);
   prog->absorbed = absorbed;
@@ -641,6 +696,41 @@ int schedule_circuit(const VqcCircuit* c, const int64_t* wrt_col, HostProgram* p
                     : VQC_E_UNSUPPORTED,
                 err);
   return VQC_OK;
+}
+
+// DevProgram of a scheduled program (its tables + the plan's observables)
+void fill_dev(const VqcPlan* p, const HostProgram& P, const ProgTabs& t, DevProgram& D) {
+  D.ops = t.ops;
+  D.segs = t.segs;
+  D.ipouts = t.ipouts;
+  D.blocks = t.blocks;
+  D.members = t.members;
+  D.diag = t.diag;
+  D.setids = t.setids;
+  D.thr_tab = t.thr_tab;
+  D.passes = t.passes;
+  D.rots = t.rots;
+  D.n_blk = P.n_blk;
+  D.n_av = P.n_av;
+  D.max_rot_pass = P.max_rot_per_pass;
+  D.max_blk_pass = P.max_blk_per_pass;
+  D.max_av_pass = P.max_av_per_pass;
+  D.term_offs = p->d_term_offs;
+  D.t_smask = p->d_smask;
+  D.t_xmask = p->d_xmask;
+  D.t_phase = p->d_tphase;
+  D.has_xy = p->has_xy ? 1 : 0;
+  D.t_coeff = p->d_tcoeff;
+  D.n = P.n;
+  D.k = P.k;
+  D.R = P.R;
+  D.NG = P.NG;
+  D.n_rot = P.n_rot;
+  D.M = p->M;
+  D.T = (int)p->smask.size();
+  D.n_pass = (int)P.passes.size();
+  D.enc_off = p->enc_off;
+  D.enc_size = p->enc_size;
 }
 
 }  // namespace
@@ -660,6 +750,8 @@ int64_t vqc_jit_source(const VqcCircuit* c, const int64_t* wrt_col, int compile,
   std::vector<uint32_t> zm;  // as for Z-string observables (trailing gates absorbed)
   std::vector<double> zc;
   if (int rc = schedule_circuit(c, wrt_col, &prog, &zm, &zc)) return rc;
+  if (prog.hbm && env_int("VQC_ADJ_DUAL", prog.R <= 3 ? 1 : 0) != 0) prog.adj_dual = true;
+  build_thr_table(prog.segs);  // per-segment thread-table offsets, as at plan creation
   const std::string src = jit_source(prog, use_split(prog.n, prog.R));
   if (compile) {
     std::string err = jit_compile_only(prog, use_split(prog.n, prog.R), compile_s);
@@ -778,18 +870,8 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
   std::string err;
   cudaError_t e = cudaGetDevice(&p->device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, p->device);
-  const std::vector<ThrEntry> thr_tab = build_thr_table(p->prog.segs);
   const HostProgram& P = p->prog;
-  if (e == cudaSuccess) e = upload(thr_tab, &p->d_thr_tab);
-  if (e == cudaSuccess) e = upload(P.ops, &p->d_ops);
-  if (e == cudaSuccess) e = upload(P.segs, &p->d_segs);
-  if (e == cudaSuccess) e = upload(P.ipouts, &p->d_ipouts);
-  if (e == cudaSuccess) e = upload(P.blocks, &p->d_blocks);
-  if (e == cudaSuccess) e = upload(P.members, &p->d_members);
-  if (e == cudaSuccess) e = upload(P.diag, &p->d_diag);
-  if (e == cudaSuccess) e = upload(P.setids, &p->d_setids);
-  if (e == cudaSuccess) e = upload(P.passes, &p->d_passes);
-  if (e == cudaSuccess) e = upload(P.rots, &p->d_rots);
+  if (e == cudaSuccess) e = p->tabs.upload_all(p->prog.segs, p->prog);
   if (e == cudaSuccess) e = upload(p->term_offs, &p->d_term_offs);
   if (e == cudaSuccess) e = upload(p->smask, &p->d_smask);
   if (e == cudaSuccess) e = upload(p->xmask, &p->d_xmask);
@@ -801,38 +883,7 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
     vqc_plan_destroy(p);
     return cuda_fail(e, "plan upload");
   }
-  DevProgram& D = p->D;
-  D.ops = p->d_ops;
-  D.segs = p->d_segs;
-  D.ipouts = p->d_ipouts;
-  D.blocks = p->d_blocks;
-  D.members = p->d_members;
-  D.diag = p->d_diag;
-  D.setids = p->d_setids;
-  D.thr_tab = p->d_thr_tab;
-  D.n_blk = P.n_blk;
-  D.n_av = P.n_av;
-  D.max_rot_pass = P.max_rot_per_pass;
-  D.max_blk_pass = P.max_blk_per_pass;
-  D.max_av_pass = P.max_av_per_pass;
-  D.passes = p->d_passes;
-  D.rots = p->d_rots;
-  D.term_offs = p->d_term_offs;
-  D.t_smask = p->d_smask;
-  D.t_xmask = p->d_xmask;
-  D.t_phase = p->d_tphase;
-  D.has_xy = p->has_xy ? 1 : 0;
-  D.t_coeff = p->d_tcoeff;
-  D.n = P.n;
-  D.k = P.k;
-  D.R = P.R;
-  D.NG = P.NG;
-  D.n_rot = P.n_rot;
-  D.M = p->M;
-  D.T = (int)p->smask.size();
-  D.n_pass = (int)P.passes.size();
-  D.enc_off = p->enc_off;
-  D.enc_size = p->enc_size;
+  fill_dev(p, P, p->tabs, p->D);
   p->state_budget = (size_t)env_int("VQC_STATE_BUDGET_MB", 16384) << 20;
   // JIT policy (VQC_JIT): unset = specialise HBM-pass plans (per-pass units
   // compile in parallel) and on-chip plans of n >= 8 qubits (shape-shared
@@ -841,12 +892,42 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
   const int jit_mode = env_int("VQC_JIT", -1);
   const bool want_jit = jit_mode > 0 || (jit_mode < 0 && (P.hbm || P.n >= 8));
   if (want_jit && P.n_fwd_ops + P.n_bwd_ops > 0) {
+    // HBM adjoint with both states per thread when its register slots allow
+    // (VQC_ADJ_DUAL overrides: 0 = thread pairs)
+    if (P.hbm && env_int("VQC_ADJ_DUAL", P.R <= 3 ? 1 : 0) != 0) p->prog.adj_dual = true;
     err = jit_build(P, use_split(P.n, P.R), &p->jit);
     if (!err.empty()) {
       vqc_plan_destroy(p);
       return fail(VQC_E_CUDA, err);
     }
     p->use_jit = true;
+    // separate forward schedule (VQC_FWD_TILE / VQC_FWD_REG) when it differs
+    const int ft = env_int("VQC_FWD_TILE", P.k), fr = std::max(3, std::min(4, env_int("VQC_FWD_REG", kHbmForwardRegs)));
+    if (P.hbm && (ft != P.k || fr != P.R)) {
+      ProgDev* f = new ProgDev();
+      p->fwd = f;
+      std::vector<uint32_t> zm = p->smask;  // the same trailing gates are absorbed; masks already rewritten
+      std::vector<double> zc = p->tcoeff;
+      const bool z = !p->has_xy;
+      if (int rc = schedule_circuit(c, wrt_col, &f->prog, z ? &zm : nullptr, z ? &zc : nullptr, ft, fr)) {
+        vqc_plan_destroy(p);
+        return rc;
+      }
+      if (!f->prog.hbm || f->prog.NG != P.NG) {
+        vqc_plan_destroy(p);
+        return fail(VQC_E_UNSUPPORTED, "forward schedule disagrees with the adjoint schedule");
+      }
+      if ((e = f->tabs.upload_all(f->prog.segs, f->prog)) != cudaSuccess) {
+        vqc_plan_destroy(p);
+        return cuda_fail(e, "plan upload");
+      }
+      fill_dev(p, f->prog, f->tabs, f->D);
+      err = jit_build(f->prog, false, &f->jit);
+      if (!err.empty()) {
+        vqc_plan_destroy(p);
+        return fail(VQC_E_CUDA, err);
+      }
+    }
   }
   *out = p;
   return VQC_OK;
@@ -854,16 +935,11 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
 
 void vqc_plan_destroy(VqcPlan* p) {
   if (!p) return;
-  cudaFree(p->d_ops);
-  cudaFree(p->d_segs);
-  cudaFree(p->d_ipouts);
-  cudaFree(p->d_blocks);
-  cudaFree(p->d_members);
-  cudaFree(p->d_diag);
-  cudaFree(p->d_setids);
-  cudaFree(p->d_thr_tab);
-  cudaFree(p->d_passes);
-  cudaFree(p->d_rots);
+  p->tabs.free_all();
+  if (p->fwd) {
+    p->fwd->tabs.free_all();
+    delete p->fwd;
+  }
   cudaFree(p->d_term_offs);
   cudaFree(p->d_smask);
   cudaFree(p->d_xmask);
@@ -885,15 +961,19 @@ int64_t vqc_plan_describe(const VqcPlan* p, char* buf, int64_t cap) {
   const HostProgram& P = p->prog;
   int nseg = 0;
   for (const PassDesc& pd : P.passes) nseg += pd.seg_end - pd.seg_begin;
-  char tmp[512];
+  char tmp[1024];
   const int len = snprintf(tmp, sizeof tmp,
                            "{\"n\": %d, \"mode\": \"%s\", \"tile_qubits\": %d, \"reg_slots\": %d, "
                            "\"passes\": %d, \"segments\": %d, \"rotations\": %d, \"grad_slots\": %d, "
                            "\"fwd_ops\": %d, \"bwd_ops\": %d, \"cols\": %d, \"obs\": %d, \"jit\": %s, "
-                           "\"jit_compile_s\": %.3f, \"jit_cubin_bytes\": %zu, \"absorbed_gates\": %d}",
+                           "\"jit_compile_s\": %.3f, \"jit_cubin_bytes\": %zu, \"absorbed_gates\": %d, \"adjoint_dual\": %s, "
+                           "\"fwd_tile_qubits\": %d, \"fwd_reg_slots\": %d, \"fwd_passes\": %d}",
                            P.n, P.hbm ? "hbm" : "smem", P.k, P.R, (int)P.passes.size(), nseg, P.n_rot,
                            P.NG, P.n_fwd_ops, P.n_bwd_ops, P.n_cols, p->M, p->use_jit ? "true" : "false",
-                           p->jit.compile_s, p->jit.cubin_bytes, P.absorbed);
+                           p->jit.compile_s + (p->fwd ? p->fwd->jit.compile_s : 0.0),
+                           p->jit.cubin_bytes + (p->fwd ? p->fwd->jit.cubin_bytes : 0), P.absorbed,
+                           P.adj_dual ? "true" : "false", p->fwd ? p->fwd->prog.k : P.k,
+                           p->fwd ? p->fwd->prog.R : P.R, (int)(p->fwd ? p->fwd->prog.passes.size() : P.passes.size()));
   if (buf && cap > 0) {
     const int64_t c = std::min<int64_t>(cap - 1, len);
     memcpy(buf, tmp, (size_t)c);

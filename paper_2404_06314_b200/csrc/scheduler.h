@@ -50,6 +50,7 @@ struct HostProgram {
   // stats
   int n_fwd_ops = 0, n_bwd_ops = 0;
   int absorbed = 0;  // trailing gates folded into the observables (absorb_trailing_gates)
+  bool adj_dual = false;  // HBM adjoint passes: both states per thread (JIT only) instead of thread pairs
 };
 
 // Fold the circuit's trailing parameter-free gates that map Z strings to Z

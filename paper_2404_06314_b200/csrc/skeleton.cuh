@@ -281,6 +281,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 template <int R, int KM, class SEGS>
 __device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A) {
   constexpr int OBS_E = KM == KM_SPLIT ? (1 << (R - 1)) : (1 << R);
+  constexpr int BMP = KM == KM_SPLIT ? MODE_SPLIT : MODE_DUAL;  // adjoint segments
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr bool ADJ = KM != KM_FWD;
   const PassDesc* pd = D.passes + A.pass;
@@ -376,7 +377,7 @@ __device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A)
   dbg_add(A, DBG_OBSERVE, tdbg);
   if constexpr (ADJ) {
     if (flags & F_BWD)
-      SEGS::template run<R, MODE_SPLIT>(make_env<MODE_SPLIT>(D, A, s_psi, s_phi, s_av, 0, pd->av_begin,
+      SEGS::template run<R, BMP>(make_env<BMP>(D, A, s_psi, s_phi, s_av, 0, pd->av_begin,
                                   s_red, s_fin, grp, true, tile_base, bl, A.bra < 0 ? 0 : A.bra, tile, n_tiles), T, pd->bseg_begin, pd->bseg_end);
   }
   dbg_add(A, DBG_BWD, tdbg);

@@ -24,7 +24,9 @@ def test_hbm_plan_has_one_kernel_pair_per_pass():
     n_pf = src.count("void __launch_bounds__") // 2
     assert n_pf >= 10 and src.count("vqc_jit_pf") == n_pf and src.count("vqc_jit_pa") == n_pf
     # every fused set of cfg4 is emitted with compile-time slots
-    assert "jop_u2<R, MODE, 0, false>" in src and "jop_ip3set<R, MODE, 15>" in src
+    # adjoint schedule: 3 register slots, both states per thread
+    assert "jop_u2<R, MODE, 0, true>" in src and "jop_ip3set<R, MODE, 7>" in src
+    assert "vqc::KM_DUAL" in src
     assert "exec_op" not in src
 
 
