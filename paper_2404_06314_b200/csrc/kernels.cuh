@@ -911,7 +911,9 @@ __device__ __forceinline__ void seg_end(const SegEnv& E, const SD& sd, const Reg
 // group; MODE_SPLIT: role-0 threads hold psi, role-1 threads phi. Gradient
 // outputs go to A.ip (rows relative to A.b0, times n_tiles). Threads with
 // active == false only take part in the barriers.
+struct RtPassMap;  // pass index maps (defined with the tile walk below)
 struct InterpSegs {
+  using PM = RtPassMap;
   template <int R, int MODE>
   __device__ __forceinline__ static void run(const SegEnv& E, const SampleTables& T, int sb, int se) {
     const DevProgram& D = E.D;
@@ -996,19 +998,40 @@ __device__ __forceinline__ uint32_t pdep32(uint32_t l, uint32_t m) {
   return j;
 }
 
+// Pass index maps: tile-local position p -> global qubit bit (the pass's
+// local qubits in ascending order) and tile id -> the non-local global bits.
+// RtPassMap reads the pass descriptor; the JIT emits a map with the positions
+// as constants (kConst), so the tile walk's index math folds to shifts.
+struct RtPassMap {
+  static constexpr bool kConst = false;
+  static constexpr int k = 0;
+  __device__ __forceinline__ static uint32_t lane_dep(const PassDesc* pd, uint32_t l) {
+    uint32_t j = 0;
+    while (l) {
+      j |= 1u << pd->local_q[__ffs(l) - 1];
+      l &= l - 1;
+    }
+    return j;
+  }
+  __device__ __forceinline__ static uint32_t local_bit(const PassDesc* pd, int p) { return 1u << pd->local_q[p]; }
+  __device__ __forceinline__ static uint32_t tile_dep(const PassDesc* pd, int n, uint32_t t) {
+    return pdep32(t, ~pd->local_mask & ((1u << n) - 1u));
+  }
+};
+
+template <class PM = RtPassMap>
 __device__ __forceinline__ TileWalk tile_walk(const PassDesc* pd, uint32_t tile_base, int k, int lane,
                                               int stride) {
   TileWalk w;
   const int Nt = 1 << k;
   w.count = Nt / stride;
-  const uint32_t lm = pd ? pd->local_mask : 0u;
-  w.base = tile_base | (pd ? pdep32((uint32_t)lane, lm) : (uint32_t)lane);
+  w.base = tile_base | (pd ? PM::lane_dep(pd, (uint32_t)lane) : (uint32_t)lane);
   w.sbase = swz((uint32_t)lane);
   const int s0 = __ffs(stride) - 1;  // stride is a power of two: hi[b] is one local bit
 #pragma unroll
   for (int b = 0; b < kMaxR; ++b) {
     const int p = s0 + b;
-    w.hi[b] = p < k ? (pd ? pdep32(1u << p, lm) : (1u << p)) : 0u;
+    w.hi[b] = p < k ? (pd ? PM::local_bit(pd, p) : (1u << p)) : 0u;
     w.shi[b] = p < k ? swz(1u << p) : 0u;
   }
   return w;

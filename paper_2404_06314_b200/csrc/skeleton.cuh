@@ -37,14 +37,14 @@ __device__ __forceinline__ void stage_terms(const DevProgram& D, TermSm* s_terms
 // sign over them is parity(base & s) ^ parity(i & h), h bit b =
 // parity(hi[b] & s), so no per-element index arithmetic is needed.
 // E: elements per thread (compile time; equals the tile walk's count)
-template <bool DUAL, int E>
+template <bool DUAL, int E, class PM = RtPassMap>
 __device__ __forceinline__ void observe(const DevProgram& D, const RunArgs& A, const PassDesc* pd, double2* s_psi,
                                         double2* s_phi, const double* s_u_row, const TermSm* s_terms,
                                         const Group& grp, double* s_red, double* s_fin, uint32_t tile_base, int k,
                                         int64_t bl0, bool do_expect, int seed_mode, int bra, int tile,
                                         int n_tiles) {
   const int lane = grp.lane_in_sample();
-  const TileWalk tw = tile_walk(pd, tile_base, k, lane, grp.TT);
+  const TileWalk tw = tile_walk<PM>(pd, tile_base, k, lane, grp.TT);
   const int count = tw.count;
   auto term_bits = [&](uint32_t mask, uint32_t& p0, uint32_t& h) {
     p0 = (uint32_t)__popc(tw.base & mask) & 1u;
@@ -284,16 +284,18 @@ __device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A)
   constexpr int BMP = KM == KM_SPLIT ? MODE_SPLIT : MODE_DUAL;  // adjoint segments
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr bool ADJ = KM != KM_FWD;
+  using PM = typename SEGS::PM;
   const PassDesc* pd = D.passes + A.pass;
-  const int k = pd->k, Nt = 1 << k;
+  const int k = PM::kConst ? PM::k : pd->k, Nt = 1 << k;
+  // threads per tile (the walk stride): compile time for JIT pass maps
+  const int wstride = PM::kConst ? ((KM == KM_SPLIT ? 2 : 1) << (PM::k - R)) : (int)blockDim.x;
   const uint32_t flags = A.flags;
   const Group grp = make_group<R, KM>(1 << (k - R), 1);
   const int tile = blockIdx.x, n_tiles = gridDim.x;
   const int64_t bl = blockIdx.y;
   const int64_t b = A.b0 + bl;
   const size_t N = (size_t)1 << D.n;
-  const uint32_t nonlocal = ~pd->local_mask & ((1u << D.n) - 1u);
-  const uint32_t tile_base = pdep32((uint32_t)tile, nonlocal);
+  const uint32_t tile_base = PM::tile_dep(pd, D.n, (uint32_t)tile);
   const SmemLayout L(1, Nt, ADJ, D.max_rot_pass, D.max_blk_pass, D.max_av_pass, A.red_slots, (int)blockDim.x,
                      D.M, D.T);
   double2* s_psi = reinterpret_cast<double2*>(smem_raw + L.psi);
@@ -320,7 +322,7 @@ __device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A)
     const double2* src = ((flags & F_LOAD_FIN) ? A.psi_fin : A.psi) + (size_t)bl * N;
     const double2* srcf = A.phi + (size_t)bl * N;
     const bool lphi = ADJ && (flags & F_LOAD_PHI);
-    const TileWalk tw = tile_walk(pd, tile_base, k, threadIdx.x, blockDim.x);
+    const TileWalk tw = tile_walk<PM>(pd, tile_base, k, threadIdx.x, wstride);
     for_tile<OBS_E>(tw, [&](uint32_t sw, uint32_t j) {
       cp_async16(s_psi + sw, src + j);
       if (lphi) cp_async16(s_phi + sw, srcf + j);
@@ -329,7 +331,7 @@ __device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A)
     // loads then come from L2 while this CTA computes)
     const int64_t nxt = ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) + A.pf_dist;
     if (A.pf_dist > 0 && nxt < (int64_t)gridDim.x * gridDim.y) {
-      const uint32_t tb2 = pdep32((uint32_t)(nxt % gridDim.x), nonlocal);
+      const uint32_t tb2 = PM::tile_dep(pd, D.n, (uint32_t)(nxt % gridDim.x));
       const int64_t row2 = nxt / gridDim.x;
       const double2* src2 = ((flags & F_LOAD_FIN) ? A.psi_fin : A.psi) + (size_t)row2 * N;
       const double2* srcf2 = A.phi + (size_t)row2 * N;
@@ -365,12 +367,12 @@ __device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A)
   if (flags & F_STORE_FIN) {
     uint32_t tb = tile_base;
     asm volatile("" : "+r"(tb));
-    const TileWalk tw = tile_walk(pd, tb, k, threadIdx.x, blockDim.x);
+    const TileWalk tw = tile_walk<PM>(pd, tb, k, threadIdx.x, wstride);
     double2* dst = A.psi_fin + (size_t)bl * N;
     for_tile<OBS_E>(tw, [&](uint32_t sw, uint32_t j) { dst[j] = s_psi[sw]; });
   }
   if (flags & (F_OBSERVE | F_SEED)) {
-    observe<ADJ, OBS_E>(D, A, pd, s_psi, s_phi, s_up, s_terms, grp, s_red, s_fin, tile_base, k, bl, (flags & F_OBSERVE) != 0,
+    observe<ADJ, OBS_E, PM>(D, A, pd, s_psi, s_phi, s_up, s_terms, grp, s_red, s_fin, tile_base, k, bl, (flags & F_OBSERVE) != 0,
                  (flags & F_SEED) ? (A.bra < 0 ? 1 : 2) : 0, A.bra, tile, n_tiles);
     __syncthreads();
   }
@@ -386,7 +388,7 @@ __device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A)
     asm volatile("" ::: "memory");
     uint32_t tb = tile_base;
     asm volatile("" : "+r"(tb));  // rebuild the tile walk here rather than keep it live
-    const TileWalk tw = tile_walk(pd, tb, k, threadIdx.x, blockDim.x);
+    const TileWalk tw = tile_walk<PM>(pd, tb, k, threadIdx.x, wstride);
     const bool spsi = (flags & F_STORE_PSI) != 0;
     double2* dst = A.psi + (size_t)bl * N;
     double2* dstf = A.phi + (size_t)bl * N;
