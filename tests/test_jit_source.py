@@ -30,8 +30,9 @@ def test_hbm_plan_has_one_kernel_pair_per_pass():
     assert "exec_op" not in src
 
 
-def test_random_hbm_circuit_compiles_for_sm100a():
+def test_random_hbm_circuit_compiles_for_sm100a(monkeypatch):
     """Every gate kind (and so every op the scheduler emits) through NVRTC."""
+    monkeypatch.setenv("VQC_JIT_CACHE", "0")  # really compile (no cubin cache)
     from test_scheduler_sim import _random
     rng = np.random.default_rng(7)
     circ, _, _ = _random(rng, 13, 60)
@@ -41,12 +42,25 @@ def test_random_hbm_circuit_compiles_for_sm100a():
         assert op in src, op
 
 
-def test_on_chip_plan_shares_code_per_segment_shape():
+def test_on_chip_plan_shares_code_per_segment_shape(monkeypatch):
     """cfg3 (on-chip): 48 segments of two shapes -> two switch cases, and the
     unit compiles in seconds (it took minutes as one copy per segment)."""
+    monkeypatch.setenv("VQC_JIT_CACHE", "0")
     spec = configs.CONFIGS[3]
     circ, obs, wrt = configs.build(spec, configs.native_api())
     src, secs = _src(circ, wrt, compile=True)
     assert src.count("case 0:") == 2 and "case 1:" not in src
     assert "__constant__ int jf0_opnd" in src and "vqc_jit_sa" in src
     assert secs < 120
+
+
+def test_cubin_cache_round_trip(tmp_path, monkeypatch):
+    """The on-disk cubin cache returns what NVRTC produced (second call reads)."""
+    monkeypatch.setenv("VQC_JIT_CACHE", str(tmp_path))
+    from test_scheduler_sim import _random
+    circ, _, _ = _random(np.random.default_rng(3), 13, 30)
+    _, t1 = _src(circ, ("a", "b", "s"), compile=True)
+    n_files = len(list(tmp_path.glob("*.cubin")))
+    _, t2 = _src(circ, ("a", "b", "s"), compile=True)
+    assert n_files >= 1 and len(list(tmp_path.glob("*.cubin"))) == n_files
+    assert t2 < t1
