@@ -396,7 +396,7 @@ int red_slots(const VqcPlan* p) { return std::max(1, std::max(p->M, p->prog.max_
 int smem_samples(const VqcPlan* p, int64_t B, bool dual, size_t* smem_bytes, int* threads_per_sample) {
   const HostProgram& P = p->prog;
   const int TPS = 1 << (P.n - P.R);
-  const bool split = dual && use_split(P.n, P.R);
+  const bool split = dual && use_split(P.n, P.R) && !P.adj_dual;
   const int TT = split ? 2 * TPS : TPS;
   *threads_per_sample = TT;
   auto bytes_for = [&](int S) {
@@ -685,6 +685,11 @@ int schedule_circuit(const VqcCircuit* c, const int64_t* wrt_col, HostProgram* p
   opt.reg_slots = 4;
   if (c->n_qubits > opt.smem_max_qubits && env_int("VQC_JIT", -1) != 0)
     opt.reg_slots = std::max(3, std::min(4, env_int("VQC_REG_SLOTS", kHbmAdjointRegs)));
+  // on-chip JIT plans large enough for thread pairs: 3 slots, both states
+  // per thread (VQC_SMEM_DUAL)
+  if (c->n_qubits <= opt.smem_max_qubits && c->n_qubits >= 9 && env_int("VQC_JIT", -1) != 0 &&
+      env_int("VQC_SMEM_DUAL", 0) != 0)
+    opt.reg_slots = 3;
   if (tile_override > 0) opt.tile_qubits = tile_override;
   if (regs_override > 0) opt.reg_slots = regs_override;
   const int absorbed = prog->absorbed;
@@ -750,11 +755,13 @@ int64_t vqc_jit_source(const VqcCircuit* c, const int64_t* wrt_col, int compile,
   std::vector<uint32_t> zm;  // as for Z-string observables (trailing gates absorbed)
   std::vector<double> zc;
   if (int rc = schedule_circuit(c, wrt_col, &prog, &zm, &zc)) return rc;
-  if (prog.hbm && env_int("VQC_ADJ_DUAL", prog.R <= 3 ? 1 : 0) != 0) prog.adj_dual = true;
+  if ((prog.hbm || env_int("VQC_SMEM_DUAL", 0) != 0) && env_int("VQC_ADJ_DUAL", prog.R <= 3 ? 1 : 0) != 0)
+    prog.adj_dual = true;
   build_thr_table(prog.segs);  // per-segment thread-table offsets, as at plan creation
-  const std::string src = jit_source(prog, use_split(prog.n, prog.R));
+  const bool split = use_split(prog.n, prog.R) && !prog.adj_dual;
+  const std::string src = jit_source(prog, split);
   if (compile) {
-    std::string err = jit_compile_only(prog, use_split(prog.n, prog.R), compile_s);
+    std::string err = jit_compile_only(prog, split, compile_s);
     if (!err.empty()) return fail(VQC_E_CUDA, err);
   }
   if (buf && cap > 0) {
@@ -894,8 +901,9 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
   if (want_jit && P.n_fwd_ops + P.n_bwd_ops > 0) {
     // HBM adjoint with both states per thread when its register slots allow
     // (VQC_ADJ_DUAL overrides: 0 = thread pairs)
-    if (P.hbm && env_int("VQC_ADJ_DUAL", P.R <= 3 ? 1 : 0) != 0) p->prog.adj_dual = true;
-    err = jit_build(P, use_split(P.n, P.R), &p->jit);
+    if ((P.hbm || (P.R <= 3 && env_int("VQC_SMEM_DUAL", 0) != 0)) && env_int("VQC_ADJ_DUAL", P.R <= 3 ? 1 : 0) != 0)
+      p->prog.adj_dual = true;
+    err = jit_build(P, use_split(P.n, P.R) && !P.adj_dual, &p->jit);
     if (!err.empty()) {
       vqc_plan_destroy(p);
       return fail(VQC_E_CUDA, err);
