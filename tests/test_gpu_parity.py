@@ -170,6 +170,41 @@ def test_random_with_cz_vs_oracle(torch_cuda, n):
         assert close(res.gradients[k], j_ref[k]) < TOL
 
 
+@pytest.mark.parametrize("n,jit", [(9, "0"), (12, "0"), (13, "0"), (14, "0"), (9, "1"), (13, "1")])
+def test_kernel_paths_vs_oracle(torch_cuda, monkeypatch, n, jit):
+    """The prebuilt interpreter (VQC_JIT=0: op-decoding kernels, 4-slot thread
+    pairs) and the JIT with every variant forced (VQC_JIT=1), on the same
+    random circuits as the default path."""
+    monkeypatch.setenv("VQC_JIT", jit)
+    rng = np.random.default_rng(300 + n)
+    circ, trainable = _rand_circuit(rng, n, 30 + 4 * n)
+    obs = _z_obs(rng, n, 2)
+    x = rng.uniform(-2, 2, (4, 4))
+    wrt = ("a", "b", "s")
+    e_ref, j_ref = oracle_batch(circ, obs, trainable, x, wrt)
+    res = _engine().run_batch(_request(circ, obs, trainable, x, wrt))
+    assert close(res.expectations, e_ref) < TOL
+    for k in wrt:
+        assert close(res.gradients[k], j_ref[k]) < TOL
+
+
+@pytest.mark.parametrize("knobs", [{"VQC_ADJ_DUAL": "0", "VQC_REG_SLOTS": "4"}, {"VQC_SMEM_DUAL": "1"},
+                                   {"VQC_FWD_TILE": "12"}])
+def test_schedule_variants_cfg4_rows(torch_cuda, monkeypatch, knobs):
+    """Alternative schedules (thread-pair 4-slot adjoint, dual on-chip adjoint,
+    12-qubit forward tiles) agree with the reference golden rows."""
+    from paper_2404_06314_b200 import configs
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    cfg = 4 if "VQC_SMEM_DUAL" not in knobs else 3
+    g = _golden(f"cfg{cfg}.npz")
+    spec = configs.CONFIGS[cfg]
+    circ, obs, wrt = configs.build(spec, configs.native_api())
+    res = _engine().run_batch(_request(circ, obs, {"w": g["w"]}, g["x_rows"], wrt))
+    assert close(res.expectations, g["expect"]) < TOL
+    assert close(res.gradients["w"], g["jac_w"]) < TOL
+
+
 def test_hbm_chunking_is_bitwise_invariant(torch_cuda, monkeypatch):
     """Row chunking (state budget) must not change any per-row result."""
     from paper_2404_06314_b200 import configs
