@@ -520,6 +520,14 @@ __device__ __forceinline__ void jop_czrun(Regs<R>& a, Regs<R>& f, const DiagRun*
   if constexpr (MODE == MODE_DUAL) g_czrun<R>(f, qreg, m, qc);
 }
 
+// fused CZ run with the quadratic form already evaluated (JIT: the run's
+// masks are compile-time constants, no descriptor loads)
+template <int R, int MODE>
+__device__ __forceinline__ void jop_czsign(Regs<R>& a, Regs<R>& f, uint32_t qreg, uint32_t m, uint32_t qc) {
+  g_czrun<R>(a, qreg, m, qc);
+  if constexpr (MODE == MODE_DUAL) g_czrun<R>(f, qreg, m, qc);
+}
+
 // inner products: partial sums into reduction slots (adjoint modes only)
 template <int R, int MODE, int S>
 __device__ __forceinline__ void jop_ip3(const SegCtx<R>& C, const Regs<R>& a, const Regs<R>& f, int role,
