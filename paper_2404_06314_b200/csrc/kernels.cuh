@@ -777,6 +777,11 @@ __device__ __forceinline__ SegEnv make_env(const DevProgram& D, const RunArgs& A
 // interpreter); the JIT emits a struct with the same static members as
 // compile-time constants, so unused folds and address maps disappear.
 struct RtSeg {
+  // JIT descriptors compute the thread maps from gi (thr_j0 / thr_lp0 / thr_sp0)
+  __host__ __device__ static constexpr bool thr_const() { return false; }
+  __device__ static uint32_t thr_j0(uint32_t) { return 0u; }
+  __device__ static uint32_t thr_lp0(uint32_t) { return 0u; }
+  __device__ static uint32_t thr_sp0(uint32_t) { return 0u; }
   const SegDesc* sd;
   __device__ __forceinline__ int nthr() const { return sd->nthr; }
   __device__ __forceinline__ int thr_off() const { return sd->thr_off; }
@@ -797,10 +802,16 @@ __device__ __forceinline__ void seg_begin(const SegEnv& E, const SD& sd, SegCtx<
   const int nthr = sd.nthr();
   C.own = E.own;
   C.partner = E.partner;
-  const ThrEntry* te = E.D.thr_tab + sd.thr_off() + (E.grp.gi & ((1 << nthr) - 1));
-  const uint2 e01 = *reinterpret_cast<const uint2*>(te);
-  C.J0 = E.tile_base | e01.x;
-  C.lp0 = e01.y;
+  if constexpr (SD::thr_const()) {
+    const uint32_t gi = (uint32_t)E.grp.gi & ((1u << nthr) - 1u);
+    C.J0 = E.tile_base | SD::thr_j0(gi);
+    C.lp0 = SD::thr_lp0(gi);
+  } else {
+    const ThrEntry* te = E.D.thr_tab + sd.thr_off() + (E.grp.gi & ((1 << nthr) - 1));
+    const uint2 e01 = *reinterpret_cast<const uint2*>(te);
+    C.J0 = E.tile_base | e01.x;
+    C.lp0 = e01.y;
+  }
   // folded CNOT runs controlled by tile (non-local) bits
   if (E.tile_base != 0) {
 #pragma unroll
@@ -850,8 +861,13 @@ __device__ __forceinline__ void seg_end(const SegEnv& E, const SD& sd, const Reg
   if (MODE == MODE_SPLIT && sd.ip_count() > 0) __syncthreads();  // partners done reading
   asm volatile("" ::: "memory");  // keep the store map's loads and math after the op loop
   if (E.active) {
-    const ThrEntry* te = E.D.thr_tab + sd.thr_off() + (grp.gi & ((1 << sd.nthr()) - 1));
-    uint32_t sp0 = te->sp0, sc[R];
+    uint32_t sp0, sc[R];
+    if constexpr (SD::thr_const()) {
+      sp0 = SD::thr_sp0((uint32_t)grp.gi & ((1u << sd.nthr()) - 1u));
+    } else {
+      const ThrEntry* te = E.D.thr_tab + sd.thr_off() + (grp.gi & ((1 << sd.nthr()) - 1));
+      sp0 = te->sp0;
+    }
     if (E.tile_base != 0) {
 #pragma unroll
       for (int t = 0; t < R; ++t)
