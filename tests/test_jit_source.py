@@ -43,14 +43,15 @@ def test_random_hbm_circuit_compiles_for_sm100a(monkeypatch):
 
 
 def test_on_chip_plan_shares_code_per_segment_shape(monkeypatch):
-    """cfg3 (on-chip): 48 segments of two shapes -> two switch cases, and the
-    unit compiles in seconds (it took minutes as one copy per segment)."""
+    """cfg3 (on-chip): 48 segments of two shapes -> one switch case per shape
+    and unit, compiled in seconds (minutes as one copy per segment)."""
     monkeypatch.setenv("VQC_JIT_CACHE", "0")
     spec = configs.CONFIGS[3]
     circ, obs, wrt = configs.build(spec, configs.native_api())
     src, secs = _src(circ, wrt, compile=True)
-    assert src.count("case 0:") == 2 and "case 1:" not in src
-    assert "__constant__ int jf0_opnd" in src and "vqc_jit_sa" in src
+    # forward-only unit (1 shape) + forward/adjoint unit (2 shapes)
+    assert src.count("case 0:") == 3 and "case 1:" not in src
+    assert "__constant__ int sab0_opnd" in src and "vqc_jit_sa" in src and "vqc_jit_sf" in src
     assert secs < 120
 
 
