@@ -412,10 +412,13 @@ int smem_samples(const VqcPlan* p, int64_t B, bool dual, size_t* smem_bytes, int
   return S;
 }
 
-size_t pass_smem(const VqcPlan* p, const HostProgram& P, bool dual) {
+// dynamic shared memory of a pass kernel; rs = reduction slots (0 for forward
+// passes that neither observe nor reduce: more CTAs fit per SM)
+size_t pass_smem(const VqcPlan* p, const HostProgram& P, bool dual, int rs = -1) {
   const int TPS = 1 << (P.k - P.R);
   return SmemLayout(1, 1 << P.k, dual, P.max_rot_per_pass, P.max_blk_per_pass, P.max_av_per_pass,
-                    red_slots(p), (dual && !P.adj_dual) ? 2 * TPS : TPS, p->M, (int)p->smask.size()).total;
+                    rs < 0 ? red_slots(p) : rs, (dual && !P.adj_dual) ? 2 * TPS : TPS, p->M,
+                    (int)p->smask.size()).total;
 }
 
 int launch(const char* name, Kern k, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
@@ -538,7 +541,7 @@ int run_core(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, const
   const int TPS = 1 << (P.k - P.R), TPSF = 1 << (PF.k - PF.R);
   const int NP = (int)P.passes.size(), NPF = (int)PF.passes.size();
   const int tiles_f = 1 << (PF.n - PF.k);
-  const size_t smF = pass_smem(p, PF, false), smB = pass_smem(p, P, true);
+  const size_t smF = pass_smem(p, PF, false), smF0 = pass_smem(p, PF, false, 0), smB = pass_smem(p, P, true);
   for (int64_t b0 = 0; b0 < B; b0 += L.chunk) {
     const int64_t nb = std::min<int64_t>(L.chunk, B - b0);
     A.b0 = b0;
@@ -580,10 +583,12 @@ int run_core(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, const
     auto fwd_pass = [&](int pi, uint32_t flags) {
       AF.pass = pi;
       AF.flags = flags;
+      const bool obs = (flags & F_OBSERVE) != 0;
+      AF.red_slots = obs ? A.red_slots : 0;
       Kern k;
       if (sep) k.cu = p->fwd->jit.pass_fwd[pi];
       else k = pass_k(p, false, pi);
-      return launch("pass_forward", k, grid_f, block_f, smF, st, DF, AF);
+      return launch("pass_forward", k, grid_f, block_f, obs ? smF : smF0, st, DF, AF);
     };
     auto adj_pass = [&](int pi, uint32_t flags) {
       A.pass = pi;
