@@ -311,6 +311,7 @@ struct VqcPlan {
   std::vector<uint32_t> smask, xmask;
   std::vector<int32_t> tphase;
   std::vector<double> tcoeff;
+  std::vector<int32_t> tobs;  // observable of each term
   bool has_xy = false;
   // device tables
   ProgTabs tabs;  // device tables of `prog`
@@ -319,6 +320,7 @@ struct VqcPlan {
   uint32_t* d_xmask = nullptr;
   int32_t* d_tphase = nullptr;
   double* d_tcoeff = nullptr;
+  int32_t* d_tobs = nullptr;
   int32_t* d_col_offs = nullptr;
   ChainEntry* d_chain = nullptr;
   DevProgram D{};
@@ -731,6 +733,7 @@ void fill_dev(const VqcPlan* p, const HostProgram& P, const ProgTabs& t, DevProg
   D.t_phase = p->d_tphase;
   D.has_xy = p->has_xy ? 1 : 0;
   D.t_coeff = p->d_tcoeff;
+  D.t_obs = p->d_tobs;
   D.n = P.n;
   D.k = P.k;
   D.R = P.R;
@@ -868,6 +871,7 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
       p->xmask.push_back((uint32_t)obs->x_masks[t]);
       p->tphase.push_back(ph);
       p->tcoeff.push_back(obs->coeffs[t]);
+      p->tobs.push_back((int32_t)m);
       if (obs->x_masks[t] != 0) p->has_xy = true;
     }
     p->term_offs[m + 1] = (int32_t)p->smask.size();
@@ -889,6 +893,7 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
   if (e == cudaSuccess) e = upload(p->xmask, &p->d_xmask);
   if (e == cudaSuccess) e = upload(p->tphase, &p->d_tphase);
   if (e == cudaSuccess) e = upload(p->tcoeff, &p->d_tcoeff);
+  if (e == cudaSuccess) e = upload(p->tobs, &p->d_tobs);
   if (e == cudaSuccess) e = upload(P.col_offs, &p->d_col_offs);
   if (e == cudaSuccess) e = upload(P.chain, &p->d_chain);
   if (e != cudaSuccess) {
@@ -958,6 +963,7 @@ void vqc_plan_destroy(VqcPlan* p) {
   cudaFree(p->d_xmask);
   cudaFree(p->d_tphase);
   cudaFree(p->d_tcoeff);
+  cudaFree(p->d_tobs);
   cudaFree(p->d_col_offs);
   cudaFree(p->d_chain);
   if (p->h_dev) cudaFree(p->h_dev);

@@ -42,6 +42,7 @@ struct DevProgram {
   const uint32_t* t_xmask;   // T flip masks (X/Y letters; nonzero only when has_xy)
   const int32_t* t_phase;    // T powers of i
   const double* t_coeff;     // T
+  const int32_t* t_obs;      // T observable index of each term
   int has_xy;                // any X/Y string (on-chip states only)
   int n, k, R, NG, n_rot, M, n_pass;
   int n_blk, n_av, max_rot_pass, max_blk_pass, max_av_pass;

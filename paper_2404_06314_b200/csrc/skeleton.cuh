@@ -24,9 +24,7 @@ __device__ __forceinline__ void stage_terms(const DevProgram& D, TermSm* s_terms
     ts.xmask = D.t_xmask[t];
     ts.phase = D.t_phase[t];
     ts.coeff = D.t_coeff[t];
-    int m = 0;
-    while (D.term_offs[m + 1] <= t) ++m;
-    ts.obs = m;
+    ts.obs = D.t_obs[t];
     s_terms[t] = ts;
   }
 }
