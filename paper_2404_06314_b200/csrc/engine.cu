@@ -555,7 +555,6 @@ int run_core(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, const
     A.expect = epart;
     A.ip = ipart;
     A.bra = -1;
-    A.pf_dist = 0;
     int rc;
     // per-sample angle / block tables of each program that runs
     RunArgs AF = A;  // forward sweep arguments
@@ -920,7 +919,7 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
     }
     p->use_jit = true;
     // separate forward schedule (VQC_FWD_TILE / VQC_FWD_REG) when it differs
-    const int ft = env_int("VQC_FWD_TILE", P.k), fr = std::max(3, std::min(4, env_int("VQC_FWD_REG", kHbmForwardRegs)));
+    const int ft = env_int("VQC_FWD_TILE", P.k), fr = std::max(3, std::min(5, env_int("VQC_FWD_REG", kHbmForwardRegs)));
     if (P.hbm && (ft != P.k || fr != P.R)) {
       ProgDev* f = new ProgDev();
       p->fwd = f;

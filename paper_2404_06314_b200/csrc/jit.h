@@ -32,9 +32,6 @@ std::string jit_compile_only(const HostProgram& P, bool split, double* seconds);
 // Generate, compile (NVRTC, sm_100a) and load. Returns "" on success.
 std::string jit_build(const HostProgram& P, bool split, JitKernels* out);
 
-// resident CTAs per SM of a JIT kernel at this block size / dynamic smem
-int jit_occupancy(CUfunction f, int block, size_t smem);
-
 // Driver-API launch of a JIT kernel with (DevProgram, RunArgs) arguments.
 struct DevProgram;
 struct RunArgs;

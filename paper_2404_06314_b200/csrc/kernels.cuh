@@ -77,7 +77,6 @@ struct RunArgs {
   unsigned long long* dbg; // VQC_DEBUG_TIMING: per-phase clock64 totals (thread 0 of each CTA)
   const double* tables;    // HBM mode: per-sample tables from k_tables (rows relative to b0)
   int64_t table_stride;    // doubles per sample
-  int64_t pf_dist;         // HBM passes: prefetch into L2 the tile of the CTA this many launch slots ahead (0 = off)
 };
 
 // phase timing (debug only): dbg[slot] += clock64 delta, slots fixed below

@@ -270,9 +270,6 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src)
   const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src) : "memory");
 }
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
-}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // One pass over HBM-resident states: CTA (tile, row) stages 2^k amplitudes.
@@ -325,20 +322,6 @@ __device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A)
       cp_async16(s_psi + sw, src + j);
       if (lphi) cp_async16(s_phi + sw, srcf + j);
     });
-    // warm L2 with the tile of the CTA that starts about one wave later (its
-    // loads then come from L2 while this CTA computes)
-    const int64_t nxt = ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) + A.pf_dist;
-    if (A.pf_dist > 0 && nxt < (int64_t)gridDim.x * gridDim.y) {
-      const uint32_t tb2 = PM::tile_dep(pd, D.n, (uint32_t)(nxt % gridDim.x));
-      const int64_t row2 = nxt / gridDim.x;
-      const double2* src2 = ((flags & F_LOAD_FIN) ? A.psi_fin : A.psi) + (size_t)row2 * N;
-      const double2* srcf2 = A.phi + (size_t)row2 * N;
-      const uint32_t dj = tile_base ^ tb2;
-      for_tile<OBS_E>(tw, [&](uint32_t sw, uint32_t j) {
-        prefetch_l2(src2 + (j ^ dj));
-        if (lphi) prefetch_l2(srcf2 + (j ^ dj));
-      });
-    }
   }
   if (A.tables != nullptr) {
     // per-sample tables precomputed by k_tables: copy this pass's slices
