@@ -230,7 +230,19 @@ class GpuWorkload:
         self.ws = torch.empty(self.plan.workspace_bytes(self.rows, native.VQC_MODE_VJP),
                               dtype=torch.uint8, device=dev)
         self.native = native
-        self.up_host = np.ones((self.rows, self.M))
+
+        # e2e host buffers in pinned (page-locked) memory: inputs, upstream and
+        # the step's results (expectations, per-row VJP rows, weight VJP)
+        def pinned(shape):
+            return torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
+
+        xh = pinned(self.x_host.shape)
+        xh[...] = self.x_host
+        self.x_host = xh
+        self.up_host = pinned((self.rows, self.M))
+        self.up_host[...] = 1.0
+        self.out_host = (pinned((self.rows, self.M)), pinned((self.rows, self.layout.n_cols)),
+                         pinned((self.layout.n_cols,)))
 
     def step(self, world: int):
         stream = self.torch.cuda.current_stream(self.dev).cuda_stream
@@ -242,7 +254,8 @@ class GpuWorkload:
         return launches
 
     def step_host(self, world: int):
-        e, _, rows, vsum = self.plan.run_batch_host(self.x_host, self.flat, upstream=self.up_host)
+        e, _, rows, vsum = self.plan.run_batch_host(self.x_host, self.flat, upstream=self.up_host,
+                                                    out=self.out_host)
         if world > 1:
             t = self.torch.from_numpy(vsum).to(self.dev)
             self.torch.distributed.all_reduce(t)
@@ -350,7 +363,7 @@ def measure_gpu(spec, args, rank, world, device, flush_buf, with_e2e: bool, step
         h2d, d2h = wl.e2e_bytes()
         res["e2e"] = {"value": spec.batch / e2e_s, "unit": "samples/s", "h2d_bytes_per_step": h2d,
                       "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
-                      "path": "vqc_run_batch_host (numpy in/out, pageable host buffers)"}
+                      "path": "vqc_run_batch_host (numpy in/out, pinned host buffers)"}
     res["plan"] = json.loads(wl.plan.describe())
     del wl
     torch.cuda.empty_cache()

@@ -191,16 +191,22 @@ class Plan:
                "vqc_adjoint")
 
     def run_batch_host(self, inputs: np.ndarray, weights: np.ndarray, upstream=None,
-                       jacobian: bool = False):
-        """numpy in / numpy out through vqc_run_batch_host (H2D + run + D2H)."""
+                       jacobian: bool = False, out=None):
+        """numpy in / numpy out through vqc_run_batch_host (H2D + run + D2H).
+        ``out``: optional preallocated (expect, rows, vsum) arrays (e.g. views of
+        pinned host memory)."""
         inputs = _f64(inputs)
         weights = _f64(weights)
         B = inputs.shape[0]
         M, C = self.num_obs, self.num_cols
-        expect = np.empty((B, M))
-        jac = np.empty((B, M, C)) if jacobian else None
-        rows = np.empty((B, C)) if upstream is not None else None
-        vsum = np.empty(C) if upstream is not None else None
+        if out is not None:
+            expect, rows, vsum = out
+            jac = None
+        else:
+            expect = np.empty((B, M))
+            jac = np.empty((B, M, C)) if jacobian else None
+            rows = np.empty((B, C)) if upstream is not None else None
+            vsum = np.empty(C) if upstream is not None else None
         up = _f64(upstream) if upstream is not None else None
 
         def p(a):
