@@ -370,6 +370,46 @@ def measure_gpu(spec, args, rank, world, device, flush_buf, with_e2e: bool, step
     return res
 
 
+def measure_jacobian(spec, rows: int, device: str) -> dict:
+    """Jacobian mode (reference run_batch semantics: one adjoint sweep per
+    observable, (B, M, cols) output), device-timed; SURVEY §8d asks for it on
+    cfg2 / cfg4 next to the VJP headline."""
+    import torch
+
+    from paper_2404_06314_b200 import configs, native
+    from paper_2404_06314_b200.engine import BatchEngine
+    circ, obs, wrt = configs.build(spec, configs.native_api())
+    x, w = configs.inputs_and_weights(spec, batch=rows or spec.batch)
+    eng = BatchEngine(device=device)
+    dev = torch.device(device)
+    plan, layout = eng.plans.get(circ, obs, wrt, dev)
+    flat = eng.base_flat(circ, {"w": w})
+    B, M, C = len(x), len(obs), layout.n_cols
+    d_x, d_w = torch.from_numpy(x).to(dev), torch.from_numpy(flat).to(dev)
+    e = torch.empty((B, M), dtype=torch.float64, device=dev)
+    j = torch.empty((B, M, C), dtype=torch.float64, device=dev)
+    ws = torch.empty(plan.workspace_bytes(B, native.VQC_MODE_JACOBIAN), dtype=torch.uint8, device=dev)
+    st = torch.cuda.current_stream().cuda_stream
+    plan.adjoint(d_x, d_w, None, e, j, None, None, ws, st)
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 3
+    t0.record()
+    for _ in range(reps):
+        plan.adjoint(d_x, d_w, None, e, j, None, None, ws, st)
+    t1.record()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / reps
+    peak, _ = fp64_peak()
+    flops = configs.flops_per_sample(spec, K=M) * B
+    out = {"config": workload_desc(spec).replace("VJP grads", "Jacobians"), "rows": B, "ms_per_call": ms,
+           "value": B / (ms * 1e-3), "unit": "samples/s",
+           "roofline_frac_fp64": flops / (ms * 1e-3) / 1e12 / peak}
+    del ws, j
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args, spec):
     import torch
     import torch.distributed as dist
@@ -394,6 +434,10 @@ def run_ours(args, spec):
                           "roofline_frac_fp64": r["roofline"]["frac"],
                           "achieved_tflops": r["roofline"]["achieved"],
                           "kernels": r["kernels"], "plan": r["plan"]})
+    jac = []
+    if world == 1 and not args.no_sweep:
+        for cid, rows in ((2, 0), (4, 2048)):
+            jac.append(measure_jacobian(configs.CONFIGS[cid], rows, device))
     line = None
     if rank == 0:
         cpu = None
@@ -416,6 +460,8 @@ def run_ours(args, spec):
         }
         if sweep:
             line["sweep"] = sweep
+        if jac:
+            line["jacobian_mode"] = jac
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
