@@ -685,6 +685,7 @@ int schedule_circuit(const VqcCircuit* c, const int64_t* wrt_col, HostProgram* p
   opt.tile_qubits = env_int("VQC_TILE_QUBITS", 11);
   opt.segment_cost = env_int("VQC_SEGMENT_COST", 4);
   opt.variants = std::max(1, env_int("VQC_SCHED_VARIANTS", 1));
+  opt.forced_low = std::max(0, std::min(3, env_int("VQC_FORCED_LOW", 3)));  // contiguous low qubits per pass
   // four register slots (16 amplitudes per thread); the scheduler and its
   // CPU checker also handle 3 and 5 (tests/test_scheduler_sim.py). Other
   // values (VQC_REG_SLOTS) only for JIT-compiled HBM plans: the prebuilt
