@@ -191,6 +191,13 @@ int sim_run(int n, int64_t G, const int64_t* kinds, const int64_t* q0, const int
   opt.tile_qubits = tile_qubits;
   opt.smem_max_qubits = smem_max_qubits;
   opt.reg_slots = reg_slots;
+  // as vqc_plan_create: trailing CNOT / CZ / X gates fold into the (Z-string)
+  // observables, which the expectation step below then uses
+  const int64_t T = M > 0 ? term_offs[M] : 0;
+  std::vector<uint32_t> zm(T);
+  std::vector<double> zc(t_coeff, t_coeff + T);
+  for (int64_t t = 0; t < T; ++t) zm[t] = (uint32_t)t_smask[t];
+  absorb_trailing_gates(&gates, n, &zm, &zc);
   HostProgram P;
   std::string e = build_program(gates, n, total_params, wc, opt, &P);
   if (e.empty()) e = check_program(P, opt);
@@ -318,7 +325,7 @@ int sim_run(int n, int64_t G, const int64_t* kinds, const int64_t* q0, const int
   }
   auto zw = [&](size_t j, int lo, int hi) {
     double w = 0;
-    for (int t = lo; t < hi; ++t) w += (__builtin_popcountll(j & (size_t)t_smask[t]) & 1) ? -t_coeff[t] : t_coeff[t];
+    for (int t = lo; t < hi; ++t) w += (__builtin_popcountll(j & (size_t)zm[t]) & 1) ? -zc[t] : zc[t];
     return w;
   };
   for (int m = 0; m < M; ++m) {
