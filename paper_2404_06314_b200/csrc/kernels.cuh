@@ -374,6 +374,18 @@ __device__ __forceinline__ void g_czrun(double2 (&a)[1 << R], uint32_t qreg, uin
 __device__ __forceinline__ void put_partial(double* redbuf, int slot, double v) {
   redbuf[slot * blockDim.x + threadIdx.x] = v;
 }
+// lagged JIT reductions: lanes 2i, 2i+1 add their partials first and one half
+// row (blockDim/2 entries) per slot is written, so two segments' partial
+// buffers fit in the space of one (jred_phase1)
+template <bool PAIR>
+__device__ __forceinline__ void put_part(double* redbuf, int slot, double v) {
+  if constexpr (PAIR) {
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    if (!(threadIdx.x & 1u)) redbuf[slot * (blockDim.x >> 1) + (threadIdx.x >> 1)] = v;
+  } else {
+    put_partial(redbuf, slot, v);
+  }
+}
 
 // compile-time slot from an unrolled loop index (no branch after unrolling)
 template <int R, typename F>
@@ -529,7 +541,7 @@ __device__ __forceinline__ void jop_czsign(Regs<R>& a, Regs<R>& f, uint32_t qreg
 }
 
 // inner products: partial sums into reduction slots (adjoint modes only)
-template <int R, int MODE, int S>
+template <int R, int MODE, int S, bool PAIR = false>
 __device__ __forceinline__ void jop_ip3(const SegCtx<R>& C, const Regs<R>& a, const Regs<R>& f, int role,
                                         double* s_red, int r0) {
   if constexpr (MODE != MODE_FWD) {
@@ -537,13 +549,13 @@ __device__ __forceinline__ void jop_ip3(const SegCtx<R>& C, const Regs<R>& a, co
     ip_dispatch<R, MODE>(C, a, f, role, [&](auto PART, auto&& p, auto&& q) {
       ip_xyz<R, S, PART.value>(p, q, ix, iy, iz);
     });
-    put_partial(s_red, r0, ix);
-    put_partial(s_red, r0 + 1, iy);
-    put_partial(s_red, r0 + 2, iz);
+    put_part<PAIR>(s_red, r0, ix);
+    put_part<PAIR>(s_red, r0 + 1, iy);
+    put_part<PAIR>(s_red, r0 + 2, iz);
   }
 }
 // KIND: 0 = X, 1 = Y on slot S
-template <int R, int MODE, int KIND, int S>
+template <int R, int MODE, int KIND, int S, bool PAIR = false>
 __device__ __forceinline__ void jop_ipxy(const SegCtx<R>& C, const Regs<R>& a, const Regs<R>& f, int role,
                                          double* s_red, int r) {
   if constexpr (MODE != MODE_FWD) {
@@ -552,10 +564,10 @@ __device__ __forceinline__ void jop_ipxy(const SegCtx<R>& C, const Regs<R>& a, c
       if constexpr (KIND == 0) v = ip_x<R, S, PART.value>(p, q);
       else v = ip_y<R, S, PART.value>(p, q);
     });
-    put_partial(s_red, r, v);
+    put_part<PAIR>(s_red, r, v);
   }
 }
-template <int R, int MODE>
+template <int R, int MODE, bool PAIR = false>
 __device__ __forceinline__ void jop_ipz(const SegCtx<R>& C, const Regs<R>& a, const Regs<R>& f, int role,
                                         double* s_red, int r, uint32_t m, bool cb) {
   if constexpr (MODE != MODE_FWD) {
@@ -563,7 +575,7 @@ __device__ __forceinline__ void jop_ipz(const SegCtx<R>& C, const Regs<R>& a, co
     ip_dispatch<R, MODE>(C, a, f, role, [&](auto PART, auto&& p, auto&& q) {
       v = ip_z<R, PART.value>(p, q, m, cb);
     });
-    put_partial(s_red, r, v);
+    put_part<PAIR>(s_red, r, v);
   }
 }
 
@@ -581,15 +593,15 @@ __device__ __forceinline__ void jop_u2set(Regs<R>& a, Regs<R>& f, const SampleTa
 
 // Im<phi|X,Y,Z|psi> on every slot of MASK; reduction slots r0, r0 + 3, ... in
 // slot order. The split-role branch is taken once for the whole set.
-template <int R, int PART, int MASK, class P, class F>
+template <int R, int PART, int MASK, bool PAIR, class P, class F>
 __device__ __forceinline__ void ip3set_part(P&& p, F&& q, double* s_red, int r0) {
   auto one = [&](auto SL, int r) {
     if constexpr (SL.value < R && ((MASK >> SL.value) & 1) != 0) {
       double ix = 0.0, iy = 0.0, iz = 0.0;
       ip_xyz<R, SL.value, PART>(p, q, ix, iy, iz);
-      put_partial(s_red, r, ix);
-      put_partial(s_red, r + 1, iy);
-      put_partial(s_red, r + 2, iz);
+      put_part<PAIR>(s_red, r, ix);
+      put_part<PAIR>(s_red, r + 1, iy);
+      put_part<PAIR>(s_red, r + 2, iz);
     }
   };
   one(IC<0>{}, r0);
@@ -598,12 +610,12 @@ __device__ __forceinline__ void ip3set_part(P&& p, F&& q, double* s_red, int r0)
   one(IC<3>{}, r0 + 3 * popc_const(MASK & 7));
   one(IC<4>{}, r0 + 3 * popc_const(MASK & 15));
 }
-template <int R, int MODE, int MASK>
+template <int R, int MODE, int MASK, bool PAIR = false>
 __device__ __forceinline__ void jop_ip3set(const SegCtx<R>& C, const Regs<R>& a, const Regs<R>& f, int role,
                                            double* s_red, int r0) {
   if constexpr (MODE != MODE_FWD) {
     ip_dispatch<R, MODE>(C, a, f, role, [&](auto PART, auto&& p, auto&& q) {
-      ip3set_part<R, PART.value, MASK>(p, q, s_red, r0);
+      ip3set_part<R, PART.value, MASK, PAIR>(p, q, s_red, r0);
     });
   }
 }
@@ -853,7 +865,7 @@ __device__ __forceinline__ void seg_publish(const SegEnv& E, const SegCtx<R>& C,
 
 // segment end: register store (through the folded store map), barrier, and the
 // segment's gradient outputs
-template <int R, int MODE, class SD>
+template <int R, int MODE, bool REDUCE = true, class SD>
 __device__ __forceinline__ void seg_end(const SegEnv& E, const SD& sd, const Regs<R>& a, const Regs<R>& f) {
   constexpr int N = 1 << R;
   const Group& grp = E.grp;
@@ -887,7 +899,7 @@ __device__ __forceinline__ void seg_end(const SegEnv& E, const SD& sd, const Reg
     }
   }
   __syncthreads();
-  if constexpr (MODE != MODE_FWD) {
+  if constexpr (MODE != MODE_FWD && REDUCE) {
     const int nout = sd.ip_count();
     if (nout > 0) {
       // phase 1: one warp per (reduction slot, sample) sums the sample's
@@ -927,6 +939,42 @@ __device__ __forceinline__ void seg_end(const SegEnv& E, const SD& sd, const Reg
         if (bl < A.nb) A.ip[(((bl * A.K) + E.bra) * E.D.NG + io.gslot) * E.n_tiles + E.tile] = v;
       }
     }
+  }
+}
+
+// Lagged segment reductions (JIT, one sample per CTA): after segment s's
+// post-store barrier run phase 2 of the previous inner-product segment (its
+// outputs from s_fin) and phase 1 of segment s (one warp per slot over the
+// pair-reduced partial rows, into the other s_fin buffer). Partial rows and
+// s_fin alternate between segments and the next post-store barrier orders
+// every reuse, so the reduction needs no barrier of its own.
+__device__ __forceinline__ void jred_phase1(const SegEnv& E, int slot0, int nred, int fin0) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int W = (int)(blockDim.x >> 1);
+  for (int s = warp; s < nred; s += nwarp) {
+    const double* base = E.s_red + (slot0 + s) * W;
+    double v = 0.0;
+    for (int t = lane; t < W; t += 32) v += base[t];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if (lane == 0) E.s_fin[fin0 + s] = v;
+  }
+}
+template <class SD>
+__device__ __forceinline__ void jred_phase2(const SegEnv& E, const SD& sd, int fin0) {
+  const RunArgs& A = E.A;
+  for (int oi = threadIdx.x; oi < sd.ip_count(); oi += blockDim.x) {
+    const IpOut io = E.D.ipouts[sd.ip_begin() + oi];
+    const double* r = E.s_fin + fin0;
+    double v;
+    if (io.avec < 0) {
+      v = r[io.red];
+    } else {
+      const double* av = E.s_av_all + 4 * (io.avec - E.av_base);
+      v = av[0] * r[io.red] + av[1] * r[io.red + 1] + av[2] * r[io.red + 2];
+    }
+    const int64_t bl = E.bl0;
+    if (bl < A.nb) A.ip[(((bl * A.K) + E.bra) * E.D.NG + io.gslot) * E.n_tiles + E.tile] = v;
   }
 }
 

@@ -167,7 +167,7 @@ struct SmemLayout {
     u = o; o += (size_t)S * nblk * 64;
     av = o; o += (size_t)S * nav * 32;
     red = o; o += (size_t)red_slots * threads * 8;
-    fin = o; o += (size_t)red_slots * S * 8;
+    fin = o; o += (size_t)2 * red_slots * S * 8;  // two buffers (lagged JIT reductions)
     up = o; o += (size_t)S * M * 8;
     terms = o; o += (size_t)n_terms * sizeof(TermSm);
     total = o + 16;
