@@ -111,6 +111,9 @@ bool use_split(int n, int R) { return (n - R) >= 5; }
 // segment), the forward sweep its own 4-slot schedule (measured on cfg4:
 // adjoint 630 -> 559 ms, forward 191 ms kept; r01 knob sweep in DESIGN.md)
 constexpr int kHbmAdjointRegs = 3;
+// on-chip plans up to this size take their per-sample tables from k_tables
+// (few threads per sample would build them through serial global loads)
+constexpr int kSmemTablesMaxN = 10;
 constexpr int kHbmForwardRegs = 4;
 
 // Plans use R = min(4, n) register slots (schedule_circuit), so only these
@@ -366,6 +369,13 @@ Layout make_layout(const VqcPlan* p, int64_t B, int mode) {
   if (!P.hbm) {
     L.chunk = B;
     L.fin = take(mode == VQC_MODE_JACOBIAN && M > 1 ? (size_t)B * N * 16 : 0);
+    // small on-chip states: per-sample tables from k_tables (one CTA per sample,
+    // rotations in parallel) instead of a serial dependent-load chain per CTA
+    const int64_t st = 2 * (int64_t)P.n_rot + 8 * (int64_t)P.n_blk + 4 * (int64_t)P.n_av;
+    if (P.n <= kSmemTablesMaxN && st > 0 && st * 8 <= 160 * 1024) {
+      L.table_stride = st;
+      L.tables = take((size_t)B * st * 8);
+    }
   } else {
     L.n_tiles = 1 << (P.n - P.k);
     const int nstates = mode == VQC_MODE_FORWARD ? 1 : (mode == VQC_MODE_VJP ? 2 : 3);
@@ -524,6 +534,15 @@ int run_core(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, const
     A.ip = ip;
     A.psi_fin = reinterpret_cast<double2*>(ws + L.fin);
     A.jacobian = mode == VQC_MODE_JACOBIAN;
+    A.tables = nullptr;
+    A.table_stride = 0;
+    if (L.table_stride > 0 && B > 0) {
+      A.tables = reinterpret_cast<double*>(ws + L.tables);
+      A.table_stride = L.table_stride;
+      if (int rc = launch("tables", Kern{k_tables, nullptr}, dim3((unsigned)B), dim3(256),
+                          (size_t)L.table_stride * 8, st, D, A))
+        return rc;
+    }
     const dim3 grid((unsigned)((B + S - 1) / S)), block((unsigned)(S * TT));
     return launch(adj ? "smem_fwd_adjoint" : "smem_forward", smem_k(p, adj), grid,
                   block, smem, st, D, A);

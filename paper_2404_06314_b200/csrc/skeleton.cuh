@@ -230,7 +230,19 @@ __device__ __forceinline__ void smem_body(const DevProgram& D, const RunArgs& A)
   for (int l = lane; l < N; l += grp.TT) s_psi[swz((uint32_t)l)] = make_double2(l == 0 ? 1.0 : 0.0, 0.0);
   if (ADJ && A.upstream != nullptr)
     for (int m = lane; m < D.M; m += grp.TT) s_up[grp.sl * D.M + m] = valid ? A.upstream[b * D.M + m] : 0.0;
-  build_tables(D, A, pd, b, valid, s_cs, s_u, s_av_all + (size_t)grp.sl * nav * 4, lane, grp.TT);
+  if (A.tables != nullptr) {
+    // per-sample tables precomputed by k_tables: [cs | u | av] of this sample
+    const double* t = A.tables + (size_t)(valid ? bl : 0) * A.table_stride;
+    double* dcs = reinterpret_cast<double*>(s_cs);
+    double* du = reinterpret_cast<double*>(s_u);
+    double* dav = s_av_all + (size_t)grp.sl * nav * 4;
+    for (int i = lane; i < 2 * nrot; i += grp.TT) dcs[i] = t[i];
+    for (int i = lane; i < 8 * nblk; i += grp.TT) du[i] = t[2 * nrot + i];
+    for (int i = lane; i < 4 * nav; i += grp.TT) dav[i] = t[2 * nrot + 8 * nblk + i];
+    __syncthreads();
+  } else {
+    build_tables(D, A, pd, b, valid, s_cs, s_u, s_av_all + (size_t)grp.sl * nav * 4, lane, grp.TT);
+  }
   const SampleTables T{s_cs, s_u, 0, 0};
 
   SEGS::template run<R, MODE_FWD>(make_env<MODE_FWD>(D, A, s_psi, s_psi, s_av_all, nav * 4, 0, s_red, s_fin,
