@@ -65,3 +65,14 @@ def test_cubin_cache_round_trip(tmp_path, monkeypatch):
     _, t2 = _src(circ, ("a", "b", "s"), compile=True)
     assert n_files >= 1 and len(list(tmp_path.glob("*.cubin"))) == n_files
     assert t2 < t1
+
+
+def test_unusable_cache_dir_still_compiles(tmp_path, monkeypatch):
+    """A cache path that cannot be a directory only costs the cache."""
+    blocker = tmp_path / "not_a_dir"
+    blocker.write_text("x")
+    monkeypatch.setenv("VQC_JIT_CACHE", str(blocker / "sub"))
+    from test_scheduler_sim import _random
+    circ, _, _ = _random(np.random.default_rng(5), 13, 20)
+    src, secs = _src(circ, ("a", "b", "s"), compile=True)
+    assert secs is not None and "vqc_jit_pa0" in src
