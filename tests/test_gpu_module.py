@@ -44,6 +44,23 @@ def test_autograd_matches_oracle(torch, cfg_id):
     assert close(xt.grad.cpu().numpy(), np.einsum("bm,bmf->bf", up, j_ref["x"])) < TOL
 
 
+def test_autograd_hbm_plan_matches_oracle(torch):
+    """cfg4 (16 qubits: HBM passes, separate forward / adjoint schedules) through
+    the autograd node with a row-dependent upstream."""
+    from paper_2404_06314_b200 import configs
+    spec, circ, obs, mod = _module(4)
+    x, _ = configs.inputs_and_weights(spec, batch=4)
+    w = mod.parameter_values()["w"]
+    xt = torch.from_numpy(x).cuda().requires_grad_(True)
+    out = mod(xt)
+    up = np.random.default_rng(4).normal(size=out.shape)
+    out.backward(torch.from_numpy(up).cuda())
+    e_ref, j_ref = oracle_batch(circ, obs, {"w": w}, x, ("w", "x"))
+    assert close(out.detach().cpu().numpy(), e_ref) < TOL
+    assert close(mod.values["w"].grad.cpu().numpy(), np.einsum("bm,bmp->p", up, j_ref["w"])) < TOL
+    assert close(xt.grad.cpu().numpy(), np.einsum("bm,bmf->bf", up, j_ref["x"])) < TOL
+
+
 def test_reference_style_backward_and_jacobians(torch):
     # model.py:644-662: backward == einsum over the Jacobian slices
     from paper_2404_06314_b200 import configs
