@@ -189,3 +189,91 @@ def expval(state: np.ndarray, coeffs, x_masks, sign_masks, phases) -> complex:
 def vjp(upstream: np.ndarray, jac: np.ndarray) -> np.ndarray:
     """model.py:141-142 / engine_server.py:135-136 contraction, per row."""
     return np.einsum("bm,bmp->bp", upstream, jac)
+
+
+# -- shift-rule and SPSA gradients (gradients.py:121-201), small cases only ----
+
+def _angles(low: Lowered, flat) -> np.ndarray:
+    """compute_angles (_kernels.py:128-134): coefficient first, factors in order."""
+    out = np.zeros(len(low.kinds))
+    for g in range(len(low.kinds)):
+        a = low.coeff[g]
+        for t in range(low.f_offs[g], low.f_offs[g + 1]):
+            a *= flat[low.f_idx[t]]
+        out[g] = a
+    return out
+
+
+def _run_angles(low: Lowered, angles) -> np.ndarray:
+    """run_program on explicit per-gate angles (circuit.py:229-245)."""
+    st = np.zeros(1 << low.n_qubits, np.complex128)
+    st[0] = 1.0
+    for g in range(len(low.kinds)):
+        st = apply_gate(st, int(low.kinds[g]), int(low.q0[g]), int(low.q1[g]), float(angles[g]))
+    return st
+
+
+def _pack_expectations(low: Lowered, st) -> np.ndarray:
+    """pack_expectations (gradients.py:84-99)."""
+    out = np.empty(low.n_obs)
+    for m in range(low.n_obs):
+        lo, hi = low.term_offs[m], low.term_offs[m + 1]
+        out[m] = expval(st, low.t_coeffs[lo:hi], low.t_xmask[lo:hi], low.t_smask[lo:hi],
+                        np.asarray(low.t_phases).reshape(-1, 2)[lo:hi]).real
+    return out
+
+
+def param_shift_row(low: Lowered, flat, wrt_col):
+    """param_shift_flat (gradients.py:137-160) for one row: (expect (M,), grad (M, n_cols))."""
+    flat = np.asarray(flat, np.float64)
+    n_cols = int(np.max(wrt_col, initial=-1)) + 1
+    angles = _angles(low, flat)
+    expect = _pack_expectations(low, _run_angles(low, angles))
+    grad = np.zeros((low.n_obs, n_cols))
+    for g in range(len(low.kinds)):
+        if low.gen_axis[g] < 0:
+            continue
+        lo, hi = low.f_offs[g], low.f_offs[g + 1]
+        partials = []
+        for t in range(lo, hi):                       # _occurrence_partials (121-134)
+            col = wrt_col[low.f_idx[t]]
+            if col < 0:
+                continue
+            partial = low.coeff[g]
+            for u in range(lo, hi):
+                if u != t:
+                    partial *= flat[low.f_idx[u]]
+            partials.append((int(col), float(partial)))
+        if not partials:
+            continue
+        base = angles[g]
+        angles[g] = base + 0.5 * np.pi
+        f_plus = _pack_expectations(low, _run_angles(low, angles))
+        angles[g] = base - 0.5 * np.pi
+        f_minus = _pack_expectations(low, _run_angles(low, angles))
+        angles[g] = base
+        occ = 0.5 * (f_plus - f_minus)
+        for col, partial in partials:
+            grad[:, col] += occ * partial
+    return expect, grad
+
+
+def spsa_row(low: Lowered, flat, flat_of_col, c: float, samples: int, rng):
+    """spsa_flat (gradients.py:180-201) for one row; ``rng`` is the row's
+    default_rng(mix_seed(seed, b)) (batch.py:197)."""
+    flat = np.array(flat, np.float64)
+    idx = np.asarray(flat_of_col, np.int64)
+    expect = _pack_expectations(low, _run_angles(low, _angles(low, flat)))
+    grad = np.zeros((low.n_obs, len(idx)))
+    base = flat[idx].copy()
+    for _ in range(samples):
+        delta = rng.integers(0, 2, size=len(idx)).astype(np.float64)
+        delta = 2.0 * delta - 1.0
+        flat[idx] = base + c * delta
+        f_plus = _pack_expectations(low, _run_angles(low, _angles(low, flat)))
+        flat[idx] = base - c * delta
+        f_minus = _pack_expectations(low, _run_angles(low, _angles(low, flat)))
+        flat[idx] = base
+        grad += np.outer(f_plus - f_minus, 1.0 / (2.0 * c * delta))
+    grad /= samples
+    return expect, grad

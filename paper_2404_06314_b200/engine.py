@@ -19,8 +19,11 @@ from .ir import Circuit
 from .observables import Observable, ObservablePack
 
 METHODS = ("adjoint", "param-shift", "spsa")
-GPU_METHODS = ("adjoint",)
+GPU_METHODS = METHODS
 _MASK64 = (1 << 64) - 1
+# rows of angle vectors per forward launch in the shift/SPSA paths (bounds the
+# (rows, R) f64 input block and the (rows, M) result block)
+SHIFT_CHUNK_ROWS = 1 << 18
 
 
 def split_workload(batch_size: int, parts: int) -> list[tuple[int, int]]:
@@ -114,6 +117,41 @@ def encoding_set(circuit: Circuit):
     return enc[0]
 
 
+def angle_circuit(circuit: Circuit):
+    """The circuit with every rotation's angle made a direct input: one
+    encoding set ``angles`` of size R, rotation r = 1.0 * angles[r]. Running
+    it forward on rows of per-gate angles is how the shift / SPSA methods
+    batch their shifted evaluations onto the GPU forward kernel. Returns
+    (circuit, rotation gate indices); cached on the source circuit."""
+    from .ir import AngleExpression, Gate, ParameterSet
+    cached = circuit.__dict__.get("_angle_circuit")
+    if cached is None:
+        rot = [g for g, gate in enumerate(circuit.gates) if gate.expr is not None]
+        slot = {g: r for r, g in enumerate(rot)}
+        gates = tuple(
+            Gate(gate.kind, gate.qubits, AngleExpression(1.0, (("angles", slot[g]),)))
+            if gate.expr is not None else gate
+            for g, gate in enumerate(circuit.gates))
+        ac = Circuit(circuit.num_qubits, gates,
+                     (ParameterSet("angles", len(rot), "encoding"),))
+        cached = (ac, np.asarray(rot, np.int64))
+        object.__setattr__(circuit, "_angle_circuit", cached)
+    return cached
+
+
+def row_angles(compiled, flats: np.ndarray, rot: np.ndarray) -> np.ndarray:
+    """angle_g = coeff_g * prod factors (compute_angles, _kernels.py:128-134)
+    for every row of ``flats`` (rows, total_params) -> (rows, R), factors
+    multiplied in declaration order like the reference."""
+    out = np.empty((flats.shape[0], len(rot)))
+    for r, g in enumerate(rot):
+        a = np.full(flats.shape[0], compiled.coeff[g])
+        for t in range(compiled.f_offs[g], compiled.f_offs[g + 1]):
+            a = a * flats[:, compiled.f_idx[t]]
+        out[:, r] = a
+    return out
+
+
 def _device(device):
     import torch
     if device is None:
@@ -202,9 +240,6 @@ class BatchEngine:
         circuit = request.circuit
         if request.method not in METHODS:
             raise ValueError(f"unknown method {request.method!r}; expected one of {METHODS}")
-        if request.method not in GPU_METHODS:
-            raise NotImplementedError(f"method {request.method!r} is not on the GPU path "
-                                      "(adjoint only)")
         enc = encoding_set(circuit)
         inputs = np.asarray(request.inputs, dtype=np.float64)
         if inputs.ndim != 2 or inputs.shape[1] != enc.size:
@@ -220,6 +255,11 @@ class BatchEngine:
                                {n: np.ascontiguousarray(grad[:, :, lo:hi])
                                 for n, lo, hi in layout.slices})
         dev = self.device
+        if C > 0 and request.method != "adjoint":
+            expect_h, grad_h = self._run_shifted(request, circuit, observables, layout,
+                                                 flat, inputs)
+            return BatchResult(expect_h, {n: np.ascontiguousarray(grad_h[:, :, lo:hi])
+                                          for n, lo, hi in layout.slices})
         plan, _ = self.plans.get(circuit, observables, tuple(request.wrt), dev)
         with torch.cuda.device(dev):
             stream = torch.cuda.current_stream(dev)
@@ -238,6 +278,103 @@ class BatchEngine:
             jac_h = jac.cpu().numpy() if jac is not None else np.zeros((B, M, 0))
         return BatchResult(expect_h, {n: np.ascontiguousarray(jac_h[:, :, lo:hi])
                                       for n, lo, hi in layout.slices})
+
+
+    def forward_angle_rows(self, circuit: Circuit, observables, angles: np.ndarray) -> np.ndarray:
+        """Expectations (rows, M) of ``circuit`` with per-row rotation angles
+        (rows, R): one GPU forward launch sequence over ``angle_circuit``."""
+        import torch
+        ac, _ = angle_circuit(circuit)
+        dev = self.device
+        plan, _ = self.plans.get(ac, observables, (), dev)
+        rows, M = angles.shape[0], len(observables)
+        with torch.cuda.device(dev):
+            stream = torch.cuda.current_stream(dev)
+            d_in = torch.from_numpy(np.ascontiguousarray(angles)).to(dev)
+            d_w = torch.zeros(max(1, angles.shape[1]), dtype=torch.float64, device=dev)
+            expect = torch.empty((rows, M), dtype=torch.float64, device=dev)
+            ws = self.workspace.get(plan.workspace_bytes(rows, native.VQC_MODE_FORWARD), dev)
+            plan.forward(d_in, d_w, expect, ws, stream.cuda_stream)
+            return expect.cpu().numpy()
+
+    def _run_shifted(self, request, circuit, observables, layout, flat, inputs):
+        """param-shift (gradients.py:137-160) and SPSA (gradients.py:180-201)
+        as batched GPU forward evaluations. Each row's shifted / perturbed
+        evaluations become extra rows of per-gate angles (computed on the host
+        in the reference's arithmetic order), so a chunk of B rows is one
+        forward call over B*(1+2S) angle rows; the finite differences and the
+        chain rule through the angle expressions are host arithmetic in the
+        reference's accumulation order."""
+        compiled = circuit.compiled()
+        enc = encoding_set(circuit)
+        off, size = compiled.offsets[enc.name]
+        _, rot = angle_circuit(circuit)
+        B, M, C = inputs.shape[0], len(observables), layout.n_cols
+        expect = np.empty((B, M))
+        grad = np.zeros((B, M, C))
+        f_offs, f_idx, wrt_col = compiled.f_offs, compiled.f_idx, layout.wrt_col
+        if request.method == "param-shift":
+            # rotation slots with a requested factor (row-independent) and,
+            # per slot, (column, factor positions of the other factors)
+            shifted, partials = [], []
+            for r, g in enumerate(rot):
+                terms = []
+                for t in range(f_offs[g], f_offs[g + 1]):
+                    col = wrt_col[f_idx[t]]
+                    if col >= 0:
+                        terms.append((int(col), [f_idx[u] for u in range(f_offs[g], f_offs[g + 1])
+                                                 if u != t]))
+                if terms:
+                    shifted.append(r)
+                    partials.append((g, terms))
+            per_row = 1 + 2 * len(shifted)
+        else:
+            if request.spsa_samples < 1:
+                raise ValueError(f"spsa_samples must be >= 1, got {request.spsa_samples}")
+            per_row = 1 + 2 * request.spsa_samples
+        step = max(1, SHIFT_CHUNK_ROWS // per_row)
+        for lo in range(0, B, step):
+            hi = min(B, lo + step)
+            n = hi - lo
+            flats = np.repeat(flat[None], n, 0)
+            flats[:, off:off + size] = inputs[lo:hi]
+            if request.method == "param-shift":
+                base = row_angles(compiled, flats, rot)                 # (n, R)
+                rows = np.repeat(base[:, None], per_row, 1)             # (n, 1+2S, R)
+                for s, r in enumerate(shifted):
+                    rows[:, 1 + 2 * s, r] = base[:, r] + 0.5 * np.pi
+                    rows[:, 2 + 2 * s, r] = base[:, r] - 0.5 * np.pi
+                e = self.forward_angle_rows(circuit, observables,
+                                            rows.reshape(n * per_row, -1)).reshape(n, per_row, M)
+                expect[lo:hi] = e[:, 0]
+                for s, (g, terms) in enumerate(partials):
+                    occ = 0.5 * (e[:, 1 + 2 * s] - e[:, 2 + 2 * s])    # (n, M)
+                    for col, others in terms:
+                        partial = np.full(n, compiled.coeff[g])
+                        for p in others:
+                            partial = partial * flats[:, p]
+                        grad[lo:hi, :, col] += occ * partial[:, None]
+            else:
+                K, c, idx = request.spsa_samples, request.spsa_c, layout.flat_of_col
+                deltas = np.empty((n, K, C))
+                for i in range(n):
+                    rng = np.random.default_rng(mix_seed(request.seed, lo + i))
+                    for k in range(K):
+                        d = rng.integers(0, 2, size=C).astype(np.float64)
+                        deltas[i, k] = 2.0 * d - 1.0
+                pf = np.repeat(flats[:, None], per_row, 1)              # (n, 1+2K, P)
+                base = flats[:, idx]
+                pf[:, 1::2][:, :, idx] = base[:, None] + c * deltas
+                pf[:, 2::2][:, :, idx] = base[:, None] - c * deltas
+                ang = row_angles(compiled, pf.reshape(n * per_row, -1), rot)
+                e = self.forward_angle_rows(circuit, observables, ang).reshape(n, per_row, M)
+                expect[lo:hi] = e[:, 0]
+                g_acc = np.zeros((n, M, C))
+                for k in range(K):
+                    diff = e[:, 1 + 2 * k] - e[:, 2 + 2 * k]                # (n, M)
+                    g_acc += diff[:, :, None] * (1.0 / (2.0 * c * deltas[:, k]))[:, None, :]
+                grad[lo:hi] = g_acc / K
+        return expect, grad
 
 
 _default: BatchEngine | None = None

@@ -226,7 +226,9 @@ class QuantumModule(torch.nn.Module):
         if up.shape != expected:
             raise ValueError(f"upstream shape {up.shape} does not match forward output {expected}")
         if (method or self.method) != "adjoint":
-            raise NotImplementedError("GPU path implements the adjoint method only")
+            # shift / SPSA: the reference's Jacobian + einsum (model.py:140-142)
+            res = self.jacobians(x, method=method, threads=threads)
+            return {n: np.einsum("bm,bmp->p", up, t) for n, t in res.gradients.items()}
         plan = self._plan(with_inputs=False)
         dev = self._engine.device
         B = x.shape[0]

@@ -155,10 +155,40 @@ def golden_random(engine: BatchEngine) -> None:
     print(f"random: {idx} cases", flush=True)
 
 
+METHOD_ROWS = {1: 16, 2: 8}
+SPSA = dict(seed=5, spsa_c=0.01, spsa_samples=3)
+
+
+def golden_methods(engine: BatchEngine) -> None:
+    """param-shift and SPSA through the reference's run_batch (batch.py:193-201)
+    on the first rows of cfg1 / cfg2 (wrt = (w, x))."""
+    out = {}
+    for cfg_id, rows in METHOD_ROWS.items():
+        spec = configs.CONFIGS[cfg_id]
+        circuit, observables, wrt = configs.build(spec, ref_api(), cz_decompose=True)
+        x, w = configs.inputs_and_weights(spec)
+        xs = x[:rows]
+        ps = engine.run_batch(BatchRequest(circuit, observables, {"w": w}, xs,
+                                           method="param-shift", wrt=wrt))
+        sp = engine.run_batch(BatchRequest(circuit, observables, {"w": w}, xs,
+                                           method="spsa", wrt=wrt, **SPSA))
+        for name, res in (("ps", ps), ("spsa", sp)):
+            out[f"cfg{cfg_id}_{name}_expect"] = res.expectations
+            for k, v in res.gradients.items():
+                out[f"cfg{cfg_id}_{name}_jac_{k}"] = v
+        out[f"cfg{cfg_id}_rows"] = np.array(rows)
+    out["spsa_seed"], out["spsa_c"], out["spsa_samples"] = (
+        np.array(SPSA["seed"]), np.array(SPSA["spsa_c"]), np.array(SPSA["spsa_samples"]))
+    np.savez_compressed(os.path.join(HERE, "methods.npz"), **out)
+    print("methods: done", flush=True)
+
+
 def main(which=None):
     engine = BatchEngine(threads=THREADS)
     if which in (None, "random"):
         golden_random(engine)
+    if which in (None, "methods"):
+        golden_methods(engine)
     for cfg_id in (1, 2, 3, 4, 5):
         if which in (None, f"cfg{cfg_id}"):
             golden_config(cfg_id, engine)
