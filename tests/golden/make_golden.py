@@ -183,7 +183,34 @@ def golden_methods(engine: BatchEngine) -> None:
     print("methods: done", flush=True)
 
 
+def golden_training() -> None:
+    """The reference's train_classifier (training.py:59-94) with Adam on a
+    4-qubit re-uploading classifier over a seeded synthetic dataset."""
+    from vqckit.datasets import Dataset
+    from vqckit.model import Constant, QuantumModule, Uniform
+    from vqckit.optim import Adam
+    from vqckit.training import train_classifier
+    rng = np.random.default_rng(2024)
+    feats = rng.uniform(-1.0, 1.0, (40, 4))
+    labels = (feats[:, 0] * feats[:, 1] > 0).astype(np.int64)
+    ds = Dataset(feats, labels, np.arange(32), np.arange(32, 40), 2)
+    circuit = vqckit.build_reuploading_ansatz(4, 2, num_features=4)
+    obs = [Observable(((2.0, "ZIII"),)), Observable(((2.0, "IZII"),))]
+    mod = QuantumModule(circuit, obs, "s", [("theta", Uniform()), ("lambda", Constant(1.0))],
+                        seed=11, threads=1)
+    opt = Adam(lr=0.05, per_set={"lambda": 0.01})
+    recs = train_classifier(ds, mod, epochs=3, batch_size=8, optimizer=opt, seed=3)
+    np.savez_compressed(os.path.join(HERE, "training.npz"), features=feats, labels=labels,
+                        loss=np.array([r.loss for r in recs]),
+                        metric=np.array([r.metric for r in recs]),
+                        theta=mod.parameters()["theta"], lam=mod.parameters()["lambda"])
+    print("training: done", flush=True)
+
+
 def main(which=None):
+    if which == "training":
+        golden_training()
+        return
     engine = BatchEngine(threads=THREADS)
     if which in (None, "random"):
         golden_random(engine)
