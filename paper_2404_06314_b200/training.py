@@ -196,3 +196,135 @@ def train_classifier(dataset, module, epochs: int, batch_size: int, optimizer,
         if log is not None:
             log(record)
     return records
+
+
+# -- REINFORCE on cart-pole (training.py:97-193, cartpole.py) -------------------
+
+# classic cart-pole constants (cartpole.py:11-23): g, masses, pole half-length,
+# push force, Euler step, termination limits, episode cap
+CARTPOLE = dict(gravity=9.8, m_cart=1.0, m_pole=0.1, half_len=0.5, force=10.0, dt=0.02,
+                angle_limit=12.0 * np.pi / 180.0, x_limit=2.4, max_steps=500)
+
+
+def cartpole_derivatives(state, push: float, c=CARTPOLE):
+    """(x_acc, theta_acc) of the frictionless cart-pole under a horizontal push."""
+    _, _, th, th_dot = state
+    m_tot = c["m_cart"] + c["m_pole"]
+    ml = c["m_pole"] * c["half_len"]
+    cos_t, sin_t = np.cos(th), np.sin(th)
+    tmp = (push + ml * th_dot ** 2 * sin_t) / m_tot
+    th_acc = (c["gravity"] * sin_t - cos_t * tmp) / (
+        c["half_len"] * (4.0 / 3.0 - c["m_pole"] * cos_t ** 2 / m_tot))
+    return tmp - ml * th_acc * cos_t / m_tot, th_acc
+
+
+class CartPoleEnv:
+    """State (x, x_dot, theta, theta_dot); action 0 pushes left, 1 right;
+    reward 1 per step survived. Same reset draws and Euler update order as
+    the reference environment (cartpole.py:26-68)."""
+
+    def __init__(self, seed: int | None = None):
+        self._rng = np.random.default_rng(seed)
+        self.state = np.zeros(4)
+        self.steps = 0
+        self.terminated = True
+
+    def reset(self, seed: int | None = None) -> np.ndarray:
+        if seed is not None:
+            self._rng = np.random.default_rng(seed)
+        self.state = self._rng.uniform(-0.05, 0.05, 4)
+        self.steps, self.terminated = 0, False
+        return self.state.copy()
+
+    def step(self, action: int):
+        if self.terminated:
+            raise RuntimeError("step() called on a terminated episode; call reset() first")
+        if action not in (0, 1):
+            raise ValueError(f"action must be 0 or 1, got {action}")
+        c = CARTPOLE
+        x_acc, th_acc = cartpole_derivatives(self.state, c["force"] if action == 1 else -c["force"])
+        x, x_dot, th, th_dot = self.state
+        # positions advance with the old velocities, then velocities update
+        self.state = np.array([x + c["dt"] * x_dot, x_dot + c["dt"] * x_acc,
+                               th + c["dt"] * th_dot, th_dot + c["dt"] * th_acc])
+        self.steps += 1
+        self.terminated = bool(abs(self.state[0]) > c["x_limit"]
+                               or abs(self.state[2]) > c["angle_limit"]
+                               or self.steps >= c["max_steps"])
+        return self.state.copy(), 1.0, self.terminated
+
+
+def cartpole_policy(depth: int = 3, seed: int | None = None, logit_scale: float = 3.0,
+                    device=None):
+    """4-qubit re-uploading policy, one scaled Z observable per action
+    (training.py:99-117), as a GPU QuantumModule."""
+    from .ir import build_reuploading_ansatz
+    from .module import Constant, QuantumModule, Uniform
+    from .observables import Observable
+    circuit = build_reuploading_ansatz(4, depth, num_features=4)
+    obs = [Observable(((logit_scale, "ZIII"),)), Observable(((logit_scale, "IZII"),))]
+    return QuantumModule(circuit, obs, "s", [("theta", Uniform()), ("lambda", Constant(1.0))],
+                         seed=seed, device=device)
+
+
+def encode_state(state: np.ndarray) -> np.ndarray:
+    return np.arctan(state)
+
+
+def returns_to_go(rewards, discount: float) -> np.ndarray:
+    out = np.empty(len(rewards))
+    acc = 0.0
+    for t in range(len(rewards) - 1, -1, -1):
+        acc = rewards[t] + discount * acc
+        out[t] = acc
+    return out
+
+
+def sample_episode(env, policy, rng, reset_seed: int):
+    """One rollout: per step a batch-1 forward, then rng.choice over the
+    softmax (training.py:134-151)."""
+    state = env.reset(seed=reset_seed)
+    states, actions, rewards, probs_all = [], [], [], []
+    done = False
+    while not done:
+        enc = encode_state(state)
+        probs = softmax(_forward(policy, enc[None, :])[0])
+        action = int(rng.choice(len(probs), p=probs))
+        states.append(enc)
+        actions.append(action)
+        probs_all.append(probs)
+        state, reward, done = env.step(action)
+        rewards.append(reward)
+    return (np.asarray(states), np.asarray(actions, np.int64), np.asarray(rewards),
+            np.asarray(probs_all))
+
+
+def train_reinforce(env, policy, episodes_per_epoch: int, epochs: int, optimizer,
+                    discount: float = 0.99, seed: int = 0, log=None) -> list[EpochRecord]:
+    """REINFORCE without baseline (training.py:154-193): the epoch's visited
+    states go through ONE batched VJP with upstream
+    (onehot(action) - softmax) * return-to-go / episodes, negated for the
+    descending optimizer."""
+    if policy.num_outputs < 2:
+        raise ValueError("policy needs one observable per action")
+    rng = np.random.default_rng(seed)
+    records = []
+    for epoch in range(epochs):
+        states, ups, returns = [], [], []
+        for _ in range(episodes_per_epoch):
+            reset_seed = int(rng.integers(0, 2 ** 31))
+            s, a, r, p = sample_episode(env, policy, rng, reset_seed)
+            ups.append((one_hot(a, policy.num_outputs) - p) * returns_to_go(r, discount)[:, None])
+            states.append(s)
+            returns.append(r.sum())
+        ascent = policy.backward(np.concatenate(states),
+                                 np.concatenate(ups) / episodes_per_epoch)
+        params = _params(policy)
+        optimizer.step(params, {n: -g for n, g in ascent.items()})
+        _store(policy, params)
+        mean_return = float(np.mean(returns))
+        record = EpochRecord(epoch, -mean_return, mean_return)
+        records.append(record)
+        if log is not None:
+            log(record)
+    return records

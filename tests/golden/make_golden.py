@@ -207,9 +207,25 @@ def golden_training() -> None:
     print("training: done", flush=True)
 
 
+def golden_reinforce() -> None:
+    """The reference's train_reinforce (training.py:154-193) on its cart-pole."""
+    from vqckit.cartpole import CartPoleEnv
+    from vqckit.optim import SGD
+    from vqckit.training import cartpole_policy, train_reinforce
+    policy = cartpole_policy(depth=2, seed=5, threads=1)
+    recs = train_reinforce(CartPoleEnv(), policy, episodes_per_epoch=2, epochs=3,
+                           optimizer=SGD(lr=0.05), seed=9)
+    np.savez_compressed(os.path.join(HERE, "reinforce.npz"),
+                        loss=np.array([r.loss for r in recs]),
+                        metric=np.array([r.metric for r in recs]),
+                        theta=policy.parameters()["theta"], lam=policy.parameters()["lambda"])
+    print("reinforce: done", [r.metric for r in recs], flush=True)
+
+
 def main(which=None):
     if which == "training":
         golden_training()
+        golden_reinforce()
         return
     engine = BatchEngine(threads=THREADS)
     if which in (None, "random"):

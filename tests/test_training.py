@@ -106,3 +106,57 @@ def test_gpu_training_matches_reference():
     vals = mod.parameter_values()
     assert np.abs(vals["theta"] - g["theta"]).max() < TOL
     assert np.abs(vals["lambda"] - g["lam"]).max() < TOL
+
+
+def _reinforce(policy):
+    from paper_2404_06314_b200.training import SGD, CartPoleEnv, train_reinforce
+    return train_reinforce(CartPoleEnv(), policy, episodes_per_epoch=2, epochs=3,
+                           optimizer=SGD(lr=0.05), seed=9)
+
+
+def _check_reinforce(recs, theta, lam):
+    g = np.load(os.path.join(GOLDEN, "reinforce.npz"))
+    assert np.array_equal(np.array([r.metric for r in recs]), g["metric"])   # episode returns
+    assert np.array_equal(np.array([r.loss for r in recs]), g["loss"])
+    assert np.abs(theta - g["theta"]).max() < TOL
+    assert np.abs(lam - g["lam"]).max() < TOL
+
+
+def test_cartpole_env_contract():
+    from paper_2404_06314_b200.training import CartPoleEnv
+    env = CartPoleEnv()
+    with pytest.raises(RuntimeError, match="reset"):
+        env.step(0)
+    s = env.reset(seed=1)
+    assert s.shape == (4,) and np.all(np.abs(s) <= 0.05)
+    with pytest.raises(ValueError, match="action must be 0 or 1"):
+        env.step(2)
+    steps = 0
+    done = False
+    while not done:
+        _, r, done = env.step(1)
+        steps += 1
+        assert r == 1.0
+    assert 1 <= steps < 500       # always pushing right drops the pole
+
+
+def test_reinforce_with_oracle_module_matches_reference(oracle_mod):
+    from paper_2404_06314_b200.ir import build_reuploading_ansatz
+    from paper_2404_06314_b200.observables import Observable
+    circuit = build_reuploading_ansatz(4, 2, num_features=4)
+    obs = [Observable(((3.0, "ZIII"),)), Observable(((3.0, "IZII"),))]
+    mod = OracleModule(circuit, obs, seed=5)
+    recs = _reinforce(mod)
+    _check_reinforce(recs, mod.params["theta"], mod.params["lambda"])
+
+
+@pytest.mark.gpu
+def test_gpu_reinforce_matches_reference():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required")
+    from paper_2404_06314_b200.training import cartpole_policy
+    policy = cartpole_policy(depth=2, seed=5, device="cuda:0")
+    recs = _reinforce(policy)
+    vals = policy.parameter_values()
+    _check_reinforce(recs, vals["theta"], vals["lambda"])
