@@ -290,7 +290,8 @@ class BatchEngine:
         rows, M = angles.shape[0], len(observables)
         with torch.cuda.device(dev):
             stream = torch.cuda.current_stream(dev)
-            d_in = torch.from_numpy(np.ascontiguousarray(angles)).to(dev)
+            d_in = (angles.contiguous() if torch.is_tensor(angles)
+                    else torch.from_numpy(np.ascontiguousarray(angles)).to(dev))
             d_w = torch.zeros(max(1, angles.shape[1]), dtype=torch.float64, device=dev)
             expect = torch.empty((rows, M), dtype=torch.float64, device=dev)
             ws = self.workspace.get(plan.workspace_bytes(rows, native.VQC_MODE_FORWARD), dev)
@@ -305,6 +306,7 @@ class BatchEngine:
         forward call over B*(1+2S) angle rows; the finite differences and the
         chain rule through the angle expressions are host arithmetic in the
         reference's accumulation order."""
+        import torch
         compiled = circuit.compiled()
         enc = encoding_set(circuit)
         off, size = compiled.offsets[enc.name]
@@ -339,13 +341,17 @@ class BatchEngine:
             flats = np.repeat(flat[None], n, 0)
             flats[:, off:off + size] = inputs[lo:hi]
             if request.method == "param-shift":
-                base = row_angles(compiled, flats, rot)                 # (n, R)
-                rows = np.repeat(base[:, None], per_row, 1)             # (n, 1+2S, R)
-                for s, r in enumerate(shifted):
-                    rows[:, 1 + 2 * s, r] = base[:, r] + 0.5 * np.pi
-                    rows[:, 2 + 2 * s, r] = base[:, r] - 0.5 * np.pi
+                # base angles on the host (n, R); the 1+2S shifted copies are
+                # built on the device: same IEEE adds as base[r] +/- pi/2
+                base = torch.from_numpy(row_angles(compiled, flats, rot)).to(self.device)
+                rows = base[:, None, :].repeat(1, per_row, 1)           # (n, 1+2S, R)
+                if shifted:
+                    j = torch.arange(len(shifted), device=base.device) * 2 + 1
+                    r = torch.as_tensor(shifted, device=base.device)
+                    rows[:, j, r] = base[:, r] + 0.5 * np.pi
+                    rows[:, j + 1, r] = base[:, r] - 0.5 * np.pi
                 e = self.forward_angle_rows(circuit, observables,
-                                            rows.reshape(n * per_row, -1)).reshape(n, per_row, M)
+                                            rows.view(n * per_row, -1)).reshape(n, per_row, M)
                 expect[lo:hi] = e[:, 0]
                 for s, (g, terms) in enumerate(partials):
                     occ = 0.5 * (e[:, 1 + 2 * s] - e[:, 2 + 2 * s])    # (n, M)
