@@ -152,6 +152,26 @@ def row_angles(compiled, flats: np.ndarray, rot: np.ndarray) -> np.ndarray:
     return out
 
 
+def device_row_angles(compiled, flats, rot: np.ndarray):
+    """``row_angles`` on a device tensor of flat rows: factors gathered per
+    rotation and multiplied left to right after the coefficient; ragged
+    factor lists are padded with an all-ones column (x * 1.0 is exact)."""
+    import torch
+    P = flats.shape[1]
+    nf = [int(compiled.f_offs[g + 1] - compiled.f_offs[g]) for g in rot]
+    width = max(nf, default=0)
+    gather = np.full((len(rot), width), P, np.int64)
+    for r, g in enumerate(rot):
+        gather[r, :nf[r]] = compiled.f_idx[compiled.f_offs[g]:compiled.f_offs[g + 1]]
+    ext = torch.cat([flats, torch.ones_like(flats[:, :1])], dim=1)
+    d_gather = torch.from_numpy(gather).to(flats.device)
+    a = torch.from_numpy(compiled.coeff[rot].copy()).to(flats.device)[None, :].expand(
+        flats.shape[0], -1)
+    for k in range(width):
+        a = a * ext[:, d_gather[:, k]]
+    return a.contiguous()
+
+
 def _device(device):
     import torch
     if device is None:
@@ -368,11 +388,16 @@ class BatchEngine:
                     for k in range(K):
                         d = rng.integers(0, 2, size=C).astype(np.float64)
                         deltas[i, k] = 2.0 * d - 1.0
-                pf = np.repeat(flats[:, None], per_row, 1)              # (n, 1+2K, P)
-                base = flats[:, idx]
-                pf[:, 1::2][:, :, idx] = base[:, None] + c * deltas
-                pf[:, 2::2][:, :, idx] = base[:, None] - c * deltas
-                ang = row_angles(compiled, pf.reshape(n * per_row, -1), rot)
+                # perturbed flats and their angles on the device (same IEEE
+                # ops as the reference: base +/- (c * delta), then coeff * f1 * f2 ...)
+                d_flats = torch.from_numpy(flats).to(self.device)
+                d_idx = torch.from_numpy(idx).to(self.device)
+                d_cd = c * torch.from_numpy(deltas).to(self.device)     # (n, K, C)
+                pf = d_flats[:, None, :].repeat(1, per_row, 1)          # (n, 1+2K, P)
+                base = d_flats[:, None, d_idx]
+                pf[:, 1::2][:, :, d_idx] = base + d_cd
+                pf[:, 2::2][:, :, d_idx] = base - d_cd
+                ang = device_row_angles(compiled, pf.view(n * per_row, -1), rot)
                 e = self.forward_angle_rows(circuit, observables, ang).reshape(n, per_row, M)
                 expect[lo:hi] = e[:, 0]
                 g_acc = np.zeros((n, M, C))

@@ -188,3 +188,18 @@ def test_gpu_module_backward_param_shift_equals_adjoint():
     adj = mod.backward(x[:6], up)
     ps = mod.backward(x[:6], up, method="param-shift")
     assert np.abs(adj["w"] - ps["w"]).max() < 1e-9
+
+
+def test_device_row_angles_equal_host_on_cpu_tensors():
+    """device_row_angles (torch gather path used by SPSA) == row_angles bit for
+    bit; run on CPU tensors here, the GPU tests cover the CUDA placement."""
+    import torch
+    from paper_2404_06314_b200.engine import angle_circuit, device_row_angles, row_angles
+    from paper_2404_06314_b200.ir import build_reuploading_ansatz
+    circ = build_reuploading_ansatz(3, 2, num_features=3)   # lambda * s products
+    comp = circ.compiled()
+    _, rot = angle_circuit(circ)
+    flats = np.random.default_rng(0).normal(size=(5, comp.total_params))
+    host = row_angles(comp, flats, rot)
+    dev = device_row_angles(comp, torch.from_numpy(flats), rot).numpy()
+    assert np.array_equal(host, dev)
