@@ -172,6 +172,39 @@ def device_row_angles(compiled, flats, rot: np.ndarray):
     return a.contiguous()
 
 
+SMEM_MAX_QUBITS = 12     # on-chip plans take any Pauli string (engine.cu kSmemMaxQubits)
+
+
+def basis_groups(observables, num_qubits: int):
+    """Split every observable's terms by their X/Y pattern. Returns
+    [(pattern, [Observable per m])]: pattern[q] is "X", "Y" or "-", and each
+    group's observables are Z strings (X/Y -> Z; an observable with no term in
+    the group gets a zero-weight identity term, so Sum_groups == original)."""
+    groups: dict = {}
+    for m, obs in enumerate(observables):
+        for coeff, string in obs.terms:
+            pat = "".join(ch if ch in "XY" else "-" for ch in string.upper())
+            zs = "".join("Z" if ch in "XYZ" else "I" for ch in string.upper())
+            groups.setdefault(pat, [[] for _ in observables])[m].append((coeff, zs))
+    ident = "I" * num_qubits
+    return [(pat, [Observable(tuple(t) if t else ((0.0, ident),)) for t in per_m])
+            for pat, per_m in groups.items()]
+
+
+def basis_circuit(circuit: Circuit, pattern: str) -> Circuit:
+    """The circuit followed by the constant basis change U with U^dag Z U = P
+    per qubit: H for X, RX(pi/2) for Y (e^{i pi X/4} Z e^{-i pi X/4} = Y).
+    Constant-angle rotations carry no factors, so no gradient columns."""
+    from .ir import AngleExpression, Gate, GateKind
+    extra = []
+    for q, ch in enumerate(pattern):     # Pauli char k acts on qubit k
+        if ch == "X":
+            extra.append(Gate(GateKind.H, (q,)))
+        elif ch == "Y":
+            extra.append(Gate(GateKind.RX, (q,), AngleExpression(0.5 * np.pi, ())))
+    return Circuit(circuit.num_qubits, circuit.gates + tuple(extra), circuit.parameter_sets)
+
+
 def _device(device):
     import torch
     if device is None:
@@ -274,6 +307,8 @@ class BatchEngine:
             return BatchResult(np.empty((B, M)),
                                {n: np.ascontiguousarray(grad[:, :, lo:hi])
                                 for n, lo, hi in layout.slices})
+        if circuit.num_qubits > SMEM_MAX_QUBITS and not all(o.is_z_only for o in observables):
+            return self._run_basis_groups(request, observables, layout, B, M, C)
         dev = self.device
         if C > 0 and request.method != "adjoint":
             expect_h, grad_h = self._run_shifted(request, circuit, observables, layout,
@@ -299,6 +334,24 @@ class BatchEngine:
         return BatchResult(expect_h, {n: np.ascontiguousarray(jac_h[:, :, lo:hi])
                                       for n, lo, hi in layout.slices})
 
+
+    def _run_basis_groups(self, request, observables, layout, B, M, C) -> BatchResult:
+        """X/Y Pauli strings on HBM plans (n > 12): one Z-basis run per X/Y
+        pattern over the basis-rotated circuit; expectations and Jacobians
+        are sums over groups (expectations are linear in the observable)."""
+        import dataclasses
+        expect = np.zeros((B, M))
+        grads = {n: np.zeros((B, M, hi - lo)) for n, lo, hi in layout.slices}
+        cache = request.circuit.__dict__.setdefault("_basis_circuits", {})
+        for pattern, group_obs in basis_groups(observables, request.circuit.num_qubits):
+            if pattern not in cache:
+                cache[pattern] = basis_circuit(request.circuit, pattern)
+            res = self.run_batch(dataclasses.replace(request, circuit=cache[pattern],
+                                                     observables=group_obs))
+            expect += res.expectations
+            for n in grads:
+                grads[n] += res.gradients[n]
+        return BatchResult(expect, grads)
 
     def forward_angle_rows(self, circuit: Circuit, observables, angles: np.ndarray) -> np.ndarray:
         """Expectations (rows, M) of ``circuit`` with per-row rotation angles

@@ -259,13 +259,19 @@ def test_xy_observables_on_chip(torch_cuda):
         assert close(res.gradients[k], j_ref[k]) < TOL
 
 
-def test_xy_observables_rejected_on_hbm_path(torch_cuda):
+def test_xy_observables_on_hbm_path(torch_cuda):
+    """cfg4 (16 qubits, HBM plans) with X / Y observables: run_batch splits
+    the terms per X/Y pattern onto basis-rotated Z-basis plans."""
     from paper_2404_06314_b200 import configs, parse_observable
     spec = configs.CONFIGS[4]
     circ, _, wrt = configs.build(spec, configs.native_api())
     x, w = configs.inputs_and_weights(spec, batch=2)
-    with pytest.raises(NotImplementedError, match="n <= 12"):
-        _engine().run_batch(_request(circ, [parse_observable("X" + "I" * 15)], {"w": w}, x, wrt))
+    obs = [parse_observable("X" + "I" * 15), parse_observable("I" * 3 + "Y" + "Z" + "I" * 11)]
+    e_ref, j_ref = oracle_batch(circ, obs, {"w": w}, x, wrt)
+    res = _engine().run_batch(_request(circ, obs, {"w": w}, x, wrt))
+    assert close(res.expectations, e_ref) < TOL
+    for k in wrt:
+        assert close(res.gradients[k], j_ref[k]) < TOL
 
 
 def test_no_gates_circuit(torch_cuda):
