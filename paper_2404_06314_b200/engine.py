@@ -371,7 +371,8 @@ class BatchEngine:
             plan.forward(d_in, d_w, expect, ws, stream.cuda_stream)
             return expect.cpu().numpy()
 
-    def _run_shifted(self, request, circuit, observables, layout, flat, inputs):
+    def _run_shifted(self, request, circuit, observables, layout, flat, inputs,
+                     rng_for_row=None):
         """param-shift (gradients.py:137-160) and SPSA (gradients.py:180-201)
         as batched GPU forward evaluations. Each row's shifted / perturbed
         evaluations become extra rows of per-gate angles (computed on the host
@@ -437,7 +438,8 @@ class BatchEngine:
                 K, c, idx = request.spsa_samples, request.spsa_c, layout.flat_of_col
                 deltas = np.empty((n, K, C))
                 for i in range(n):
-                    rng = np.random.default_rng(mix_seed(request.seed, lo + i))
+                    rng = (rng_for_row(lo + i) if rng_for_row is not None
+                           else np.random.default_rng(mix_seed(request.seed, lo + i)))
                     for k in range(K):
                         d = rng.integers(0, 2, size=C).astype(np.float64)
                         deltas[i, k] = 2.0 * d - 1.0
