@@ -61,15 +61,15 @@ class QuantumFunction(torch.autograd.Function):
     """(inputs (B,F), flat (P,)) -> expectations (B,M) with adjoint backward."""
 
     @staticmethod
-    def forward(ctx, inputs, flat, module):
+    def forward(ctx, inputs, flat, module, group=None):
         dev = inputs.device
-        plan = module._plan(with_inputs=False)
+        plan = module._plan(with_inputs=False, group=group)
         B = inputs.shape[0]
         expect = torch.empty((B, module.num_outputs), dtype=torch.float64, device=dev)
         if B > 0 and module.num_outputs > 0:
             ws = module._engine.workspace.get(plan.workspace_bytes(B, native.VQC_MODE_FORWARD), dev)
             plan.forward(inputs, flat, expect, ws, torch.cuda.current_stream(dev).cuda_stream)
-        ctx.module = module
+        ctx.module, ctx.group = module, group
         ctx.save_for_backward(inputs, flat)
         return expect
 
@@ -78,7 +78,7 @@ class QuantumFunction(torch.autograd.Function):
         inputs, flat = ctx.saved_tensors
         module = ctx.module
         need_x = ctx.needs_input_grad[0]
-        plan = module._plan(with_inputs=need_x)
+        plan = module._plan(with_inputs=need_x, group=ctx.group)
         dev = inputs.device
         B = inputs.shape[0]
         upstream = grad_out.contiguous().to(torch.float64)
@@ -91,7 +91,7 @@ class QuantumFunction(torch.autograd.Function):
         cols = module._trainable_cols
         grad_flat[module._trainable_flat] = vsum[:cols]
         grad_x = rows[:, cols:] if need_x else None
-        return grad_x, grad_flat, None
+        return grad_x, grad_flat, None, None
 
 
 class QuantumModule(torch.nn.Module):
@@ -169,10 +169,26 @@ class QuantumModule(torch.nn.Module):
         return tuple(n for n, _ in self.trainable_specs)
 
     # -- plumbing ----------------------------------------------------------------
-    def _plan(self, with_inputs: bool):
+    def _plan(self, with_inputs: bool, group=None):
         wrt = self.trainable_names() + ((self.encoding_set,) if with_inputs else ())
-        plan, _ = self._engine.plans.get(self.circuit, self.observables, wrt, self._engine.device)
+        circ, obs = ((self.circuit, self.observables) if group is None
+                     else self._basis_groups()[group])
+        plan, _ = self._engine.plans.get(circ, obs, wrt, self._engine.device)
         return plan
+
+    def _basis_groups(self):
+        """None when the plan takes the observables directly; for X/Y Pauli
+        strings on HBM plans (n > 12) the [(basis circuit, Z observables)]
+        split of engine.basis_groups, whose outputs sum to the original."""
+        if "_groups" not in self.__dict__:
+            from .engine import SMEM_MAX_QUBITS, basis_circuit, basis_groups
+            groups = None
+            if (self.circuit.num_qubits > SMEM_MAX_QUBITS
+                    and not all(o.is_z_only for o in self.observables)):
+                groups = [(basis_circuit(self.circuit, pat), obs)
+                          for pat, obs in basis_groups(self.observables, self.circuit.num_qubits)]
+            self.__dict__["_groups"] = groups
+        return self.__dict__["_groups"]
 
     def flat_weights(self) -> torch.Tensor:
         """Flat parameter vector in declaration order, encoding slot zeroed."""
@@ -202,7 +218,14 @@ class QuantumModule(torch.nn.Module):
     # -- API ---------------------------------------------------------------------
     def forward(self, inputs) -> torch.Tensor:
         """(B, M) expectations; differentiable w.r.t. weights and inputs."""
-        return QuantumFunction.apply(self._as_inputs(inputs), self.flat_weights(), self)
+        x, flat = self._as_inputs(inputs), self.flat_weights()
+        groups = self._basis_groups()
+        if groups is None:
+            return QuantumFunction.apply(x, flat, self, None)
+        out = QuantumFunction.apply(x, flat, self, 0)
+        for g in range(1, len(groups)):
+            out = out + QuantumFunction.apply(x, flat, self, g)
+        return out
 
     def jacobians(self, inputs, method: str | None = None, wrt=None,
                   threads: int | None = None) -> BatchResult:
@@ -229,18 +252,22 @@ class QuantumModule(torch.nn.Module):
             # shift / SPSA: the reference's Jacobian + einsum (model.py:140-142)
             res = self.jacobians(x, method=method, threads=threads)
             return {n: np.einsum("bm,bmp->p", up, t) for n, t in res.gradients.items()}
-        plan = self._plan(with_inputs=False)
         dev = self._engine.device
         B = x.shape[0]
-        vsum = torch.zeros(plan.num_cols, dtype=torch.float64, device=dev)
-        if B > 0 and self.num_outputs > 0:
-            d_up = torch.from_numpy(np.ascontiguousarray(up)).to(dev)
-            ws = self._engine.workspace.get(plan.workspace_bytes(B, native.VQC_MODE_VJP), dev)
-            with torch.no_grad():
-                plan.adjoint(x, self.flat_weights().detach(), d_up, None, None, None, vsum, ws,
-                             torch.cuda.current_stream(dev).cuda_stream)
+        groups = self._basis_groups()
+        host = None
+        for g in (range(len(groups)) if groups is not None else (None,)):
+            plan = self._plan(with_inputs=False, group=g)
+            vsum = torch.zeros(plan.num_cols, dtype=torch.float64, device=dev)
+            if B > 0 and self.num_outputs > 0:
+                d_up = torch.from_numpy(np.ascontiguousarray(up)).to(dev)
+                ws = self._engine.workspace.get(plan.workspace_bytes(B, native.VQC_MODE_VJP), dev)
+                with torch.no_grad():
+                    plan.adjoint(x, self.flat_weights().detach(), d_up, None, None, None, vsum,
+                                 ws, torch.cuda.current_stream(dev).cuda_stream)
+            part = vsum.cpu().numpy()
+            host = part if host is None else host + part
         out, col = {}, 0
-        host = vsum.cpu().numpy()
         for n in self.trainable_names():
             size = self.circuit.set_named(n).size
             out[n] = host[col:col + size].copy()

@@ -90,3 +90,27 @@ def test_gpu_xy_observables_on_hbm_plans(n, seed):
         assert close(res.gradients[k], j_ref[k]) < TOL
     fwd = BatchEngine(device="cuda:0").run_batch(BatchRequest(circ, obs, {"w": w}, x))
     assert close(fwd.expectations, e_ref) < TOL
+
+
+@pytest.mark.gpu
+def test_gpu_module_autograd_xy_on_hbm_plans():
+    """QuantumModule.forward / autograd and .backward with X/Y observables at
+    n = 13: per-group QuantumFunction nodes summed, vs the oracle."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required")
+    from paper_2404_06314_b200.module import QuantumModule
+    circ, obs, w, x = _random(2, 13, n_gates=50)
+    mod = QuantumModule(circ, obs, "s", ["w"], seed=0, device="cuda:0")
+    with torch.no_grad():
+        mod.values["w"].copy_(torch.from_numpy(w))
+    xt = torch.from_numpy(x).cuda().requires_grad_(True)
+    out = mod(xt)
+    up = np.random.default_rng(1).normal(size=out.shape)
+    out.backward(torch.from_numpy(up).cuda())
+    e_ref, j_ref = oracle_batch(circ, obs, {"w": w}, x, ("w", "s"))
+    assert close(out.detach().cpu().numpy(), e_ref) < TOL
+    assert close(mod.values["w"].grad.cpu().numpy(), np.einsum("bm,bmp->p", up, j_ref["w"])) < TOL
+    assert close(xt.grad.cpu().numpy(), np.einsum("bm,bmf->bf", up, j_ref["s"])) < TOL
+    vjp = mod.backward(x, up)
+    assert close(vjp["w"], np.einsum("bm,bmp->p", up, j_ref["w"])) < TOL
