@@ -115,7 +115,7 @@ def test_optimizer_step_reduces_loss(torch):
         loss = ((mod(x) - target) ** 2).mean()
         loss.backward()
         opt.step()
-        losses.append(float(loss))
+        losses.append(float(loss.detach()))
     assert losses[-1] < losses[0]
 
 
