@@ -333,3 +333,47 @@ class HybridModule(torch.nn.Module):
         out = self.forward(inputs)
         out.backward(up)
         return {k: v.grad.detach().cpu().numpy().copy() for k, v in named.items()}
+
+
+# -- checkpoints (model.py:227-269: same JSON layout, so files interchange) ----
+
+def checkpoint_dict(module) -> dict:
+    quantum = module.quantum if isinstance(module, HybridModule) else module
+    out = {"sets": {n: v.tolist() for n, v in quantum.parameter_values().items()}}
+    if isinstance(module, HybridModule):
+        for block in ("pre", "post"):
+            w, b = getattr(module, f"{block}_weight"), getattr(module, f"{block}_bias")
+            out[block] = {"weight": w.detach().cpu().numpy().tolist(),
+                          "bias": b.detach().cpu().numpy().tolist()}
+    return out
+
+
+def save_checkpoint(module, path) -> None:
+    import json
+    with open(path, "w") as fh:
+        json.dump(checkpoint_dict(module), fh, indent=2)
+        fh.write("\n")
+
+
+def load_checkpoint(module, path) -> None:
+    """Restore parameter values in place; set names and shapes must match."""
+    import json
+    with open(path) as fh:
+        data = json.load(fh)
+    quantum = module.quantum if isinstance(module, HybridModule) else module
+    with torch.no_grad():
+        for name, values in data.get("sets", {}).items():
+            values = np.asarray(values, dtype=np.float64)
+            if name not in quantum.values:
+                raise ValueError(f"checkpoint set {name!r} not in module")
+            if values.shape != tuple(quantum.values[name].shape):
+                raise ValueError(f"checkpoint set {name!r} has shape {values.shape}, "
+                                 f"expected {tuple(quantum.values[name].shape)}")
+            quantum.values[name].copy_(torch.from_numpy(values))
+        if isinstance(module, HybridModule):
+            for block in ("pre", "post"):
+                if block in data:
+                    getattr(module, f"{block}_weight").copy_(
+                        torch.from_numpy(np.asarray(data[block]["weight"], np.float64)))
+                    getattr(module, f"{block}_bias").copy_(
+                        torch.from_numpy(np.asarray(data[block]["bias"], np.float64)))

@@ -328,3 +328,42 @@ def train_reinforce(env, policy, episodes_per_epoch: int, epochs: int, optimizer
         if log is not None:
             log(record)
     return records
+
+
+# -- dataset helpers (datasets.py:47-66, 106-125) --------------------------------
+
+Dataset = ArrayDataset
+
+
+def split_indices(n: int, seed: int, test_fraction: float = 0.2):
+    """Sorted, disjoint train / test indices from one seeded permutation."""
+    order = np.random.default_rng(seed).permutation(n)
+    n_test = int(round(n * test_fraction))
+    return np.sort(order[n_test:]), np.sort(order[:n_test])
+
+
+def from_arrays(features, labels, seed: int = 0, test_fraction: float = 0.2) -> ArrayDataset:
+    features = np.asarray(features, dtype=np.float64)
+    labels = np.asarray(labels)
+    if np.any(labels != labels.astype(np.int64)):
+        raise ValueError("labels must be integers")
+    labels = labels.astype(np.int64)
+    if np.any(labels < 0):
+        raise ValueError("labels must be non-negative")
+    classes = int(labels.max()) + 1 if len(labels) else 0
+    tr, te = split_indices(len(labels), seed, test_fraction)
+    return ArrayDataset(features, labels, tr, te, classes)
+
+
+def synthetic_blobs(samples_per_class: int = 60, num_features: int = 4, num_classes: int = 2,
+                    separation: float = 3.0, noise: float = 0.5, seed: int = 0,
+                    test_fraction: float = 0.2) -> ArrayDataset:
+    """One Gaussian blob per class around a random direction scaled to
+    ``separation``; draws: centres first, then each class's noise in order."""
+    rng = np.random.default_rng(seed)
+    centers = rng.normal(size=(num_classes, num_features))
+    centers = centers / np.linalg.norm(centers, axis=1, keepdims=True) * separation
+    feats = np.concatenate([centers[c] + noise * rng.normal(size=(samples_per_class, num_features))
+                            for c in range(num_classes)])
+    labels = np.repeat(np.arange(num_classes, dtype=np.int64), samples_per_class)
+    return from_arrays(feats, labels, seed=seed, test_fraction=test_fraction)

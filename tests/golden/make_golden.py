@@ -224,6 +224,10 @@ def golden_reinforce() -> None:
 
 def main(which=None):
     if which == "training":
+        from vqckit.datasets import synthetic_blobs
+        ds = synthetic_blobs(samples_per_class=10, num_features=3, num_classes=3, seed=4)
+        np.savez_compressed(os.path.join(HERE, "blobs.npz"), features=ds.features,
+                            labels=ds.labels, train_idx=ds.train_idx, test_idx=ds.test_idx)
         golden_training()
         golden_reinforce()
         return
