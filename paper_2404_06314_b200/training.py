@@ -367,3 +367,40 @@ def synthetic_blobs(samples_per_class: int = 60, num_features: int = 4, num_clas
                             for c in range(num_classes)])
     labels = np.repeat(np.arange(num_classes, dtype=np.int64), samples_per_class)
     return from_arrays(feats, labels, seed=seed, test_fraction=test_fraction)
+
+
+def load_dataset(path, seed: int = 0, test_fraction: float = 0.2) -> ArrayDataset:
+    """Text table -> dataset (datasets.py:69-103): comma- or whitespace-
+    separated, '#' comments and blank lines skipped, an optional non-numeric
+    header as the first content row, last column = integer label."""
+    rows, width, seen_content = [], None, False
+    with open(path) as fh:
+        for lineno, raw in enumerate(fh, start=1):
+            line = raw.strip()
+            if not line or line.startswith("#"):
+                continue
+            fields = line.split(",") if "," in line else line.split()
+            try:
+                values = [float(f) for f in fields]
+            except ValueError as exc:
+                if not seen_content:          # header row
+                    seen_content = True
+                    continue
+                raise ValueError(f"{path}:{lineno}: malformed row") from exc
+            seen_content = True
+            if width is None:
+                width = len(values)
+                if width < 2:
+                    raise ValueError(f"{path}:{lineno}: need at least one feature column "
+                                     "and one label column")
+            elif len(values) != width:
+                raise ValueError(f"{path}:{lineno}: expected {width} columns, "
+                                 f"got {len(values)}")
+            if values[-1] != int(values[-1]):
+                raise ValueError(f"{path}:{lineno}: unknown label {values[-1]!r} "
+                                 "(labels must be integers)")
+            rows.append(values)
+    if not rows:
+        raise ValueError(f"{path}: no data rows")
+    data = np.asarray(rows)
+    return from_arrays(data[:, :-1], data[:, -1], seed, test_fraction)

@@ -228,6 +228,10 @@ def main(which=None):
         ds = synthetic_blobs(samples_per_class=10, num_features=3, num_classes=3, seed=4)
         np.savez_compressed(os.path.join(HERE, "blobs.npz"), features=ds.features,
                             labels=ds.labels, train_idx=ds.train_idx, test_idx=ds.test_idx)
+        from vqckit.datasets import load_dataset
+        tb = load_dataset(os.path.join(HERE, "toy_table.csv"), seed=2, test_fraction=0.4)
+        np.savez_compressed(os.path.join(HERE, "toy_table.npz"), features=tb.features,
+                            labels=tb.labels, train_idx=tb.train_idx, test_idx=tb.test_idx)
         golden_training()
         golden_reinforce()
         return

@@ -71,3 +71,28 @@ def test_checkpoint_errors(tmp_path):
     bad.write_text(json.dumps({"sets": {"theta": [1.0]}}))
     with pytest.raises(ValueError, match="has shape"):
         load_checkpoint(mod, bad)
+
+
+def test_load_dataset_matches_reference():
+    """tests/golden/toy_table.csv (comment, header, blank line) loaded by the
+    reference -> toy_table.npz."""
+    from paper_2404_06314_b200.training import load_dataset
+    g = np.load(os.path.join(GOLDEN, "toy_table.npz"))
+    ds = load_dataset(os.path.join(GOLDEN, "toy_table.csv"), seed=2, test_fraction=0.4)
+    for k in ("features", "labels", "train_idx", "test_idx"):
+        assert np.array_equal(getattr(ds, k), g[k]), k
+
+
+@pytest.mark.parametrize("text,match", [
+    ("1,2\n3,x\n", "malformed row"),
+    ("1\n", "at least one feature"),
+    ("1,2,0\n1,1\n", "expected 3 columns"),
+    ("1,0.5\n", "unknown label"),
+    ("# only comments\n\n", "no data rows"),
+])
+def test_load_dataset_errors(tmp_path, text, match):
+    from paper_2404_06314_b200.training import load_dataset
+    p = tmp_path / "t.csv"
+    p.write_text(text)
+    with pytest.raises(ValueError, match=match):
+        load_dataset(p)
