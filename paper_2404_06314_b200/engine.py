@@ -15,6 +15,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import native
+from .instrument import sweep_counters
 from .ir import Circuit
 from .observables import Observable, ObservablePack
 
@@ -324,11 +325,14 @@ class BatchEngine:
             if C == 0:
                 ws = self.workspace.get(plan.workspace_bytes(B, native.VQC_MODE_FORWARD), dev)
                 plan.forward(d_in, d_w, expect, ws, stream.cuda_stream)
+                sweep_counters.add_forward(B)
                 jac = None
             else:
                 ws = self.workspace.get(plan.workspace_bytes(B, native.VQC_MODE_JACOBIAN), dev)
                 jac = torch.empty((B, M, C), dtype=torch.float64, device=dev)
                 plan.adjoint(d_in, d_w, None, expect, jac, None, None, ws, stream.cuda_stream)
+                sweep_counters.add_forward(B)
+                sweep_counters.add_reverse(B, B * M)
             expect_h = expect.cpu().numpy()
             jac_h = jac.cpu().numpy() if jac is not None else np.zeros((B, M, 0))
         return BatchResult(expect_h, {n: np.ascontiguousarray(jac_h[:, :, lo:hi])
@@ -369,6 +373,7 @@ class BatchEngine:
             expect = torch.empty((rows, M), dtype=torch.float64, device=dev)
             ws = self.workspace.get(plan.workspace_bytes(rows, native.VQC_MODE_FORWARD), dev)
             plan.forward(d_in, d_w, expect, ws, stream.cuda_stream)
+            sweep_counters.add_forward(rows)
             return expect.cpu().numpy()
 
     def _run_shifted(self, request, circuit, observables, layout, flat, inputs,

@@ -25,6 +25,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
+from .instrument import sweep_counters
 from . import native
 from .engine import BatchEngine, BatchRequest, BatchResult, encoding_set
 
@@ -69,6 +70,7 @@ class QuantumFunction(torch.autograd.Function):
         if B > 0 and module.num_outputs > 0:
             ws = module._engine.workspace.get(plan.workspace_bytes(B, native.VQC_MODE_FORWARD), dev)
             plan.forward(inputs, flat, expect, ws, torch.cuda.current_stream(dev).cuda_stream)
+            sweep_counters.add_forward(B)
         ctx.module, ctx.group = module, group
         ctx.save_for_backward(inputs, flat)
         return expect
@@ -87,6 +89,8 @@ class QuantumFunction(torch.autograd.Function):
         ws = module._engine.workspace.get(plan.workspace_bytes(B, native.VQC_MODE_VJP), dev)
         plan.adjoint(inputs, flat, upstream, None, None, rows, vsum, ws,
                      torch.cuda.current_stream(dev).cuda_stream)
+        sweep_counters.add_forward(B)       # the adjoint re-evolves psi forward first
+        sweep_counters.add_reverse(B, B)    # one VJP-seeded bra per row
         grad_flat = torch.zeros_like(flat)
         cols = module._trainable_cols
         grad_flat[module._trainable_flat] = vsum[:cols]
@@ -265,6 +269,8 @@ class QuantumModule(torch.nn.Module):
                 with torch.no_grad():
                     plan.adjoint(x, self.flat_weights().detach(), d_up, None, None, None, vsum,
                                  ws, torch.cuda.current_stream(dev).cuda_stream)
+                sweep_counters.add_forward(B)
+                sweep_counters.add_reverse(B, B)
             part = vsum.cpu().numpy()
             host = part if host is None else host + part
         out, col = {}, 0
