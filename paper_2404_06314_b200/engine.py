@@ -94,6 +94,7 @@ class BatchRequest:
     seed: int = 0
     spsa_c: float = 0.01
     spsa_samples: int = 1
+    row_offset: int = 0                 # global index of row 0 (rank shards: SPSA seeds)
 
 
 @dataclass
@@ -444,7 +445,8 @@ class BatchEngine:
                 deltas = np.empty((n, K, C))
                 for i in range(n):
                     rng = (rng_for_row(lo + i) if rng_for_row is not None
-                           else np.random.default_rng(mix_seed(request.seed, lo + i)))
+                           else np.random.default_rng(
+                               mix_seed(request.seed, request.row_offset + lo + i)))
                     for k in range(K):
                         d = rng.integers(0, 2, size=C).astype(np.float64)
                         deltas[i, k] = 2.0 * d - 1.0

@@ -101,3 +101,30 @@ def allreduce_module_grads(module, group=None) -> None:
     for g in grads:
         g.copy_(flat[off: off + g.numel()].view_as(g))
         off += g.numel()
+
+
+def sharded_run_batch(request, run: Callable, rank: int, world: int, group=None,
+                      gather: bool = True):
+    """``run_batch`` semantics over ranks for any method: this rank evaluates
+    its contiguous rows (``row_offset`` keeps SPSA's per-row seeds global, as
+    the reference's worker threads do, batch.py:197), then expectations and
+    Jacobians are all-gathered in row order. ``run(request) -> BatchResult``
+    is the per-rank engine call (``BatchEngine.run_batch`` on this rank's GPU)."""
+    import dataclasses
+
+    from .engine import BatchResult
+
+    inputs = np.asarray(request.inputs, np.float64)
+    B = inputs.shape[0]
+    lo, hi = shard_rows(B, world, rank)
+    local = run(dataclasses.replace(request, inputs=inputs[lo:hi],
+                                    row_offset=request.row_offset + lo))
+    if not gather:
+        return local
+    M = local.expectations.shape[1]
+    expect = gather_rows(local.expectations, B, world, group)
+    grads = {}
+    for name, g in local.gradients.items():
+        flat = gather_rows(g.reshape(g.shape[0], -1), B, world, group)
+        grads[name] = np.ascontiguousarray(flat.reshape(B, M, -1))
+    return BatchResult(expect, grads)

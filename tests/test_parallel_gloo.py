@@ -80,3 +80,70 @@ def test_world_size_2_gloo(tmp_path):
         np.testing.assert_array_equal(d["exp"], e_ref)
     lo0, hi0 = np.load(tmp_path / "r0.npz")["lo"], np.load(tmp_path / "r0.npz")["hi"]
     assert (int(lo0), int(hi0)) == (0, 7)
+
+
+def _spsa_run(circ, obs, wrt):
+    """CPU stand-in for BatchEngine.run_batch(method="spsa"): the oracle's
+    SPSA per row with the engine's seeding rule mix_seed(seed, row_offset + b)."""
+    from oracle import oracle
+    from paper_2404_06314_b200.engine import BatchResult, WrtLayout, mix_seed
+    from conftest import lowered
+
+    def run(req):
+        comp = circ.compiled()
+        layout = WrtLayout.build(comp, wrt)
+        off, size = comp.offsets["x"]
+        flat = comp.flat_values({"w": req.trainable_values["w"], "x": np.zeros(size)})
+        low = lowered(circ, obs)
+        B = req.inputs.shape[0]
+        e = np.zeros((B, len(obs)))
+        j = np.zeros((B, len(obs), layout.n_cols))
+        for b in range(B):
+            f = flat.copy()
+            f[off:off + size] = req.inputs[b]
+            rng = np.random.default_rng(mix_seed(req.seed, req.row_offset + b))
+            e[b], j[b] = oracle.spsa_row(low, f, layout.flat_of_col, req.spsa_c,
+                                         req.spsa_samples, rng)
+        return BatchResult(e, {n: j[:, :, lo:hi] for n, lo, hi in layout.slices})
+    return run
+
+
+def _spsa_problem():
+    from paper_2404_06314_b200 import configs
+    from paper_2404_06314_b200.engine import BatchRequest
+    spec = configs.CONFIGS[1]
+    circ, obs, wrt = configs.build(spec, configs.native_api())
+    x, w = configs.inputs_and_weights(spec, batch=7)
+    req = BatchRequest(circ, obs, {"w": w}, x, method="spsa", wrt=wrt, seed=5, spsa_samples=2)
+    return circ, obs, wrt, req
+
+
+def _spsa_worker(rank, world, port, out_dir):
+    import torch.distributed as dist
+
+    from paper_2404_06314_b200 import parallel
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        circ, obs, wrt, req = _spsa_problem()
+        res = parallel.sharded_run_batch(req, _spsa_run(circ, obs, wrt), rank, world)
+        np.savez(os.path.join(out_dir, f"s{rank}.npz"), exp=res.expectations,
+                 **{f"g_{k}": v for k, v in res.gradients.items()})
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_sharded_run_batch_spsa_seeds_are_global(tmp_path):
+    """Sharded SPSA == single-process SPSA bit for bit: each rank seeds its
+    rows with the GLOBAL row index (row_offset), then rows are gathered."""
+    world = 2
+    mp.start_processes(_spsa_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world,
+                       start_method="spawn")
+    circ, obs, wrt, req = _spsa_problem()
+    full = _spsa_run(circ, obs, wrt)(req)
+    for r in range(world):
+        d = np.load(tmp_path / f"s{r}.npz")
+        np.testing.assert_array_equal(d["exp"], full.expectations)
+        for k in wrt:
+            np.testing.assert_array_equal(d[f"g_{k}"], full.gradients[k])
