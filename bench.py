@@ -19,6 +19,15 @@ inputs), plus the one NCCL all-reduce of the weight gradients for N > 1.
 * ``cpu_baseline``: the CPU oracle (C restatement of the reference kernels,
   OpenMP over rows like the reference's thread pool) on a bounded row sample.
 * ``--impl reference``: that CPU path alone, as the reference arm.
+* ``--gpus N`` without an outer torchrun re-launches this script under
+  ``torch.distributed.run`` with N ranks (one per GPU, NCCL); rows shard
+  with the reference's split and the weight gradient is all-reduced once
+  per step. ``--dry-run`` runs the same launcher / sharding / all-reduce /
+  max-over-ranks path on gloo with a host-only step (CPU test of the N > 1
+  plumbing).
+* ``parity``: the bench checks its own timed outputs: the first 8 rows
+  against the reference's goldens (tests/golden) and, at N = 1, the last
+  rows against the oracle rows the cpu_baseline leg computes anyway.
 """
 
 from __future__ import annotations
@@ -136,64 +145,194 @@ def dist_setup():
     return world, rank, local
 
 
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch(args) -> int:
+    """``--gpus N`` (N > 1) outside torchrun: run this script under
+    ``torch.distributed.run`` with N ranks on this node (127.0.0.1)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def nccl_log_setup() -> str | None:
+    """NCCL_DEBUG=INFO into per-job files (not stdout, which carries the one
+    JSON line); rank 0 summarises the communicator lines afterwards."""
+    if "NCCL_DEBUG" in os.environ and "NCCL_DEBUG_FILE" not in os.environ:
+        return None
+    d = f"/tmp/vqc_bench_nccl_{os.environ.get('MASTER_PORT', 'x')}_{os.getppid()}"
+    os.makedirs(d, exist_ok=True)
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_FILE", os.path.join(d, "%h.%p.log"))
+    return d
+
+
+def nccl_summary(d: str | None) -> dict | None:
+    """Communicator evidence (version, nRanks, NVLS / channel lines)."""
+    import glob
+    if not d:
+        return None
+    files = sorted(glob.glob(os.path.join(d, "*.log")))
+    keep = ("NCCL version", "Init COMPLETE", "NVLS", "nRanks", "P2P/CUMEM", "via P2P")
+    lines = []
+    for f in files:
+        try:
+            with open(f) as fh:
+                lines += [ln.strip()[-220:] for ln in fh if any(k in ln for k in keep)]
+        except OSError:
+            pass
+    return {"files": len(files), "lines": lines[:16]}
+
+
+def host_cpu() -> dict:
+    """Host CPU identity: physical cores (the reference's default thread
+    count, batch.py:47-51), logical cores and the model string."""
+    try:
+        import psutil
+        physical = psutil.cpu_count(logical=False)
+    except Exception:
+        physical = None
+    logical = os.cpu_count() or 1
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except AttributeError:
+        usable = logical
+    return {"physical": physical or logical, "logical": logical, "usable": usable, "model": model}
+
+
 # ----------------------------------------------------------------------------- CPU arms
 
-def cpu_reference_rows(spec, rows: int, threads: int):
-    """Reference semantics on the CPU oracle: run_batch(method='adjoint', wrt)
-    (Jacobian, M+1 reverse sweeps per row; batch.py:478-480) + the backward
-    einsum (model.py:661). Returns wall seconds."""
+def cpu_reference_rows(spec, xs, threads: int, combined: bool = False):
+    """Reference semantics on the CPU oracle for rows ``xs``.
+
+    combined=False: run_batch(method='adjoint', wrt) (the Jacobian, M+1
+    reverse sweeps per row; batch.py:147-217) + the backward einsum
+    (model.py:140-142) — what the reference's QuantumModule.backward costs.
+    combined=True: the best-case VJP-equivalent reference call, one
+    observable sum_m O_m (observables.py:21-47; valid for the bench's
+    row-uniform upstream) — 2 reverse sweeps per row.
+    Returns (seconds, per-row VJP rows (len(xs), n_cols), expectations)."""
     from paper_2404_06314_b200 import configs
+    from paper_2404_06314_b200.observables import Observable
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from conftest import oracle_batch
     circ, obs, wrt = configs.build(spec, configs.native_api())
-    x, w = configs.inputs_and_weights(spec)
-    xs = x[:rows]
+    _, w = configs.inputs_and_weights(spec, batch=1)
+    if combined:
+        obs = [Observable(tuple(t for o in obs for t in o.terms))]
     t0 = time.perf_counter()
     e, jac = oracle_batch(circ, obs, {"w": w}, xs, wrt, threads=threads)
-    up = np.ones((rows, len(obs)))
-    _ = {k: np.einsum("bm,bmp->p", up, v) for k, v in jac.items()}
-    return time.perf_counter() - t0
+    up = np.ones((len(xs), len(obs)))
+    vjp_rows = np.concatenate([np.einsum("bm,bmp->bp", up, jac[k]) for k in wrt], axis=1)
+    _ = vjp_rows.sum(axis=0)
+    return time.perf_counter() - t0, vjp_rows, e
 
 
-def cpu_rows_for(spec, threads: int, target_s: float) -> int:
-    """Bounded sample: rows so one timed sample takes about target_s."""
-    t1 = cpu_reference_rows(spec, max(1, threads), threads)  # one row per thread
-    per_round = max(t1, 1e-4)
-    rounds = max(1, int(target_s / per_round))
+def cpu_rows_for(spec, threads: int, target_s: float, min_rounds: int = 4) -> int:
+    """Bounded sample: a multiple of ``threads`` rows (>= min_rounds rows per
+    thread, SURVEY §8d asks >= 4T on cfg4) taking about target_s."""
+    x, _ = configs_inputs(spec)
+    t1, _, _ = cpu_reference_rows(spec, x[:threads], threads)   # one row per thread
+    rounds = max(min_rounds, int(target_s / max(t1, 1e-4)))
     return int(min(spec.batch, rounds * threads))
 
 
-def cpu_baseline(spec, target_s: float = 10.0) -> dict:
-    threads = os.cpu_count() or 1
+def configs_inputs(spec):
+    from paper_2404_06314_b200 import configs
+    return configs.inputs_and_weights(spec)
+
+
+def cpu_baseline(spec, target_s: float = 10.0) -> tuple[dict, dict]:
+    """Both CPU numbers on the LAST rows of the batch (so the bench's own GPU
+    outputs for those rows can be checked against them): the reference's
+    Jacobian + einsum backward, and its VJP-equivalent combined-observable
+    call. Returns (cpu_baseline dict, oracle rows for the parity check)."""
+    cpu = host_cpu()
+    threads = cpu["physical"]
     rows = cpu_rows_for(spec, threads, target_s)
-    dt = cpu_reference_rows(spec, rows, threads)
-    return {"value": rows / dt, "unit": "samples/s", "cores": threads, "kind": "port",
-            "sample": f"{rows} of {spec.batch} rows of cfg{spec.cfg_id}, oracle (C port of vqckit "
-                      f"_kernels.py, Jacobian + einsum = reference backward semantics), "
-                      f"{threads} OpenMP threads, {dt:.1f} s"}
+    x, _ = configs_inputs(spec)
+    lo = spec.batch - rows
+    dt, vjp_rows, e = cpu_reference_rows(spec, x[lo:], threads)
+    dtc, vjp_c, _ = cpu_reference_rows(spec, x[lo:], threads, combined=True)
+    out = {"value": rows / dt, "unit": "samples/s", "cores": threads, "kind": "port",
+           "sample": f"rows {lo}..{spec.batch - 1} ({rows} of {spec.batch}) of cfg{spec.cfg_id}; "
+                     f"oracle = C restatement of vqckit _kernels.py + run_batch, reference "
+                     f"backward semantics (Jacobian, M+1 reverse sweeps per row, + einsum), "
+                     f"{threads} OpenMP threads = physical cores, {dt:.1f} s",
+           "cpu_model": cpu["model"], "physical_cores": cpu["physical"],
+           "logical_cores": cpu["logical"],
+           "vjp_equivalent": {"value": rows / dtc, "unit": "samples/s", "seconds": dtc,
+                              "call": "one combined observable sum_m O_m (observables.py:21-47), "
+                                      "2 reverse sweeps per row; valid for upstream = ones"},
+           "rows_measured": rows, "extrapolation": "linear in rows (rows are independent)"}
+    check = {"lo": lo, "vjp_rows": vjp_rows, "vjp_rows_combined": vjp_c, "expect": e}
+    return out, check
+
+
+def config_block(spec, world: int) -> dict:
+    """The ``config`` object both arms print (same keys, so the driver can
+    match the lines)."""
+    return {"workload": workload_desc(spec), "batch": spec.batch, "qubits": spec.n,
+            "layers": spec.layers, "observables": len(configs_terms(spec)),
+            "mode": "vjp (upstream = ones)",
+            "parallelism": f"dp{world} (row shards, split_workload; 1 NCCL all-reduce of the "
+                           "weight grads per step)" if world > 1 else "dp1",
+            "l2": "flushed between timed steps (256 MiB write); states stream through "
+                  "a >1 GiB HBM workspace"}
+
+
+def configs_terms(spec):
+    from paper_2404_06314_b200 import configs
+    return configs.observable_terms(spec)
 
 
 def run_reference(args, spec):
+    """Reference arm: the oracle (reference kernels restated in C) on all
+    physical cores, a bounded row sample per step; rank 0 only."""
     world, rank, _ = dist_setup()
     if rank != 0:
         return
-    threads = os.cpu_count() or 1
-    rows = cpu_rows_for(spec, threads, target_s=args.ref_step_s)
+    cpu = host_cpu()
+    threads = cpu["physical"]
+    rows = cpu_rows_for(spec, threads, target_s=args.ref_step_s, min_rounds=1)
+    x, _ = configs_inputs(spec)
     for _ in range(args.warmup):
-        cpu_reference_rows(spec, threads, threads)
-    times = [cpu_reference_rows(spec, rows, threads) for _ in range(args.steps)]
+        cpu_reference_rows(spec, x[:threads], threads)
+    times = [cpu_reference_rows(spec, x[:rows], threads)[0] for _ in range(args.steps)]
     per_step = statistics.mean(times)
     value = rows / per_step
+    dtc = cpu_reference_rows(spec, x[:rows], threads, combined=True)[0]
     line = {
         "metric": METRIC, "value": value, "unit": "samples/s", "impl": "reference",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_desc(spec), "batch": spec.batch, "qubits": spec.n,
-                   "layers": spec.layers, "step_sample_rows": rows},
+        "config": config_block(spec, max(world, args.gpus)),
         "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads, "kind": "port",
                          "sample": f"{rows} rows per step of cfg{spec.cfg_id} (bounded sample; "
-                                   "rows are independent so samples/s extrapolates linearly)"},
+                                   "rows are independent so samples/s extrapolates linearly); "
+                                   "reference backward semantics (Jacobian + einsum)",
+                         "cpu_model": cpu["model"], "physical_cores": cpu["physical"],
+                         "logical_cores": cpu["logical"],
+                         "vjp_equivalent": {"value": rows / dtc, "unit": "samples/s",
+                                            "call": "combined observable sum_m O_m"}},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -213,6 +352,7 @@ class GpuWorkload:
         circ, obs, wrt = configs.build(spec, configs.native_api())
         x, w = configs.inputs_and_weights(spec)
         lo, hi = split_workload(spec.batch, world)[rank]
+        self.lo, self.hi = lo, hi
         self.rows = hi - lo
         self.engine = BatchEngine(device=device)
         self.plan, self.layout = self.engine.plans.get(circ, obs, wrt, torch.device(device))
@@ -308,7 +448,48 @@ def roofline_from_profile(spec, prof: dict, steps: int, rows_total: int) -> dict
     return out
 
 
-def measure_gpu(spec, args, rank, world, device, flush_buf, with_e2e: bool, steps: int, warmup: int):
+def _rel_err(a, b) -> float:
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    if a.size == 0:
+        return 0.0
+    return float((np.abs(a - b) / np.maximum(1.0, np.abs(b))).max())
+
+
+def parity_check(spec, wl, oracle_rows=None) -> dict:
+    """The timed step's own outputs (expectations and per-row VJP rows of
+    the LAST timed step) against (a) the reference's goldens for the first
+    rows of the batch this rank holds and (b) oracle rows from the
+    cpu_baseline leg (last rows of the batch, N = 1). Tolerance 1e-10."""
+    out = {"tol": 1e-10, "checked_rows": []}
+    errs = []
+    exp = wl.expect.cpu().numpy()
+    rows = wl.rows_out.cpu().numpy()
+    P = spec.num_weights
+    try:
+        g = np.load(os.path.join(ROOT, "tests", "golden", f"cfg{spec.cfg_id}.npz"))
+        lo, hi = wl.lo, min(wl.hi, wl.lo + 8, int(g["expect"].shape[0]))
+        if hi > lo:
+            ref_w = g["jac_w"][lo:hi].sum(axis=1)
+            errs += [_rel_err(exp[:hi - lo], g["expect"][lo:hi]),
+                     _rel_err(rows[:hi - lo, :P], ref_w)]
+            if "vjp_x_rows" in g.files:
+                errs.append(_rel_err(rows[:hi - lo, P:], g["vjp_x_rows"][lo:hi]))
+            out["checked_rows"].append(f"{lo}..{hi - 1} vs reference goldens")
+    except (OSError, KeyError):
+        pass
+    if oracle_rows is not None:
+        c_lo = oracle_rows["lo"]
+        if wl.lo <= c_lo and wl.hi == spec.batch:
+            k = c_lo - wl.lo
+            errs += [_rel_err(exp[k:], oracle_rows["expect"]), _rel_err(rows[k:], oracle_rows["vjp_rows"])]
+            out["checked_rows"].append(f"{c_lo}..{spec.batch - 1} vs oracle (cpu_baseline leg)")
+    out["max_err"] = max(errs) if errs else None
+    out["ok"] = bool(errs) and max(errs) <= out["tol"]
+    return out
+
+
+def measure_gpu(spec, args, rank, world, device, flush_buf, with_e2e: bool, steps: int, warmup: int,
+                oracle_rows_fn=None):
     import torch
     import torch.distributed as dist
 
@@ -365,6 +546,11 @@ def measure_gpu(spec, args, rank, world, device, flush_buf, with_e2e: bool, step
                       "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
                       "path": "vqc_run_batch_host (numpy in/out, pinned host buffers)"}
     res["plan"] = json.loads(wl.plan.describe())
+    # e2e overwrote the device outputs only through host buffers: re-run one
+    # device step so wl.expect / wl.rows_out hold this configuration's result
+    wl.step(1)
+    torch.cuda.synchronize()
+    res["parity"] = parity_check(spec, wl, oracle_rows_fn() if oracle_rows_fn else None)
     del wl
     torch.cuda.empty_cache()
     return res
@@ -410,20 +596,76 @@ def measure_jacobian(spec, rows: int, device: str) -> dict:
     return out
 
 
+def run_dry(args, spec) -> None:
+    """--dry-run: the N > 1 plumbing without kernels (gloo): ranks shard the
+    rows with split_workload, a host-only step reduces each shard and the
+    partial sums are all-reduced once per step; max-over-ranks timing and the
+    rank-0 line are the GPU arm's."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2404_06314_b200.engine import split_workload
+    world, rank, _ = dist_setup()
+    if world > 1:
+        dist.init_process_group("gloo")
+    x, _ = configs_inputs(spec)
+    lo, hi = split_workload(spec.batch, world)[rank]
+    times = []
+    for k in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        part = torch.from_numpy(np.array([x[lo:hi].sum(), float(hi - lo)]))
+        if world > 1:
+            dist.all_reduce(part)
+        if k >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    t = torch.tensor([sum(times)], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        ms = float(t.item()) / max(1, args.steps) * 1e3
+        print(json.dumps({"metric": METRIC, "dry_run": True, "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "ms_per_step": ms,
+                          "config": config_block(spec, world),
+                          "check": {"rows": float(part[1]), "sum": float(part[0]),
+                                    "expected_sum": float(x.sum())}}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def run_ours(args, spec):
     import torch
     import torch.distributed as dist
 
     from paper_2404_06314_b200 import build, configs
     world, rank, local = dist_setup()
+    if world != args.gpus and rank == 0:
+        print(f"bench: WORLD_SIZE={world} overrides --gpus {args.gpus}", file=sys.stderr)
+    nccl_dir = None
     if world > 1:
+        if torch.cuda.device_count() < world:
+            raise SystemExit(f"bench: {world} ranks need {world} visible GPUs, "
+                             f"found {torch.cuda.device_count()}")
+        nccl_dir = nccl_log_setup()
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     device = f"cuda:{local if world > 1 else 0}"
     torch.cuda.set_device(device)
-    build.build()
+    if rank == 0:
+        build.build()
+    if world > 1:
+        dist.barrier()
     flush = torch.zeros(256 << 20 >> 3, dtype=torch.float64, device=device)
-    res = measure_gpu(spec, args, rank, world, device, flush, True, args.steps, args.warmup)
+    cpu, oracle_rows = None, None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        def oracle_rows_fn():
+            nonlocal cpu, oracle_rows
+            cpu, oracle_rows = cpu_baseline(spec, target_s=args.cpu_target_s)
+            return oracle_rows
+    else:
+        oracle_rows_fn = None
+    res = measure_gpu(spec, args, rank, world, device, flush, True, args.steps, args.warmup,
+                      oracle_rows_fn)
     sweep = []
     if world == 1 and not args.no_sweep:
         for cid in (1, 2, 3, 5):
@@ -433,31 +675,29 @@ def run_ours(args, spec):
                           "ms_per_step": r["ms_per_step"],
                           "roofline_frac_fp64": r["roofline"]["frac"],
                           "achieved_tflops": r["roofline"]["achieved"],
+                          "parity_max_err": r["parity"]["max_err"],
                           "kernels": r["kernels"], "plan": r["plan"]})
     jac = []
     if world == 1 and not args.no_sweep:
         for cid, rows in ((2, 0), (4, 2048)):
             jac.append(measure_jacobian(configs.CONFIGS[cid], rows, device))
     line = None
+    if world > 1:
+        dist.barrier()
     if rank == 0:
-        cpu = None
-        if world == 1 and not args.no_cpu:
-            cpu = cpu_baseline(spec, target_s=args.cpu_target_s)
         line = {
             "metric": METRIC, "value": res["value"], "unit": "samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded: x ~ U(-pi,pi) (B,n), weights ~ U(0,2pi); BASELINE cfg4)",
-            "config": {"workload": workload_desc(spec), "batch": spec.batch, "qubits": spec.n,
-                       "layers": spec.layers, "observables": 16, "mode": "vjp (upstream = ones)",
-                       "parallelism": f"dp{world} (row shards, split_workload; 1 NCCL all-reduce "
-                                      "of the weight grads)" if world > 1 else "dp1",
-                       "l2": "flushed between timed steps (256 MiB write); states stream through "
-                             "a >1 GiB HBM workspace"},
+            "config": config_block(spec, world),
             "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": res["e2e"],
-            "gpu_launches": res["gpu_launches"], "clocks": res["clocks"], "kernels": res["kernels"],
-            "plan": res["plan"],
+            "gpu_launches": res["gpu_launches"], "clocks": res["clocks"],
+            "parity": res["parity"], "parity_max_err": res["parity"]["max_err"],
+            "kernels": res["kernels"], "plan": res["plan"],
         }
+        if world > 1:
+            line["nccl"] = nccl_summary(nccl_dir)
         if sweep:
             line["sweep"] = sweep
         if jac:
@@ -480,11 +720,19 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-target-s", type=float, default=10.0)
     ap.add_argument("--ref-step-s", type=float, default=4.0)
+    ap.add_argument("--dry-run", action="store_true",
+                    help="host-only N-rank plumbing check on gloo (no kernels)")
     args = ap.parse_args()
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
     from paper_2404_06314_b200 import configs
     spec = configs.CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, spec)
+    elif args.dry_run:
+        run_dry(args, spec)
     else:
         run_ours(args, spec)
 

@@ -15,7 +15,6 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import native
-from .instrument import sweep_counters
 from .ir import Circuit
 from .observables import Observable, ObservablePack
 
@@ -326,14 +325,11 @@ class BatchEngine:
             if C == 0:
                 ws = self.workspace.get(plan.workspace_bytes(B, native.VQC_MODE_FORWARD), dev)
                 plan.forward(d_in, d_w, expect, ws, stream.cuda_stream)
-                sweep_counters.add_forward(B)
                 jac = None
             else:
                 ws = self.workspace.get(plan.workspace_bytes(B, native.VQC_MODE_JACOBIAN), dev)
                 jac = torch.empty((B, M, C), dtype=torch.float64, device=dev)
                 plan.adjoint(d_in, d_w, None, expect, jac, None, None, ws, stream.cuda_stream)
-                sweep_counters.add_forward(B)
-                sweep_counters.add_reverse(B, B * M)
             expect_h = expect.cpu().numpy()
             jac_h = jac.cpu().numpy() if jac is not None else np.zeros((B, M, 0))
         return BatchResult(expect_h, {n: np.ascontiguousarray(jac_h[:, :, lo:hi])
@@ -360,9 +356,24 @@ class BatchEngine:
 
     def forward_angle_rows(self, circuit: Circuit, observables, angles: np.ndarray) -> np.ndarray:
         """Expectations (rows, M) of ``circuit`` with per-row rotation angles
-        (rows, R): one GPU forward launch sequence over ``angle_circuit``."""
-        import torch
+        (rows, R): one GPU forward launch sequence over ``angle_circuit``.
+        X/Y strings on HBM plans (n > 12) run one Z-basis launch per basis
+        group over the angle circuit followed by its constant basis change
+        (the same split as ``run_batch``)."""
         ac, _ = angle_circuit(circuit)
+        if circuit.num_qubits > SMEM_MAX_QUBITS and not all(o.is_z_only for o in observables):
+            cache = ac.__dict__.setdefault("_basis_circuits", {})
+            total = None
+            for pattern, group_obs in basis_groups(observables, circuit.num_qubits):
+                if pattern not in cache:
+                    cache[pattern] = basis_circuit(ac, pattern)
+                e = self._forward_rows(cache[pattern], group_obs, angles)
+                total = e if total is None else total + e
+            return total
+        return self._forward_rows(ac, observables, angles)
+
+    def _forward_rows(self, ac: Circuit, observables, angles) -> np.ndarray:
+        import torch
         dev = self.device
         plan, _ = self.plans.get(ac, observables, (), dev)
         rows, M = angles.shape[0], len(observables)
@@ -374,7 +385,6 @@ class BatchEngine:
             expect = torch.empty((rows, M), dtype=torch.float64, device=dev)
             ws = self.workspace.get(plan.workspace_bytes(rows, native.VQC_MODE_FORWARD), dev)
             plan.forward(d_in, d_w, expect, ws, stream.cuda_stream)
-            sweep_counters.add_forward(rows)
             return expect.cpu().numpy()
 
     def _run_shifted(self, request, circuit, observables, layout, flat, inputs,

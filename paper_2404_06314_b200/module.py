@@ -25,7 +25,6 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from .instrument import sweep_counters
 from . import native
 from .engine import BatchEngine, BatchRequest, BatchResult, encoding_set
 
@@ -69,8 +68,8 @@ class QuantumFunction(torch.autograd.Function):
         expect = torch.empty((B, module.num_outputs), dtype=torch.float64, device=dev)
         if B > 0 and module.num_outputs > 0:
             ws = module._engine.workspace.get(plan.workspace_bytes(B, native.VQC_MODE_FORWARD), dev)
-            plan.forward(inputs, flat, expect, ws, torch.cuda.current_stream(dev).cuda_stream)
-            sweep_counters.add_forward(B)
+            with torch.cuda.device(dev):   # launches go to the plan's device context
+                plan.forward(inputs, flat, expect, ws, torch.cuda.current_stream(dev).cuda_stream)
         ctx.module, ctx.group = module, group
         ctx.save_for_backward(inputs, flat)
         return expect
@@ -87,10 +86,9 @@ class QuantumFunction(torch.autograd.Function):
         rows = torch.empty((B, plan.num_cols), dtype=torch.float64, device=dev)
         vsum = torch.empty((plan.num_cols,), dtype=torch.float64, device=dev)
         ws = module._engine.workspace.get(plan.workspace_bytes(B, native.VQC_MODE_VJP), dev)
-        plan.adjoint(inputs, flat, upstream, None, None, rows, vsum, ws,
-                     torch.cuda.current_stream(dev).cuda_stream)
-        sweep_counters.add_forward(B)       # the adjoint re-evolves psi forward first
-        sweep_counters.add_reverse(B, B)    # one VJP-seeded bra per row
+        with torch.cuda.device(dev):
+            plan.adjoint(inputs, flat, upstream, None, None, rows, vsum, ws,
+                         torch.cuda.current_stream(dev).cuda_stream)
         grad_flat = torch.zeros_like(flat)
         cols = module._trainable_cols
         grad_flat[module._trainable_flat] = vsum[:cols]
@@ -266,11 +264,9 @@ class QuantumModule(torch.nn.Module):
             if B > 0 and self.num_outputs > 0:
                 d_up = torch.from_numpy(np.ascontiguousarray(up)).to(dev)
                 ws = self._engine.workspace.get(plan.workspace_bytes(B, native.VQC_MODE_VJP), dev)
-                with torch.no_grad():
+                with torch.no_grad(), torch.cuda.device(dev):
                     plan.adjoint(x, self.flat_weights().detach(), d_up, None, None, None, vsum,
                                  ws, torch.cuda.current_stream(dev).cuda_stream)
-                sweep_counters.add_forward(B)
-                sweep_counters.add_reverse(B, B)
             part = vsum.cpu().numpy()
             host = part if host is None else host + part
         out, col = {}, 0
@@ -339,47 +335,3 @@ class HybridModule(torch.nn.Module):
         out = self.forward(inputs)
         out.backward(up)
         return {k: v.grad.detach().cpu().numpy().copy() for k, v in named.items()}
-
-
-# -- checkpoints (model.py:227-269: same JSON layout, so files interchange) ----
-
-def checkpoint_dict(module) -> dict:
-    quantum = module.quantum if isinstance(module, HybridModule) else module
-    out = {"sets": {n: v.tolist() for n, v in quantum.parameter_values().items()}}
-    if isinstance(module, HybridModule):
-        for block in ("pre", "post"):
-            w, b = getattr(module, f"{block}_weight"), getattr(module, f"{block}_bias")
-            out[block] = {"weight": w.detach().cpu().numpy().tolist(),
-                          "bias": b.detach().cpu().numpy().tolist()}
-    return out
-
-
-def save_checkpoint(module, path) -> None:
-    import json
-    with open(path, "w") as fh:
-        json.dump(checkpoint_dict(module), fh, indent=2)
-        fh.write("\n")
-
-
-def load_checkpoint(module, path) -> None:
-    """Restore parameter values in place; set names and shapes must match."""
-    import json
-    with open(path) as fh:
-        data = json.load(fh)
-    quantum = module.quantum if isinstance(module, HybridModule) else module
-    with torch.no_grad():
-        for name, values in data.get("sets", {}).items():
-            values = np.asarray(values, dtype=np.float64)
-            if name not in quantum.values:
-                raise ValueError(f"checkpoint set {name!r} not in module")
-            if values.shape != tuple(quantum.values[name].shape):
-                raise ValueError(f"checkpoint set {name!r} has shape {values.shape}, "
-                                 f"expected {tuple(quantum.values[name].shape)}")
-            quantum.values[name].copy_(torch.from_numpy(values))
-        if isinstance(module, HybridModule):
-            for block in ("pre", "post"):
-                if block in data:
-                    getattr(module, f"{block}_weight").copy_(
-                        torch.from_numpy(np.asarray(data[block]["weight"], np.float64)))
-                    getattr(module, f"{block}_bias").copy_(
-                        torch.from_numpy(np.asarray(data[block]["bias"], np.float64)))

@@ -36,21 +36,34 @@ def shard_rows(batch: int, world: int, rank: int) -> tuple[int, int]:
     return split_workload(batch, world)[rank]
 
 
-def allreduce_sum(vec, group=None):
-    """Sum a 1-D gradient vector over ranks in place (one collective).
+def _comm_device(group=None):
+    """Where collective buffers live: the current CUDA device under NCCL
+    (NCCL only moves device memory), host memory under gloo."""
+    import torch
+    import torch.distributed as dist
+    if dist.get_backend(group) == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
 
-    numpy input goes through a CPU tensor (gloo); torch CUDA tensors go
-    straight to NCCL.
-    """
+
+def _active(group=None) -> bool:
+    import torch.distributed as dist
+    return dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
+
+
+def allreduce_sum(vec, group=None):
+    """Sum a 1-D gradient vector over ranks (one collective). torch tensors
+    are reduced in place on their own device; numpy arrays are staged through
+    a tensor on the backend's device and returned as a new array."""
     import torch
     import torch.distributed as dist
 
-    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
+    if not _active(group):
         return vec
     if isinstance(vec, np.ndarray):
-        t = torch.from_numpy(np.ascontiguousarray(vec))
+        t = torch.from_numpy(np.ascontiguousarray(vec, np.float64)).to(_comm_device(group))
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
-        return t.numpy()
+        return t.cpu().numpy()
     dist.all_reduce(vec, op=dist.ReduceOp.SUM, group=group)
     return vec
 
@@ -67,21 +80,24 @@ def sharded_vjp(inputs: np.ndarray, upstream: np.ndarray,
 
 
 def gather_rows(local: np.ndarray, batch: int, world: int, group=None) -> np.ndarray:
-    """All-gather per-row outputs into the full (batch, ...) array on every rank."""
+    """All-gather per-row outputs into the full (batch, ...) array on every
+    rank. Shards may be empty (batch < world, batch == 0): every rank sends a
+    buffer padded to the largest shard (at least one row)."""
     import torch
     import torch.distributed as dist
 
-    if not dist.is_available() or not dist.is_initialized() or world == 1:
+    if not _active(group) or world == 1:
         return local
     ranges = split_workload(batch, world)
-    width = local.shape[1:] if local.ndim > 1 else ()
-    pad_rows = max(hi - lo for lo, hi in ranges)
+    width = tuple(local.shape[1:])
+    pad_rows = max(1, max(hi - lo for lo, hi in ranges))
     buf = np.zeros((pad_rows, *width))
     buf[: local.shape[0]] = local
-    t = torch.from_numpy(buf)
-    outs = [torch.zeros_like(t) for _ in range(world)]
+    t = torch.from_numpy(buf).to(_comm_device(group))
+    outs = [torch.empty_like(t) for _ in range(world)]
     dist.all_gather(outs, t, group=group)
-    return np.concatenate([o.numpy()[: hi - lo] for o, (lo, hi) in zip(outs, ranges)], axis=0)
+    parts = [o.cpu().numpy()[: hi - lo] for o, (lo, hi) in zip(outs, ranges)]
+    return np.concatenate(parts, axis=0).reshape(batch, *width)
 
 
 def allreduce_module_grads(module, group=None) -> None:
@@ -90,7 +106,7 @@ def allreduce_module_grads(module, group=None) -> None:
     import torch
     import torch.distributed as dist
 
-    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
+    if not _active(group):
         return
     grads = [p.grad for p in module.parameters() if p.grad is not None]
     if not grads:
@@ -121,10 +137,11 @@ def sharded_run_batch(request, run: Callable, rank: int, world: int, group=None,
                                     row_offset=request.row_offset + lo))
     if not gather:
         return local
-    M = local.expectations.shape[1]
     expect = gather_rows(local.expectations, B, world, group)
     grads = {}
     for name, g in local.gradients.items():
-        flat = gather_rows(g.reshape(g.shape[0], -1), B, world, group)
-        grads[name] = np.ascontiguousarray(flat.reshape(B, M, -1))
+        # explicit widths: numpy cannot infer -1 for a zero-row shard
+        rows, m, size = g.shape
+        flat = gather_rows(g.reshape(rows, m * size), B, world, group)
+        grads[name] = np.ascontiguousarray(flat.reshape(B, m, size))
     return BatchResult(expect, grads)

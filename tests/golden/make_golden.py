@@ -31,7 +31,9 @@ from vqckit import (AngleExpression, BatchEngine, BatchRequest, Circuit, Gate,  
 
 from paper_2404_06314_b200 import configs  # noqa: E402
 
-ROWS = {1: 32, 2: 64, 3: 32, 4: 4, 5: 2}
+# SURVEY §8(c) parity protocol: full batch for cfg1-3 comes from the oracle
+# (pinned to these rows); cfg4 the first 64 rows, cfg5 the first 8
+ROWS = {1: 32, 2: 64, 3: 32, 4: 64, 5: 8}
 THREADS = 8
 
 
@@ -65,6 +67,15 @@ def golden_config(cfg_id: int, engine: BatchEngine) -> None:
     if "x" in res.gradients:
         out["jac_x"] = res.gradients["x"]
         out["vjp_x_rows"] = np.einsum("bm,bmf->bf", up, res.gradients["x"])
+    if len(observables) > 1:
+        # the reference's VJP-equivalent call: one combined
+        # observable sum_m u_m O_m (observables.py:21-47), u = ones
+        combined = Observable(tuple(t for o in observables for t in o.terms))
+        comb = engine.run_batch(BatchRequest(circuit, [combined], {"w": w}, xs, wrt=wrt))
+        out["comb_expect"] = comb.expectations
+        out["comb_vjp_w"] = comb.gradients["w"].sum(axis=(0, 1))
+        if "x" in comb.gradients:
+            out["comb_vjp_x_rows"] = comb.gradients["x"][:, 0, :]
     np.savez_compressed(os.path.join(HERE, f"cfg{cfg_id}.npz"), **out)
     print(f"cfg{cfg_id}: {rows} rows in {dt:.1f}s", flush=True)
 
@@ -207,33 +218,9 @@ def golden_training() -> None:
     print("training: done", flush=True)
 
 
-def golden_reinforce() -> None:
-    """The reference's train_reinforce (training.py:154-193) on its cart-pole."""
-    from vqckit.cartpole import CartPoleEnv
-    from vqckit.optim import SGD
-    from vqckit.training import cartpole_policy, train_reinforce
-    policy = cartpole_policy(depth=2, seed=5, threads=1)
-    recs = train_reinforce(CartPoleEnv(), policy, episodes_per_epoch=2, epochs=3,
-                           optimizer=SGD(lr=0.05), seed=9)
-    np.savez_compressed(os.path.join(HERE, "reinforce.npz"),
-                        loss=np.array([r.loss for r in recs]),
-                        metric=np.array([r.metric for r in recs]),
-                        theta=policy.parameters()["theta"], lam=policy.parameters()["lambda"])
-    print("reinforce: done", [r.metric for r in recs], flush=True)
-
-
 def main(which=None):
     if which == "training":
-        from vqckit.datasets import synthetic_blobs
-        ds = synthetic_blobs(samples_per_class=10, num_features=3, num_classes=3, seed=4)
-        np.savez_compressed(os.path.join(HERE, "blobs.npz"), features=ds.features,
-                            labels=ds.labels, train_idx=ds.train_idx, test_idx=ds.test_idx)
-        from vqckit.datasets import load_dataset
-        tb = load_dataset(os.path.join(HERE, "toy_table.csv"), seed=2, test_fraction=0.4)
-        np.savez_compressed(os.path.join(HERE, "toy_table.npz"), features=tb.features,
-                            labels=tb.labels, train_idx=tb.train_idx, test_idx=tb.test_idx)
         golden_training()
-        golden_reinforce()
         return
     engine = BatchEngine(threads=THREADS)
     if which in (None, "random"):

@@ -91,6 +91,74 @@ def test_config_golden_vjp(torch_cuda, cfg_id):
         assert close(rows.cpu().numpy()[:, lo:hi], g["vjp_x_rows"]) < TOL
 
 
+def _vjp_device(torch, eng, circ, obs, wrt, w, x, up):
+    """vqc_adjoint in VJP mode on device buffers: (expect, per-row VJP rows, summed VJP)."""
+    from paper_2404_06314_b200 import native
+    plan, layout = eng.plans.get(circ, obs, wrt, eng.device)
+    dev = eng.device
+    B, M = len(x), len(obs)
+    flat = eng.base_flat(circ, {"w": w})
+    d_x, d_w = torch.from_numpy(x).to(dev), torch.from_numpy(flat).to(dev)
+    d_up = torch.from_numpy(np.ascontiguousarray(up)).to(dev)
+    rows = torch.empty((B, layout.n_cols), dtype=torch.float64, device=dev)
+    vsum = torch.empty((layout.n_cols,), dtype=torch.float64, device=dev)
+    expect = torch.empty((B, M), dtype=torch.float64, device=dev)
+    ws = torch.empty(plan.workspace_bytes(B, native.VQC_MODE_VJP), dtype=torch.uint8, device=dev)
+    plan.adjoint(d_x, d_w, d_up, expect, None, rows, vsum, ws, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    return expect.cpu().numpy(), rows.cpu().numpy(), vsum.cpu().numpy()
+
+
+@pytest.mark.parametrize("cfg_id", [1, 2, 3])
+def test_config_full_batch_vs_oracle(torch_cuda, cfg_id):
+    """SURVEY §8(c) protocol: the FULL batch of cfg1-3 (cfg3: 4096 rows, so
+    every CTA index of the on-chip kernel, rows 4032-4095 included) in
+    Jacobian mode and in VJP mode with a row-dependent upstream, against the
+    oracle (itself pinned to the reference goldens)."""
+    torch = torch_cuda
+    from paper_2404_06314_b200 import configs
+    spec = configs.CONFIGS[cfg_id]
+    circ, obs, wrt = configs.build(spec, configs.native_api())
+    x, w = configs.inputs_and_weights(spec)
+    e_ref, j_ref = oracle_batch(circ, obs, {"w": w}, x, wrt)
+    eng = _engine()
+    res = eng.run_batch(_request(circ, obs, {"w": w}, x, wrt))
+    assert res.expectations.shape == (spec.batch, len(obs))
+    assert close(res.expectations, e_ref) < TOL
+    for k in wrt:
+        assert close(res.gradients[k], j_ref[k]) < TOL
+    hi = slice(spec.batch - 64, spec.batch)   # the last CTAs of the launch
+    for k in wrt:
+        assert close(res.gradients[k][hi], j_ref[k][hi]) < TOL
+    up = np.random.default_rng(cfg_id).normal(size=(spec.batch, len(obs)))
+    e, rows, vsum = _vjp_device(torch, eng, circ, obs, wrt, w, x, up)
+    ref_rows = np.concatenate([np.einsum("bm,bmp->bp", up, j_ref[k]) for k in wrt], axis=1)
+    assert close(e, e_ref) < TOL
+    assert close(rows, ref_rows) < TOL
+    assert close(vsum, ref_rows.sum(axis=0)) < 1e-10 * max(1.0, np.abs(ref_rows).sum(axis=0).max())
+
+
+def test_combined_observable_vjp_matches_reference_call(torch_cuda):
+    """The VJP kernel (one bra seeded with sum_m O_m psi) equals the
+    reference's own VJP-equivalent call, run_batch with one combined
+    observable (goldens comb_*, cfg2 and cfg4)."""
+    torch = torch_cuda
+    from paper_2404_06314_b200 import configs
+    for cfg_id in (2, 4):
+        g = _golden(f"cfg{cfg_id}.npz")
+        if "comb_vjp_w" not in g.files:
+            pytest.skip("goldens predate the combined-observable fixtures")
+        spec = configs.CONFIGS[cfg_id]
+        circ, obs, wrt = configs.build(spec, configs.native_api())
+        x = g["x_rows"]
+        e, rows, vsum = _vjp_device(torch, _engine(), circ, obs, wrt, g["w"], x,
+                                    np.ones((len(x), len(obs))))
+        P = spec.num_weights
+        assert close(e.sum(axis=1), g["comb_expect"][:, 0]) < TOL
+        assert close(vsum[:P], g["comb_vjp_w"]) < TOL
+        assert close(rows[:, P:], g["comb_vjp_x_rows"]) < TOL
+
+
 def _random_cases():
     path = os.path.join(GOLDEN, "random.npz")
     if not os.path.exists(path):

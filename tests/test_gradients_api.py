@@ -67,3 +67,52 @@ def test_gpu_single_binding_methods(oracle_mod, seed):
         assert close(sp.gradients[k], v) < TOL
     empty = G.adjoint_gradients(circ, b, [], wrt)
     assert empty.expectations.shape == (0,) and empty.gradients["w"].shape == (0, 5)
+
+
+@pytest.mark.gpu
+def test_gpu_spsa_fd_xy_observables_hbm_plan(oracle_mod):
+    """SPSA and finite differences with X/Y strings at n = 13 (HBM plans are
+    Z-only at the ABI): both must take the basis-group split like run_batch."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required")
+    from paper_2404_06314_b200 import gradients as G
+    circ, obs, b = _case(3, n=13)
+    assert not all(o.is_z_only for o in obs)
+    wrt = ("w", "s")
+    e_ref, j_ref, layout, flat = _oracle(oracle_mod, circ, obs, b, wrt)
+    split = lambda j: {n: j[:, lo:hi] for n, lo, hi in layout.slices}  # noqa: E731
+    fd = G.finite_difference_gradients(circ, b, obs, wrt)
+    assert close(fd.expectations, e_ref) < TOL
+    for k, v in split(j_ref).items():
+        assert np.abs(fd.gradients[k] - v).max() < 1e-5
+    sp = G.spsa_gradients(circ, b, obs, wrt, c=0.01, samples=2, seed=4)
+    e_o, j_o = oracle_mod.spsa_row(lowered(circ, obs), flat, layout.flat_of_col, 0.01, 2,
+                                   np.random.default_rng(4))
+    assert close(sp.expectations, e_o) < TOL
+    for k, v in split(j_o).items():
+        assert close(sp.gradients[k], v) < TOL
+
+
+@pytest.mark.gpu
+def test_gpu_spsa_row_offset_slices_bitwise():
+    """run_batch(method='spsa') on two row slices with matching row_offset
+    concatenates to the full-batch result bit for bit (rank sharding)."""
+    import dataclasses
+
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required")
+    from paper_2404_06314_b200 import configs
+    from paper_2404_06314_b200.engine import BatchEngine, BatchRequest
+    spec = configs.CONFIGS[2]
+    circ, obs, wrt = configs.build(spec, configs.native_api())
+    x, w = configs.inputs_and_weights(spec, batch=10)
+    eng = BatchEngine(device="cuda:0")
+    req = BatchRequest(circ, obs, {"w": w}, x, method="spsa", wrt=wrt, seed=9, spsa_samples=2)
+    full = eng.run_batch(req)
+    a = eng.run_batch(dataclasses.replace(req, inputs=x[:4]))
+    b = eng.run_batch(dataclasses.replace(req, inputs=x[4:], row_offset=4))
+    assert np.array_equal(np.concatenate([a.expectations, b.expectations]), full.expectations)
+    for k in full.gradients:
+        assert np.array_equal(np.concatenate([a.gradients[k], b.gradients[k]]), full.gradients[k])

@@ -147,3 +147,52 @@ def test_sharded_run_batch_spsa_seeds_are_global(tmp_path):
         np.testing.assert_array_equal(d["exp"], full.expectations)
         for k in wrt:
             np.testing.assert_array_equal(d[f"g_{k}"], full.gradients[k])
+
+
+def _tiny_run(req):
+    """Per-rank stand-in with the engine's output shapes: (b, M) and (b, M, size)."""
+    from paper_2404_06314_b200.engine import BatchResult
+    x = np.asarray(req.inputs)
+    b = x.shape[0]
+    e = np.stack([x.sum(axis=1), x[:, 0] if b else np.zeros(0)], axis=1) if b else np.zeros((0, 2))
+    g = np.repeat(x[:, None, :], 2, axis=1) + req.row_offset
+    return BatchResult(e, {"x": g})
+
+
+def _empty_worker(rank, world, port, out_dir):
+    import torch.distributed as dist
+
+    from paper_2404_06314_b200 import parallel
+    from paper_2404_06314_b200.engine import BatchRequest
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        for B in (1, 0):
+            x = np.arange(3.0 * B).reshape(B, 3)
+            req = BatchRequest(None, [], {}, x)
+            res = parallel.sharded_run_batch(req, _tiny_run, rank, world)
+            np.savez(os.path.join(out_dir, f"e{B}_{rank}.npz"), exp=res.expectations,
+                     g=res.gradients["x"])
+        v = parallel.allreduce_sum(np.array([1.0, 2.0]))
+        np.save(os.path.join(out_dir, f"v{rank}.npy"), v)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_sharded_run_batch_empty_shards(tmp_path):
+    """B < world (a rank gets no rows) and B == 0 must not hang or raise."""
+    world = 2
+    mp.start_processes(_empty_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world,
+                       start_method="spawn")
+    for B in (1, 0):
+        x = np.arange(3.0 * B).reshape(B, 3)
+        from paper_2404_06314_b200.engine import BatchRequest
+        full = _tiny_run(BatchRequest(None, [], {}, x))
+        for r in range(world):
+            d = np.load(tmp_path / f"e{B}_{r}.npz")
+            assert d["exp"].shape == (B, 2) and d["g"].shape == (B, 2, 3)
+            np.testing.assert_array_equal(d["exp"], full.expectations)
+            np.testing.assert_array_equal(d["g"], full.gradients["x"])
+    for r in range(world):
+        np.testing.assert_array_equal(np.load(tmp_path / f"v{r}.npy"), [2.0, 4.0])
