@@ -61,6 +61,17 @@ def fp64_peak() -> tuple[float, str]:
         return FP64_PEAK_FALLBACK, "measured earlier on this pool (tools/probe_peaks.cu)"
 
 
+def fp32_peak() -> tuple[float, str]:
+    """FFMA throughput (complex64 mode's pipe): measured by tools/probe_peaks.cu
+    when profiles/peaks_fp64.json carries it, else twice the FP64 figure
+    (B200: 128 FP32 vs 64 FP64 lanes per SM)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "peaks_fp64.json")) as fh:
+            return float(json.load(fh)["fp32_fma_tflops"]), "measured (tools/probe_peaks.cu FFMA loop)"
+    except Exception:
+        return 2.0 * fp64_peak()[0], "2 x the measured FP64 DFMA figure (128 vs 64 lanes per SM)"
+
+
 def hbm_peak() -> float:
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -342,7 +353,7 @@ def run_reference(args, spec):
 # ----------------------------------------------------------------------------- GPU arm
 
 class GpuWorkload:
-    def __init__(self, spec, rank: int, world: int, device):
+    def __init__(self, spec, rank: int, world: int, device, precision: str = "complex128"):
         import torch
 
         from paper_2404_06314_b200 import configs, native
@@ -354,7 +365,8 @@ class GpuWorkload:
         lo, hi = split_workload(spec.batch, world)[rank]
         self.lo, self.hi = lo, hi
         self.rows = hi - lo
-        self.engine = BatchEngine(device=device)
+        self.precision = precision
+        self.engine = BatchEngine(device=device, precision=precision)
         self.plan, self.layout = self.engine.plans.get(circ, obs, wrt, torch.device(device))
         self.flat = self.engine.base_flat(circ, {"w": w})
         self.x_host = np.ascontiguousarray(x[lo:hi])
@@ -408,9 +420,10 @@ class GpuWorkload:
         return h2d, d2h
 
 
-def roofline_from_profile(spec, prof: dict, steps: int, rows_total: int) -> dict:
+def roofline_from_profile(spec, prof: dict, steps: int, rows_total: int,
+                          precision: str = "complex128") -> dict:
     from paper_2404_06314_b200 import configs
-    peak, how = fp64_peak()
+    peak, how = fp64_peak() if precision == "complex128" else fp32_peak()
     evo = {k: v for k, v in prof.items() if k.startswith("pass_") or k.startswith("smem_")}
     evo_ms = sum(v[0] for v in evo.values()) / steps
     evo_launches = sum(v[1] for v in evo.values()) / steps
@@ -418,7 +431,8 @@ def roofline_from_profile(spec, prof: dict, steps: int, rows_total: int) -> dict
     achieved = flops / (evo_ms * 1e-3) / 1e12 if evo_ms > 0 else 0.0
     total_ms = sum(v[0] for v in prof.values()) / steps
     out = {
-        "bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+        "bound": "fp64" if precision == "complex128" else "fp32", "achieved": achieved, "peak": peak,
+        "unit": "TFLOP/s",
         "frac": achieved / peak, "traffic": None,
         "kernel": "+".join(sorted(evo)) if evo else None,
         "kernel_share_of_step": evo_ms / total_ms if total_ms > 0 else None,
@@ -460,7 +474,7 @@ def parity_check(spec, wl, oracle_rows=None) -> dict:
     the LAST timed step) against (a) the reference's goldens for the first
     rows of the batch this rank holds and (b) oracle rows from the
     cpu_baseline leg (last rows of the batch, N = 1). Tolerance 1e-10."""
-    out = {"tol": 1e-10, "checked_rows": []}
+    out = {"tol": 1e-10 if wl.precision == "complex128" else 1e-5, "checked_rows": []}
     errs = []
     exp = wl.expect.cpu().numpy()
     rows = wl.rows_out.cpu().numpy()
@@ -489,12 +503,12 @@ def parity_check(spec, wl, oracle_rows=None) -> dict:
 
 
 def measure_gpu(spec, args, rank, world, device, flush_buf, with_e2e: bool, steps: int, warmup: int,
-                oracle_rows_fn=None):
+                oracle_rows_fn=None, precision: str = "complex128"):
     import torch
     import torch.distributed as dist
 
     from paper_2404_06314_b200 import native
-    wl = GpuWorkload(spec, rank, world, device)
+    wl = GpuWorkload(spec, rank, world, device, precision)
     for _ in range(warmup):
         wl.step(world)
     torch.cuda.synchronize()
@@ -526,7 +540,7 @@ def measure_gpu(spec, args, rank, world, device, flush_buf, with_e2e: bool, step
     res = {"value": value, "ms_per_step": ms_per_step, "gpu_launches": launches, "clocks": clk,
            "kernels": {k: {"ms_per_step": v[0] / steps, "launches_per_step": v[1] / steps}
                        for k, v in prof.items()},
-           "roofline": roofline_from_profile(spec, prof, steps, wl.rows)}
+           "roofline": roofline_from_profile(spec, prof, steps, wl.rows, precision)}
     if with_e2e:
         for _ in range(max(1, warmup)):
             wl.step_host(world)
@@ -676,6 +690,18 @@ def run_ours(args, spec):
                           "roofline_frac_fp64": r["roofline"]["frac"],
                           "achieved_tflops": r["roofline"]["achieved"],
                           "parity_max_err": r["parity"]["max_err"],
+                          "kernels": r["kernels"], "plan": r["plan"]})
+    if world == 1 and not args.no_sweep:
+        # the optional complex64 mode (north star: 1e-5), same workloads
+        for cid in (3, 4, 5):
+            s = configs.CONFIGS[cid]
+            r = measure_gpu(s, args, rank, world, device, flush, False, 3, 2, precision="complex64")
+            sweep.append({"config": workload_desc(s).replace("complex128", "complex64"),
+                          "precision": "complex64", "value": r["value"], "unit": "samples/s",
+                          "ms_per_step": r["ms_per_step"],
+                          "roofline_frac_fp32": r["roofline"]["frac"],
+                          "achieved_tflops": r["roofline"]["achieved"],
+                          "parity_max_err": r["parity"]["max_err"], "parity_tol": r["parity"]["tol"],
                           "kernels": r["kernels"], "plan": r["plan"]})
     jac = []
     if world == 1 and not args.no_sweep:

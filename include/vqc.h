@@ -87,7 +87,9 @@ typedef struct VqcPlan VqcPlan;
  * builds the rotation/angle tables, the WrtLayout chain-rule table
  * (gradients.py:58-77, _kernels.py:269-278) and the pass/segment schedule,
  * and uploads them to the current device. wrt_col has total_params entries,
- * each an output column or -1. precision: 0 = complex128 (only mode). */
+ * each an output column or -1. precision: 0 = complex128 states, 1 = complex64
+ * states (JIT kernels; angles, block matrices, reductions and all outputs stay
+ * float64; parity target 1e-5 against the complex128 reference). */
 int vqc_plan_create(const VqcCircuit* circuit, const VqcObservables* obs, const int64_t* wrt_col,
                     int precision, VqcPlan** out);
 void vqc_plan_destroy(VqcPlan* plan);

@@ -357,6 +357,7 @@ Layout make_layout(const VqcPlan* p, int64_t B, int mode) {
   const int64_t N = (int64_t)1 << P.n;
   const int M = p->M;
   L.K = mode == VQC_MODE_JACOBIAN ? std::max(M, 1) : 1;
+  const size_t esz = P.precision == 1 ? 8 : 16;
   size_t off = 0;
   auto take = [&](size_t bytes) {
     const size_t o = off;
@@ -368,7 +369,7 @@ Layout make_layout(const VqcPlan* p, int64_t B, int mode) {
   L.rows = take(mode == VQC_MODE_VJP ? (size_t)B * P.n_cols * sizeof(double) : 0);
   if (!P.hbm) {
     L.chunk = B;
-    L.fin = take(mode == VQC_MODE_JACOBIAN && M > 1 ? (size_t)B * N * 16 : 0);
+    L.fin = take(mode == VQC_MODE_JACOBIAN && M > 1 ? (size_t)B * N * esz : 0);
     // small on-chip states: per-sample tables from k_tables (one CTA per sample,
     // rotations in parallel) instead of a serial dependent-load chain per CTA
     const int64_t st = 2 * (int64_t)P.n_rot + 8 * (int64_t)P.n_blk + 4 * (int64_t)P.n_av;
@@ -379,14 +380,14 @@ Layout make_layout(const VqcPlan* p, int64_t B, int mode) {
   } else {
     L.n_tiles = 1 << (P.n - P.k);
     const int nstates = mode == VQC_MODE_FORWARD ? 1 : (mode == VQC_MODE_VJP ? 2 : 3);
-    const size_t per = (size_t)nstates * N * 16 + (size_t)L.K * P.NG * L.n_tiles * 8 +
+    const size_t per = (size_t)nstates * N * esz + (size_t)L.K * P.NG * L.n_tiles * 8 +
                        (size_t)M * L.n_tiles * 8;
     int64_t chunk = (int64_t)(p->state_budget / std::max<size_t>(per, 1));
     chunk = std::max<int64_t>(1, std::min<int64_t>(chunk, B));
     L.chunk = chunk;
-    L.psi = take((size_t)chunk * N * 16);
-    L.phi = take(adj ? (size_t)chunk * N * 16 : 0);
-    L.fin = take(mode == VQC_MODE_JACOBIAN ? (size_t)chunk * N * 16 : 0);
+    L.psi = take((size_t)chunk * N * esz);
+    L.phi = take(adj ? (size_t)chunk * N * esz : 0);
+    L.fin = take(mode == VQC_MODE_JACOBIAN ? (size_t)chunk * N * esz : 0);
     L.ipart = take(adj ? (size_t)chunk * L.K * P.NG * L.n_tiles * 8 : 0);
     const int ftiles = p->fwd ? 1 << (p->fwd->prog.n - p->fwd->prog.k) : L.n_tiles;
     L.epart = take((size_t)chunk * M * std::max(L.n_tiles, ftiles) * 8);
@@ -404,6 +405,9 @@ Layout make_layout(const VqcPlan* p, int64_t B, int mode) {
 
 int red_slots(const VqcPlan* p) { return std::max(1, std::max(p->M, p->prog.max_red_per_seg)); }
 
+// bytes per state element: complex128 or complex64
+int elem_bytes(const VqcPlan* p) { return p->prog.precision == 1 ? 8 : 16; }
+
 // samples per CTA in smem mode
 int smem_samples(const VqcPlan* p, int64_t B, bool dual, size_t* smem_bytes, int* threads_per_sample) {
   const HostProgram& P = p->prog;
@@ -413,12 +417,14 @@ int smem_samples(const VqcPlan* p, int64_t B, bool dual, size_t* smem_bytes, int
   *threads_per_sample = TT;
   auto bytes_for = [&](int S) {
     return SmemLayout(S, 1 << P.n, dual, P.n_rot, P.n_blk, P.n_av, red_slots(p), S * TT, p->M,
-                      (int)p->smask.size()).total;
+                      (int)p->smask.size(), elem_bytes(p)).total;
   };
   const int max_threads = P.R >= 5 ? 256 : (split ? 512 : (P.R >= 4 ? 256 : 512));
   int smax = std::max(1, max_threads / TT);
   const int64_t want = std::max<int64_t>(1, (B + 2 * p->sms - 1) / (2 * p->sms));
   int S = 1;
+  // JIT kernels of n >= 12 lag their reductions, which assumes one sample per CTA
+  if (p->use_jit && P.n >= 12) smax = 1;
   while (S * 2 <= smax && S * 2 <= want && bytes_for(S * 2) <= (size_t)kMaxSmemBytes) S *= 2;
   *smem_bytes = bytes_for(S);
   return S;
@@ -430,7 +436,7 @@ size_t pass_smem(const VqcPlan* p, const HostProgram& P, bool dual, int rs = -1)
   const int TPS = 1 << (P.k - P.R);
   return SmemLayout(1, 1 << P.k, dual, P.max_rot_per_pass, P.max_blk_per_pass, P.max_av_per_pass,
                     rs < 0 ? red_slots(p) : rs, (dual && !P.adj_dual) ? 2 * TPS : TPS, p->M,
-                    (int)p->smask.size()).total;
+                    (int)p->smask.size(), elem_bytes(p)).total;
 }
 
 int launch(const char* name, Kern k, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
@@ -785,6 +791,7 @@ int64_t vqc_jit_source(const VqcCircuit* c, const int64_t* wrt_col, int compile,
   if (int rc = schedule_circuit(c, wrt_col, &prog, &zm, &zc)) return rc;
   if ((prog.hbm || env_int("VQC_SMEM_DUAL", 0) != 0) && env_int("VQC_ADJ_DUAL", prog.R <= 3 ? 1 : 0) != 0)
     prog.adj_dual = true;
+  prog.precision = env_int("VQC_JIT_SOURCE_PRECISION", 0) == 1 ? 1 : 0;  // dump / compile a complex64 plan
   build_thr_table(prog.segs);  // per-segment thread-table offsets, as at plan creation
   const bool split = use_split(prog.n, prog.R) && !prog.adj_dual;
   const std::string src = jit_source(prog, split);
@@ -842,7 +849,10 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
   g_err.clear();
   if (!c || !obs || !out) return fail(VQC_E_INVALID, "NULL argument");
   *out = nullptr;
-  if (precision != 0) return fail(VQC_E_UNSUPPORTED, "only complex128 precision (0) is implemented");
+  if (precision != 0 && precision != 1)
+    return fail(VQC_E_INVALID, "precision must be 0 (complex128) or 1 (complex64), got " + std::to_string(precision));
+  if (precision == 1 && env_int("VQC_JIT", -1) == 0)
+    return fail(VQC_E_UNSUPPORTED, "complex64 plans run JIT-compiled kernels only (VQC_JIT=0 set)");
   if (c->n_qubits < 1 || c->n_qubits > kMaxQubits)
     return fail(VQC_E_INVALID, "num_qubits must be in [1, 24], got " + std::to_string(c->n_qubits));
   if (c->n_gates < 0 || c->total_params < 0) return fail(VQC_E_INVALID, "negative sizes");
@@ -903,6 +913,7 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
     delete p;
     return rc;
   }
+  p->prog.precision = precision;
   std::string err;
   cudaError_t e = cudaGetDevice(&p->device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, p->device);
@@ -927,8 +938,9 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
   // segment code, one unit); 1 = every plan, 0 = interpreter only. Small
   // circuits are launch-bound and stay on the prebuilt interpreter.
   const int jit_mode = env_int("VQC_JIT", -1);
-  const bool want_jit = jit_mode > 0 || (jit_mode < 0 && (P.hbm || P.n >= 8));
-  if (want_jit && P.n_fwd_ops + P.n_bwd_ops > 0) {
+  // complex64 plans always specialise (the interpreter kernels are complex128)
+  const bool want_jit = precision == 1 || jit_mode > 0 || (jit_mode < 0 && (P.hbm || P.n >= 8));
+  if (want_jit && (P.n_fwd_ops + P.n_bwd_ops > 0 || precision == 1)) {
     // HBM adjoint with both states per thread when its register slots allow
     // (VQC_ADJ_DUAL overrides: 0 = thread pairs)
     if ((P.hbm || (P.R <= 3 && env_int("VQC_SMEM_DUAL", 0) != 0)) && env_int("VQC_ADJ_DUAL", P.R <= 3 ? 1 : 0) != 0)
@@ -951,6 +963,7 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
         vqc_plan_destroy(p);
         return rc;
       }
+      f->prog.precision = precision;
       if (!f->prog.hbm || f->prog.NG != P.NG) {
         vqc_plan_destroy(p);
         return fail(VQC_E_UNSUPPORTED, "forward schedule disagrees with the adjoint schedule");
@@ -1006,13 +1019,14 @@ int64_t vqc_plan_describe(const VqcPlan* p, char* buf, int64_t cap) {
                            "\"passes\": %d, \"segments\": %d, \"rotations\": %d, \"grad_slots\": %d, "
                            "\"fwd_ops\": %d, \"bwd_ops\": %d, \"cols\": %d, \"obs\": %d, \"jit\": %s, "
                            "\"jit_compile_s\": %.3f, \"jit_cubin_bytes\": %zu, \"absorbed_gates\": %d, \"adjoint_dual\": %s, "
-                           "\"fwd_tile_qubits\": %d, \"fwd_reg_slots\": %d, \"fwd_passes\": %d}",
+                           "\"fwd_tile_qubits\": %d, \"fwd_reg_slots\": %d, \"fwd_passes\": %d, \"precision\": \"%s\"}",
                            P.n, P.hbm ? "hbm" : "smem", P.k, P.R, (int)P.passes.size(), nseg, P.n_rot,
                            P.NG, P.n_fwd_ops, P.n_bwd_ops, P.n_cols, p->M, p->use_jit ? "true" : "false",
                            p->jit.compile_s + (p->fwd ? p->fwd->jit.compile_s : 0.0),
                            p->jit.cubin_bytes + (p->fwd ? p->fwd->jit.cubin_bytes : 0), P.absorbed,
                            P.adj_dual ? "true" : "false", p->fwd ? p->fwd->prog.k : P.k,
-                           p->fwd ? p->fwd->prog.R : P.R, (int)(p->fwd ? p->fwd->prog.passes.size() : P.passes.size()));
+                           p->fwd ? p->fwd->prog.R : P.R, (int)(p->fwd ? p->fwd->prog.passes.size() : P.passes.size()),
+                           P.precision == 1 ? "complex64" : "complex128");
   if (buf && cap > 0) {
     const int64_t c = std::min<int64_t>(cap - 1, len);
     memcpy(buf, tmp, (size_t)c);

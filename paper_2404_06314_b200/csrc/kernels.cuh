@@ -26,6 +26,21 @@ struct IC {
   static constexpr int value = V;
 };
 
+// State element type. complex128 by default; a plan created with precision
+// 1 (complex64) is JIT-compiled with VQC_C64 defined: states, registers and
+// gate arithmetic are single precision, while angles, fused-block matrices,
+// inner-product reductions, expectations and gradients stay float64 (the
+// north star's optional complex64 mode, 1e-5 against the reference).
+#ifdef VQC_C64
+typedef float real_t;
+typedef float2 cplx_t;
+__device__ __forceinline__ cplx_t mk_c(real_t a, real_t b) { return make_float2(a, b); }
+#else
+typedef double real_t;
+typedef double2 cplx_t;
+__device__ __forceinline__ cplx_t mk_c(real_t a, real_t b) { return make_double2(a, b); }
+#endif
+
 struct DevProgram {
   const Op* ops;
   const SegDesc* segs;
@@ -66,9 +81,9 @@ struct RunArgs {
   int bra;                 // Jacobian bra for this launch (-1: VJP seed / all in-kernel)
   double* expect;          // (nb, M, n_tiles) rows relative to b0
   double* ip;              // (nb, K, NG, n_tiles) rows relative to b0
-  double2* psi;            // HBM mode: (nb, 2^n) state buffers, row relative to b0
-  double2* phi;
-  double2* psi_fin;        // HBM Jacobian / smem Jacobian scratch
+  cplx_t* psi;             // HBM mode: (nb, 2^n) state buffers, row relative to b0
+  cplx_t* phi;
+  cplx_t* psi_fin;        // HBM Jacobian / smem Jacobian scratch
   int pass;
   uint32_t flags;
   int S;                   // samples per CTA (smem mode)
@@ -103,6 +118,9 @@ __device__ __forceinline__ double neg_if(double x, bool c) {
   const int hi = __double2hiint(x) ^ (c ? (int)0x80000000 : 0);
   return __hiloint2double(hi, __double2loint(x));
 }
+__device__ __forceinline__ float neg_if(float x, bool c) {
+  return __int_as_float(__float_as_int(x) ^ (c ? (int)0x80000000 : 0));
+}
 
 __device__ __forceinline__ double flat_val(const DevProgram& D, const RunArgs& A, int64_t b, int idx) {
   const int64_t e = (int64_t)idx - D.enc_off;
@@ -134,52 +152,52 @@ __device__ __forceinline__ void with_slot(uint32_t s, F&& f) {
 
 // RX: a0' = c a0 - i s a1 ; a1' = -i s a0 + c a1   (_kernels.py:32-42)
 template <int R, int S>
-__device__ __forceinline__ void g_rx(double2 (&a)[1 << R], double c, double s) {
+__device__ __forceinline__ void g_rx(cplx_t (&a)[1 << R], real_t c, real_t s) {
 #pragma unroll
   for (int i = 0; i < (1 << R); ++i)
     if (!((i >> S) & 1)) {
       const int j = i | (1 << S);
-      const double2 x = a[i], y = a[j];
-      a[i] = make_double2(c * x.x + s * y.y, c * x.y - s * y.x);
-      a[j] = make_double2(s * x.y + c * y.x, c * y.y - s * x.x);
+      const cplx_t x = a[i], y = a[j];
+      a[i] = mk_c(c * x.x + s * y.y, c * x.y - s * y.x);
+      a[j] = mk_c(s * x.y + c * y.x, c * y.y - s * x.x);
     }
 }
 
 // RY: a0' = c a0 - s a1 ; a1' = s a0 + c a1   (_kernels.py:45-55)
 template <int R, int S>
-__device__ __forceinline__ void g_ry(double2 (&a)[1 << R], double c, double s) {
+__device__ __forceinline__ void g_ry(cplx_t (&a)[1 << R], real_t c, real_t s) {
 #pragma unroll
   for (int i = 0; i < (1 << R); ++i)
     if (!((i >> S) & 1)) {
       const int j = i | (1 << S);
-      const double2 x = a[i], y = a[j];
-      a[i] = make_double2(c * x.x - s * y.x, c * x.y - s * y.y);
-      a[j] = make_double2(s * x.x + c * y.x, s * x.y + c * y.y);
+      const cplx_t x = a[i], y = a[j];
+      a[i] = mk_c(c * x.x - s * y.x, c * x.y - s * y.y);
+      a[j] = mk_c(s * x.x + c * y.x, s * x.y + c * y.y);
     }
 }
 
 // H (_kernels.py:69-78)
 template <int R, int S>
-__device__ __forceinline__ void g_h(double2 (&a)[1 << R]) {
-  const double inv = 0.70710678118654746;  // 1.0 / np.sqrt(2.0) as float64
+__device__ __forceinline__ void g_h(cplx_t (&a)[1 << R]) {
+  const real_t inv = (real_t)0.70710678118654746;  // 1.0 / np.sqrt(2.0) as float64
 #pragma unroll
   for (int i = 0; i < (1 << R); ++i)
     if (!((i >> S) & 1)) {
       const int j = i | (1 << S);
-      const double2 x = a[i], y = a[j];
-      a[i] = make_double2((x.x + y.x) * inv, (x.y + y.y) * inv);
-      a[j] = make_double2((x.x - y.x) * inv, (x.y - y.y) * inv);
+      const cplx_t x = a[i], y = a[j];
+      a[i] = mk_c((x.x + y.x) * inv, (x.y + y.y) * inv);
+      a[j] = mk_c((x.x - y.x) * inv, (x.y - y.y) * inv);
     }
 }
 
 // X: swap pairs (_kernels.py:81-88) — pure register renaming
 template <int R, int S>
-__device__ __forceinline__ void g_x(double2 (&a)[1 << R]) {
+__device__ __forceinline__ void g_x(cplx_t (&a)[1 << R]) {
 #pragma unroll
   for (int i = 0; i < (1 << R); ++i)
     if (!((i >> S) & 1)) {
       const int j = i | (1 << S);
-      const double2 t = a[i];
+      const cplx_t t = a[i];
       a[i] = a[j];
       a[j] = t;
     }
@@ -187,13 +205,13 @@ __device__ __forceinline__ void g_x(double2 (&a)[1 << R]) {
 
 // CNOT with both qubits in registers (_kernels.py:91-100)
 template <int R, int C, int T>
-__device__ __forceinline__ void g_cnot_rr(double2 (&a)[1 << R]) {
+__device__ __forceinline__ void g_cnot_rr(cplx_t (&a)[1 << R]) {
   if constexpr (C != T) {
 #pragma unroll
     for (int i = 0; i < (1 << R); ++i)
       if (((i >> C) & 1) && !((i >> T) & 1)) {
         const int j = i | (1 << T);
-        const double2 t = a[i];
+        const cplx_t t = a[i];
         a[i] = a[j];
         a[j] = t;
       }
@@ -202,12 +220,12 @@ __device__ __forceinline__ void g_cnot_rr(double2 (&a)[1 << R]) {
 
 // CNOT with a per-thread constant control bit
 template <int R, int T>
-__device__ __forceinline__ void g_cnot_cr(double2 (&a)[1 << R], bool ctrl) {
+__device__ __forceinline__ void g_cnot_cr(cplx_t (&a)[1 << R], bool ctrl) {
 #pragma unroll
   for (int i = 0; i < (1 << R); ++i)
     if (!((i >> T) & 1)) {
       const int j = i | (1 << T);
-      const double2 x = a[i], y = a[j];
+      const cplx_t x = a[i], y = a[j];
       a[i] = ctrl ? y : x;
       a[j] = ctrl ? x : y;
     }
@@ -215,24 +233,24 @@ __device__ __forceinline__ void g_cnot_cr(double2 (&a)[1 << R], bool ctrl) {
 
 // diagonal RZ phase: bit 0 -> e^{-i s}, bit 1 -> e^{+i s} (_kernels.py:58-66)
 template <int R>
-__device__ __forceinline__ void g_rz(double2 (&a)[1 << R], double c, double s, uint32_t slot_mask,
+__device__ __forceinline__ void g_rz(cplx_t (&a)[1 << R], real_t c, real_t s, uint32_t slot_mask,
                                      bool cbit) {
 #pragma unroll
   for (int i = 0; i < (1 << R); ++i) {
     const bool one = slot_mask ? ((i & slot_mask) != 0) : cbit;
-    const double t = one ? s : -s;
-    const double2 x = a[i];
-    a[i] = make_double2(c * x.x - t * x.y, c * x.y + t * x.x);
+    const real_t t = one ? s : -s;
+    const cplx_t x = a[i];
+    a[i] = mk_c(c * x.x - t * x.y, c * x.y + t * x.x);
   }
 }
 
 // CZ: negate where both bits are 1 (sign-bit flips, no FP64 work)
 template <int R>
-__device__ __forceinline__ void g_cz(double2 (&a)[1 << R], uint32_t mask, bool cond) {
+__device__ __forceinline__ void g_cz(cplx_t (&a)[1 << R], uint32_t mask, bool cond) {
 #pragma unroll
   for (int i = 0; i < (1 << R); ++i) {
     const bool neg = cond && ((i & mask) == mask);
-    a[i] = make_double2(neg_if(a[i].x, neg), neg_if(a[i].y, neg));
+    a[i] = mk_c(neg_if(a[i].x, neg), neg_if(a[i].y, neg));
   }
 }
 
@@ -254,50 +272,50 @@ __device__ __forceinline__ constexpr bool take_pair(int i) {
 
 template <int R, int S, int PART, class P, class F>
 __device__ __forceinline__ double ip_x(P&& p, F&& f) {
-  double acc = 0.0;
+  real_t acc = 0;
 #pragma unroll
   for (int i = 0; i < (1 << R); ++i)
     if (!((i >> S) & 1) && take_pair<R, S, PART>(i)) {
       const int j = i | (1 << S);
-      const double2 f0 = f(i), f1 = f(j), p0 = p(i), p1 = p(j);
+      const cplx_t f0 = f(i), f1 = f(j), p0 = p(i), p1 = p(j);
       acc += f0.x * p1.y - f0.y * p1.x;
       acc += f1.x * p0.y - f1.y * p0.x;
     }
-  return acc;
+  return (double)acc;
 }
 template <int R, int S, int PART, class P, class F>
 __device__ __forceinline__ double ip_y(P&& p, F&& f) {
-  double acc = 0.0;
+  real_t acc = 0;
 #pragma unroll
   for (int i = 0; i < (1 << R); ++i)
     if (!((i >> S) & 1) && take_pair<R, S, PART>(i)) {
       const int j = i | (1 << S);
-      const double2 f0 = f(i), f1 = f(j), p0 = p(i), p1 = p(j);
+      const cplx_t f0 = f(i), f1 = f(j), p0 = p(i), p1 = p(j);
       acc -= f0.x * p1.x + f0.y * p1.y;
       acc += f1.x * p0.x + f1.y * p0.y;
     }
-  return acc;
+  return (double)acc;
 }
 // Z on a register slot (mask = 1 << slot) or a per-thread constant bit (mask 0)
 template <int R, int PART, class P, class F>
 __device__ __forceinline__ double ip_z(P&& p, F&& f, uint32_t slot_mask, bool cbit) {
-  double acc = 0.0;
+  real_t acc = 0;
 #pragma unroll
   for (int i = 0; i < (1 << R); ++i) {
     if (PART >= 0 && R >= 1 && (i & 1) != PART) continue;
     const bool one = slot_mask ? ((i & slot_mask) != 0) : cbit;
-    const double2 fi = f(i), pi = p(i);
-    const double v = fi.x * pi.y - fi.y * pi.x;
+    const cplx_t fi = f(i), pi = p(i);
+    const real_t v = fi.x * pi.y - fi.y * pi.x;
     acc += one ? -v : v;
   }
-  return acc;
+  return (double)acc;
 }
 // All three Pauli inner products of slot S in one sweep, as explicit FMA
 // chains (12 DFMA per pair) split over two accumulator sets (alternate pairs)
 // so the dependent chains are half as long.
 template <int R, int S, int PART, class P, class F>
 __device__ __forceinline__ void ip_xyz(P&& p, F&& f, double& ix, double& iy, double& iz) {
-  double ax[2] = {0.0, 0.0}, ay[2] = {0.0, 0.0}, az[2] = {0.0, 0.0};
+  real_t ax[2] = {0, 0}, ay[2] = {0, 0}, az[2] = {0, 0};
   int k = 0;
 #pragma unroll
   for (int i = 0; i < (1 << R); ++i)
@@ -305,7 +323,7 @@ __device__ __forceinline__ void ip_xyz(P&& p, F&& f, double& ix, double& iy, dou
       const int j = i | (1 << S);
       const int c = k & 1;
       ++k;
-      const double2 f0 = f(i), f1 = f(j), p0 = p(i), p1 = p(j);
+      const cplx_t f0 = f(i), f1 = f(j), p0 = p(i), p1 = p(j);
       ax[c] = fma(f0.x, p1.y, ax[c]);
       ax[c] = fma(-f0.y, p1.x, ax[c]);
       ax[c] = fma(f1.x, p0.y, ax[c]);
@@ -319,9 +337,9 @@ __device__ __forceinline__ void ip_xyz(P&& p, F&& f, double& ix, double& iy, dou
       az[c] = fma(-f1.x, p1.y, az[c]);
       az[c] = fma(f1.y, p1.x, az[c]);
     }
-  ix += ax[0] + ax[1];
-  iy += ay[0] + ay[1];
-  iz += az[0] + az[1];
+  ix += (double)(ax[0] + ax[1]);   // per-thread partials widen to float64
+  iy += (double)(ay[0] + ay[1]);
+  iz += (double)(az[0] + az[1]);
 }
 
 // ---------------------------------------------------------------------------
@@ -345,27 +363,27 @@ struct Group {
 
 // general 2x2 on slot S: a0' = u00 a0 + u01 a1 ; a1' = u10 a0 + u11 a1
 template <int R, int S>
-__device__ __forceinline__ void g_u2(double2 (&a)[1 << R], const double2 u00, const double2 u01,
-                                     const double2 u10, const double2 u11) {
+__device__ __forceinline__ void g_u2(cplx_t (&a)[1 << R], const cplx_t u00, const cplx_t u01,
+                                     const cplx_t u10, const cplx_t u11) {
 #pragma unroll
   for (int i = 0; i < (1 << R); ++i)
     if (!((i >> S) & 1)) {
       const int j = i | (1 << S);
-      const double2 x = a[i], y = a[j];
-      a[i] = make_double2(u00.x * x.x - u00.y * x.y + u01.x * y.x - u01.y * y.y,
+      const cplx_t x = a[i], y = a[j];
+      a[i] = mk_c(u00.x * x.x - u00.y * x.y + u01.x * y.x - u01.y * y.y,
                           u00.x * x.y + u00.y * x.x + u01.x * y.y + u01.y * y.x);
-      a[j] = make_double2(u10.x * x.x - u10.y * x.y + u11.x * y.x - u11.y * y.y,
+      a[j] = mk_c(u10.x * x.x - u10.y * x.y + u11.x * y.x - u11.y * y.y,
                           u10.x * x.y + u10.y * x.x + u11.x * y.y + u11.y * y.x);
     }
 }
 
 // fused CZ run (program.h DiagRun): per-register sign from a quadratic form
 template <int R>
-__device__ __forceinline__ void g_czrun(double2 (&a)[1 << R], uint32_t qreg, uint32_t m, uint32_t qc) {
+__device__ __forceinline__ void g_czrun(cplx_t (&a)[1 << R], uint32_t qreg, uint32_t m, uint32_t qc) {
 #pragma unroll
   for (int i = 0; i < (1 << R); ++i) {
     const bool neg = ((qc ^ (qreg >> i) ^ (uint32_t)__popc((uint32_t)i & m)) & 1u) != 0u;
-    a[i] = make_double2(neg_if(a[i].x, neg), neg_if(a[i].y, neg));
+    a[i] = mk_c(neg_if(a[i].x, neg), neg_if(a[i].y, neg));
   }
 }
 
@@ -414,8 +432,8 @@ struct SegCtx {
   uint32_t J0;
   uint32_t lp0;
   uint32_t lc[R];
-  double2* own;
-  const double2* partner;
+  cplx_t* own;
+  const cplx_t* partner;
   __device__ __forceinline__ uint32_t addr(int i) const {
     uint32_t ad = lp0;
 #pragma unroll
@@ -428,8 +446,8 @@ struct SegCtx {
 // Run one inner-product op: dual reads both register sets; split computes
 // half of the pairs from its own registers and the partner's shared copy.
 template <int R, int MODE, class K>
-__device__ __forceinline__ void ip_dispatch(const SegCtx<R>& C, const double2 (&a)[1 << R],
-                                            const double2 (&f)[1 << R], int role, K&& kernel) {
+__device__ __forceinline__ void ip_dispatch(const SegCtx<R>& C, const cplx_t (&a)[1 << R],
+                                            const cplx_t (&f)[1 << R], int role, K&& kernel) {
   auto ra = [&](int i) { return a[i]; };
   if constexpr (MODE == MODE_DUAL) {
     auto rf = [&](int i) { return f[i]; };
@@ -456,18 +474,18 @@ __device__ __forceinline__ void ip_dispatch(const SegCtx<R>& C, const double2 (&
 // these through with_slot; the per-plan JIT (jit.cpp) emits direct calls, so
 // both paths run the same arithmetic in the same order.
 template <int R>
-using Regs = double2[1 << R];
+using Regs = cplx_t[1 << R];
 
 template <int R, int MODE, int KIND, int S, bool ADJ>
 __device__ __forceinline__ void jop_rot(Regs<R>& a, Regs<R>& f, const SampleTables& T, int r) {
   const double2 cs = T.cs[r];
-  const double sn = ADJ ? -cs.y : cs.y;
+  const real_t c = (real_t)cs.x, sn = (real_t)(ADJ ? -cs.y : cs.y);
   if constexpr (KIND == G_RX) {
-    g_rx<R, S>(a, cs.x, sn);
-    if constexpr (MODE == MODE_DUAL) g_rx<R, S>(f, cs.x, sn);
+    g_rx<R, S>(a, c, sn);
+    if constexpr (MODE == MODE_DUAL) g_rx<R, S>(f, c, sn);
   } else {
-    g_ry<R, S>(a, cs.x, sn);
-    if constexpr (MODE == MODE_DUAL) g_ry<R, S>(f, cs.x, sn);
+    g_ry<R, S>(a, c, sn);
+    if constexpr (MODE == MODE_DUAL) g_ry<R, S>(f, c, sn);
   }
 }
 
@@ -475,22 +493,23 @@ __device__ __forceinline__ void jop_rot(Regs<R>& a, Regs<R>& f, const SampleTabl
 template <int R, int MODE, bool ADJ>
 __device__ __forceinline__ void jop_rz(Regs<R>& a, Regs<R>& f, const SampleTables& T, int r, uint32_t m, bool cb) {
   const double2 cs = T.cs[r];
-  const double sn = ADJ ? -cs.y : cs.y;
-  g_rz<R>(a, cs.x, sn, m, cb);
-  if constexpr (MODE == MODE_DUAL) g_rz<R>(f, cs.x, sn, m, cb);
+  const real_t c = (real_t)cs.x, sn = (real_t)(ADJ ? -cs.y : cs.y);
+  g_rz<R>(a, c, sn, m, cb);
+  if constexpr (MODE == MODE_DUAL) g_rz<R>(f, c, sn, m, cb);
 }
 
 // fused block (relative id blk) on slot S; ADJ applies U^dagger
 template <int R, int MODE, int S, bool ADJ>
 __device__ __forceinline__ void jop_u2(Regs<R>& a, Regs<R>& f, const SampleTables& T, int blk) {
   const double2* u = T.u + 4 * blk;
-  double2 u00 = u[0], u01 = u[1], u10 = u[2], u11 = u[3];
+  cplx_t u00 = mk_c((real_t)u[0].x, (real_t)u[0].y), u01 = mk_c((real_t)u[1].x, (real_t)u[1].y),
+         u10 = mk_c((real_t)u[2].x, (real_t)u[2].y), u11 = mk_c((real_t)u[3].x, (real_t)u[3].y);
   if constexpr (ADJ) {
-    const double2 t = u01;
+    const cplx_t t = u01;
     u00.y = -u00.y;
     u11.y = -u11.y;
-    u01 = make_double2(u10.x, -u10.y);
-    u10 = make_double2(t.x, -t.y);
+    u01 = mk_c(u10.x, -u10.y);
+    u10 = mk_c(t.x, -t.y);
   }
   g_u2<R, S>(a, u00, u01, u10, u11);
   if constexpr (MODE == MODE_DUAL) g_u2<R, S>(f, u00, u01, u10, u11);
@@ -759,8 +778,8 @@ __device__ __forceinline__ void exec_op(const DevProgram& D, const Op op, Regs<R
 struct SegEnv {
   const DevProgram& D;
   const RunArgs& A;
-  double2* s_psi;
-  double2* s_phi;
+  cplx_t* s_psi;
+  cplx_t* s_phi;
   const double* s_av_all;
   int av_stride, av_base;
   double* s_red;
@@ -770,17 +789,17 @@ struct SegEnv {
   uint32_t tile_base;
   int64_t bl0;
   int bra, tile, n_tiles;
-  double2* own;
-  const double2* partner;
+  cplx_t* own;
+  const cplx_t* partner;
 };
 
 template <int MODE>
-__device__ __forceinline__ SegEnv make_env(const DevProgram& D, const RunArgs& A, double2* s_psi, double2* s_phi,
+__device__ __forceinline__ SegEnv make_env(const DevProgram& D, const RunArgs& A, cplx_t* s_psi, cplx_t* s_phi,
                                            const double* s_av_all, int av_stride, int av_base, double* s_red,
                                            double* s_fin, const Group& grp, bool active, uint32_t tile_base,
                                            int64_t bl0, int bra, int tile, int n_tiles) {
-  double2* own = (MODE == MODE_SPLIT && grp.role) ? s_phi : s_psi;
-  const double2* partner = (MODE == MODE_SPLIT && grp.role) ? s_psi : s_phi;
+  cplx_t* own = (MODE == MODE_SPLIT && grp.role) ? s_phi : s_psi;
+  const cplx_t* partner = (MODE == MODE_SPLIT && grp.role) ? s_psi : s_phi;
   return SegEnv{D, A, s_psi, s_phi, s_av_all, av_stride, av_base, s_red, s_fin, grp, active, tile_base,
                 bl0, bra, tile, n_tiles, own, partner};
 }

@@ -51,6 +51,7 @@ struct HostProgram {
   int n_fwd_ops = 0, n_bwd_ops = 0;
   int absorbed = 0;  // trailing gates folded into the observables (absorb_trailing_gates)
   bool adj_dual = false;  // HBM adjoint passes: both states per thread (JIT only) instead of thread pairs
+  int precision = 0;      // 0 = complex128 states, 1 = complex64 (JIT kernels compiled with VQC_C64)
 };
 
 // Fold the circuit's trailing parameter-free gates that map Z strings to Z

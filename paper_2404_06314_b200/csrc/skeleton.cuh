@@ -36,8 +36,8 @@ __device__ __forceinline__ void stage_terms(const DevProgram& D, TermSm* s_terms
 // parity(hi[b] & s), so no per-element index arithmetic is needed.
 // E: elements per thread (compile time; equals the tile walk's count)
 template <bool DUAL, int E, class PM = RtPassMap>
-__device__ __forceinline__ void observe(const DevProgram& D, const RunArgs& A, const PassDesc* pd, double2* s_psi,
-                                        double2* s_phi, const double* s_u_row, const TermSm* s_terms,
+__device__ __forceinline__ void observe(const DevProgram& D, const RunArgs& A, const PassDesc* pd, cplx_t* s_psi,
+                                        cplx_t* s_phi, const double* s_u_row, const TermSm* s_terms,
                                         const Group& grp, double* s_red, double* s_fin, uint32_t tile_base, int k,
                                         int64_t bl0, bool do_expect, int seed_mode, int bra, int tile,
                                         int n_tiles) {
@@ -56,8 +56,9 @@ __device__ __forceinline__ void observe(const DevProgram& D, const RunArgs& A, c
     for (int i = 0; i < E; ++i) {
       p2[i] = 0.0;
       if (i < count) {
-        const double2 x = s_psi[swz((uint32_t)lane + (uint32_t)i * (uint32_t)grp.TT)];
-        p2[i] = x.x * x.x + x.y * x.y;
+        const cplx_t x = s_psi[swz((uint32_t)lane + (uint32_t)i * (uint32_t)grp.TT)];
+        const double xr = x.x, xi = x.y;   // |psi_j|^2 in float64 for either state type
+        p2[i] = xr * xr + xi * xi;
       }
     }
     for (int m = 0; m < D.M; ++m) s_red[m * (int)blockDim.x + threadIdx.x] = 0.0;
@@ -81,9 +82,10 @@ __device__ __forceinline__ void observe(const DevProgram& D, const RunArgs& A, c
         for (int i = 0; i < count; ++i) {
           const uint32_t l = (uint32_t)lane + (uint32_t)i * (uint32_t)grp.TT;
           const uint32_t kx = l ^ ts.xmask;
-          const double2 a = s_psi[swz(l)], bq = s_psi[swz(kx)];
+          const cplx_t ca = s_psi[swz(l)], cb = s_psi[swz(kx)];
+          const double ax = ca.x, ay = ca.y, bx = cb.x, by = cb.y;
           // conj(a) * bq
-          double re = a.x * bq.x + a.y * bq.y, im = a.x * bq.y - a.y * bq.x;
+          double re = ax * bx + ay * by, im = ax * by - ay * bx;
           const int ph = ts.phase & 3;  // multiply by i^ph, keep the real part
           double r = ph == 0 ? re : ph == 1 ? -im : ph == 2 ? -re : im;
           v += (__popc(kx & ts.mask) & 1) ? -r : r;
@@ -130,8 +132,8 @@ __device__ __forceinline__ void observe(const DevProgram& D, const RunArgs& A, c
         if (i >= count) break;
         const uint32_t l = (uint32_t)lane + (uint32_t)i * (uint32_t)grp.TT;
         const uint32_t p = swz(l);
-        const double2 x = s_psi[p];
-        double2 phi = make_double2(w[i] * x.x, w[i] * x.y);
+        const cplx_t x = s_psi[p];
+        double2 phi = make_double2(w[i] * (double)x.x, w[i] * (double)x.y);
         if (D.has_xy) {
           // pauli_sum_apply (_kernels.py:166-179) for the X/Y strings
           for (int t = 0; t < D.T; ++t) {
@@ -140,7 +142,7 @@ __device__ __forceinline__ void observe(const DevProgram& D, const RunArgs& A, c
             const double e = seed_mode == 1 ? s_u_row[ts.obs] * ts.coeff : (ts.obs == bra ? ts.coeff : 0.0);
             if (e == 0.0) continue;
             const uint32_t kx = l ^ ts.xmask;
-            const double2 bq = s_psi[swz(kx)];
+            const double2 bq = make_double2((double)s_psi[swz(kx)].x, (double)s_psi[swz(kx)].y);
             const int ph = ts.phase & 3;
             double2 v = ph == 0 ? bq : ph == 1 ? make_double2(-bq.y, bq.x)
                       : ph == 2 ? make_double2(-bq.x, -bq.y) : make_double2(bq.y, -bq.x);
@@ -149,7 +151,7 @@ __device__ __forceinline__ void observe(const DevProgram& D, const RunArgs& A, c
             phi.y += sg * v.y;
           }
         }
-        s_phi[p] = phi;
+        s_phi[p] = mk_c((real_t)phi.x, (real_t)phi.y);
       }
     }
   }
@@ -158,11 +160,12 @@ __device__ __forceinline__ void observe(const DevProgram& D, const RunArgs& A, c
 // Shared-memory carve-up (kernels and host sizing must agree).
 struct SmemLayout {
   size_t psi, phi, cs, u, av, red, fin, up, terms, total;  // byte offsets
+  // esz: bytes per state element (16 complex128, 8 complex64)
   __host__ __device__ SmemLayout(int S, int n_amp, bool dual, int nrot, int nblk, int nav, int red_slots,
-                                 int threads, int M, int n_terms) {
+                                 int threads, int M, int n_terms, int esz) {
     size_t o = 0;
-    psi = o; o += (size_t)S * n_amp * 16;
-    phi = o; o += dual ? (size_t)S * n_amp * 16 : 0;
+    psi = o; o += (size_t)S * n_amp * esz;
+    phi = o; o += dual ? (size_t)S * n_amp * esz : 0;
     cs = o; o += (size_t)S * nrot * 16;
     u = o; o += (size_t)S * nblk * 64;
     av = o; o += (size_t)S * nav * 32;
@@ -215,9 +218,9 @@ __device__ __forceinline__ void smem_body(const DevProgram& D, const RunArgs& A)
   const int64_t b = A.b0 + (valid ? bl : 0);
   const PassDesc* pd = D.passes;
   const int nrot = D.n_rot, nblk = D.n_blk, nav = D.n_av;
-  const SmemLayout L(A.S, N, ADJ, nrot, nblk, nav, A.red_slots, (int)blockDim.x, D.M, D.T);
-  double2* s_psi = reinterpret_cast<double2*>(smem_raw + L.psi) + (size_t)grp.sl * N;
-  double2* s_phi = reinterpret_cast<double2*>(smem_raw + L.phi) + (size_t)grp.sl * N;
+  const SmemLayout L(A.S, N, ADJ, nrot, nblk, nav, A.red_slots, (int)blockDim.x, D.M, D.T, (int)sizeof(cplx_t));
+  cplx_t* s_psi = reinterpret_cast<cplx_t*>(smem_raw + L.psi) + (size_t)grp.sl * N;
+  cplx_t* s_phi = reinterpret_cast<cplx_t*>(smem_raw + L.phi) + (size_t)grp.sl * N;
   double2* s_cs = reinterpret_cast<double2*>(smem_raw + L.cs) + (size_t)grp.sl * nrot;
   double2* s_u = reinterpret_cast<double2*>(smem_raw + L.u) + (size_t)grp.sl * nblk * 4;
   double* s_av_all = reinterpret_cast<double*>(smem_raw + L.av);
@@ -227,7 +230,7 @@ __device__ __forceinline__ void smem_body(const DevProgram& D, const RunArgs& A)
   TermSm* s_terms = reinterpret_cast<TermSm*>(smem_raw + L.terms);
   stage_terms(D, s_terms);
 
-  for (int l = lane; l < N; l += grp.TT) s_psi[swz((uint32_t)l)] = make_double2(l == 0 ? 1.0 : 0.0, 0.0);
+  for (int l = lane; l < N; l += grp.TT) s_psi[swz((uint32_t)l)] = mk_c(l == 0 ? 1 : 0, 0);
   if (ADJ && A.upstream != nullptr)
     for (int m = lane; m < D.M; m += grp.TT) s_up[grp.sl * D.M + m] = valid ? A.upstream[b * D.M + m] : 0.0;
   if (A.tables != nullptr) {
@@ -259,7 +262,7 @@ __device__ __forceinline__ void smem_body(const DevProgram& D, const RunArgs& A)
     } else {
       observe<true, OBS_E>(D, A, nullptr, s_psi, s_phi, nullptr, s_terms, grp, s_red, s_fin, 0u, n, bl0,
                     A.expect != nullptr, 0, 0, 0, 1);
-      double2* fin = A.psi_fin + (size_t)bl * N;
+      cplx_t* fin = A.psi_fin + (size_t)bl * N;
       if (D.M > 1 && valid)
         for (int l = lane; l < N; l += grp.TT) fin[l] = s_psi[swz((uint32_t)l)];
       for (int m = 0; m < D.M; ++m) {
@@ -283,6 +286,15 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src)
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+// one state element (16 B complex128 through L2 only; 8 B complex64)
+__device__ __forceinline__ void cp_async_elem(cplx_t* smem_dst, const cplx_t* gmem_src) {
+#ifdef VQC_C64
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gmem_src) : "memory");
+#else
+  cp_async16(smem_dst, gmem_src);
+#endif
+}
 
 // One pass over HBM-resident states: CTA (tile, row) stages 2^k amplitudes.
 template <int R, int KM, class SEGS>
@@ -304,9 +316,9 @@ __device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A)
   const size_t N = (size_t)1 << D.n;
   const uint32_t tile_base = PM::tile_dep(pd, D.n, (uint32_t)tile);
   const SmemLayout L(1, Nt, ADJ, D.max_rot_pass, D.max_blk_pass, D.max_av_pass, A.red_slots, (int)blockDim.x,
-                     D.M, D.T);
-  double2* s_psi = reinterpret_cast<double2*>(smem_raw + L.psi);
-  double2* s_phi = reinterpret_cast<double2*>(smem_raw + L.phi);
+                     D.M, D.T, (int)sizeof(cplx_t));
+  cplx_t* s_psi = reinterpret_cast<cplx_t*>(smem_raw + L.psi);
+  cplx_t* s_phi = reinterpret_cast<cplx_t*>(smem_raw + L.phi);
   double2* s_cs = reinterpret_cast<double2*>(smem_raw + L.cs);
   double2* s_u = reinterpret_cast<double2*>(smem_raw + L.u);
   double* s_av = reinterpret_cast<double*>(smem_raw + L.av);
@@ -322,17 +334,17 @@ __device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A)
     for (int m = threadIdx.x; m < D.M; m += blockDim.x) s_up[m] = A.upstream[b * D.M + m];
   if (flags & F_INIT) {
     for (int l = threadIdx.x; l < Nt; l += blockDim.x)
-      s_psi[swz((uint32_t)l)] = make_double2((tile_base == 0 && l == 0) ? 1.0 : 0.0, 0.0);
+      s_psi[swz((uint32_t)l)] = mk_c((tile_base == 0 && l == 0) ? 1 : 0, 0);
   } else {
     // asynchronous 16-byte copies straight into the swizzled tile; they land
     // while the per-sample tables are built
-    const double2* src = ((flags & F_LOAD_FIN) ? A.psi_fin : A.psi) + (size_t)bl * N;
-    const double2* srcf = A.phi + (size_t)bl * N;
+    const cplx_t* src = ((flags & F_LOAD_FIN) ? A.psi_fin : A.psi) + (size_t)bl * N;
+    const cplx_t* srcf = A.phi + (size_t)bl * N;
     const bool lphi = ADJ && (flags & F_LOAD_PHI);
     const TileWalk tw = tile_walk<PM>(pd, tile_base, k, threadIdx.x, wstride);
     for_tile<OBS_E>(tw, [&](uint32_t sw, uint32_t j) {
-      cp_async16(s_psi + sw, src + j);
-      if (lphi) cp_async16(s_phi + sw, srcf + j);
+      cp_async_elem(s_psi + sw, src + j);
+      if (lphi) cp_async_elem(s_phi + sw, srcf + j);
     });
   }
   if (A.tables != nullptr) {
@@ -361,7 +373,7 @@ __device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A)
     uint32_t tb = tile_base;
     asm volatile("" : "+r"(tb));
     const TileWalk tw = tile_walk<PM>(pd, tb, k, threadIdx.x, wstride);
-    double2* dst = A.psi_fin + (size_t)bl * N;
+    cplx_t* dst = A.psi_fin + (size_t)bl * N;
     for_tile<OBS_E>(tw, [&](uint32_t sw, uint32_t j) { dst[j] = s_psi[sw]; });
   }
   if (flags & (F_OBSERVE | F_SEED)) {
@@ -383,8 +395,8 @@ __device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A)
     asm volatile("" : "+r"(tb));  // rebuild the tile walk here rather than keep it live
     const TileWalk tw = tile_walk<PM>(pd, tb, k, threadIdx.x, wstride);
     const bool spsi = (flags & F_STORE_PSI) != 0;
-    double2* dst = A.psi + (size_t)bl * N;
-    double2* dstf = A.phi + (size_t)bl * N;
+    cplx_t* dst = A.psi + (size_t)bl * N;
+    cplx_t* dstf = A.phi + (size_t)bl * N;
     for_tile<OBS_E>(tw, [&](uint32_t sw, uint32_t j) {
       if (spsi) dst[j] = s_psi[sw];
       if (sphi) dstf[j] = s_phi[sw];

@@ -216,14 +216,17 @@ def _device(device):
 
 
 class PlanCache:
-    """(circuit, observables, wrt, device) -> native.Plan."""
+    """(circuit, observables, wrt, device, precision) -> native.Plan."""
 
-    def __init__(self):
+    def __init__(self, precision: str = "complex128"):
+        if precision not in native.PRECISIONS:
+            raise ValueError(f"precision must be one of {tuple(native.PRECISIONS)}, got {precision!r}")
+        self.precision = precision
         self._plans: dict = {}
         self._lock = threading.Lock()
 
     def get(self, circuit: Circuit, observables, wrt: tuple, device):
-        key = (circuit, tuple(observables), tuple(wrt), str(device))
+        key = (circuit, tuple(observables), tuple(wrt), str(device), self.precision)
         with self._lock:
             plan = self._plans.get(key)
             if plan is None:
@@ -232,7 +235,8 @@ class PlanCache:
                 layout = WrtLayout.build(compiled, wrt)
                 enc = encoding_set(circuit)
                 off, size = compiled.offsets[enc.name]
-                plan = (native.Plan(compiled, pack, layout.wrt_col, off, size, device), layout)
+                plan = (native.Plan(compiled, pack, layout.wrt_col, off, size, device,
+                                    self.precision), layout)
                 self._plans[key] = plan
             return plan
 
@@ -253,14 +257,19 @@ class Workspace:
 
 
 class BatchEngine:
-    """GPU replacement for vqckit's BatchEngine (batch.py:120-217)."""
+    """GPU replacement for vqckit's BatchEngine (batch.py:120-217).
 
-    def __init__(self, threads: int | None = None, device=None):
+    ``precision``: "complex128" (the reference's state type, default) or
+    "complex64" (single-precision states, float64 angles, reductions and
+    outputs; matches the reference to 1e-5)."""
+
+    def __init__(self, threads: int | None = None, device=None, precision: str = "complex128"):
         if threads is not None and threads < 1:
             raise ValueError(f"threads must be >= 1, got {threads}")
         self.threads = threads
         self._device_arg = device
-        self.plans = PlanCache()
+        self.precision = precision
+        self.plans = PlanCache(precision)
         self.workspace = Workspace()
 
     @property

@@ -102,12 +102,14 @@ class QuantumModule(torch.nn.Module):
     Construction mirrors model.py:60-97: ``trainable`` is an ordered sequence
     of set names or (name, initializer) pairs; unlisted initializers default
     to Uniform[0, 2pi); values are drawn in that order from one
-    ``np.random.default_rng(seed)``.
+    ``np.random.default_rng(seed)``. ``precision="complex64"`` evolves
+    single-precision states (float64 angles, reductions and outputs; within
+    1e-5 of the complex128 reference).
     """
 
     def __init__(self, circuit, observables, encoding_set: str, trainable,
                  seed: int | None = None, threads: int | None = None,
-                 method: str = "adjoint", device=None):
+                 method: str = "adjoint", device=None, precision: str = "complex128"):
         super().__init__()
         self.circuit = circuit
         self.observables = list(observables)
@@ -135,7 +137,7 @@ class QuantumModule(torch.nn.Module):
                 raise ValueError(f"set {n!r} is not trainable")
         self.trainable_specs = tuple(specs)
         rng = np.random.default_rng(seed)
-        self._engine = BatchEngine(threads, device=device)
+        self._engine = BatchEngine(threads, device=device, precision=precision)
         dev = self._engine.device
         self._params = torch.nn.ParameterList()
         for n, init in specs:

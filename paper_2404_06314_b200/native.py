@@ -22,6 +22,8 @@ _F64P = ctypes.POINTER(ctypes.c_double)
 _VP = ctypes.c_void_p
 
 VQC_MODE_FORWARD, VQC_MODE_VJP, VQC_MODE_JACOBIAN = 0, 1, 2
+# state precision of a plan (vqc_plan_create's precision argument)
+PRECISIONS = {"complex128": 0, "complex64": 1}
 _ERRORS = {-1: ValueError, -2: NotImplementedError, -3: RuntimeError, -4: RuntimeError,
            -5: MemoryError}
 
@@ -120,8 +122,13 @@ def _f64(a):
 class Plan:
     """Owns one VqcPlan* (device tables for one circuit/observables/wrt)."""
 
-    def __init__(self, compiled, pack, wrt_col, enc_offset: int, enc_size: int, device=None):
+    def __init__(self, compiled, pack, wrt_col, enc_offset: int, enc_size: int, device=None,
+                 precision: str = "complex128"):
         import torch  # noqa: F401  (CUDA context on the right device)
+
+        if precision not in PRECISIONS:
+            raise ValueError(f"precision must be one of {tuple(PRECISIONS)}, got {precision!r}")
+        self.precision = precision
 
         lib = load_library()
         self._keep = [_i64(compiled.kinds), _i64(compiled.q0), _i64(compiled.q1),
@@ -148,10 +155,12 @@ class Plan:
             import torch
             with torch.cuda.device(device):
                 rc = lib.vqc_plan_create(ctypes.byref(circ), ctypes.byref(obs),
-                                         k[11].ctypes.data_as(_I64P), 0, ctypes.byref(handle))
+                                         k[11].ctypes.data_as(_I64P), PRECISIONS[precision],
+                                         ctypes.byref(handle))
         else:
             rc = lib.vqc_plan_create(ctypes.byref(circ), ctypes.byref(obs),
-                                     k[11].ctypes.data_as(_I64P), 0, ctypes.byref(handle))
+                                     k[11].ctypes.data_as(_I64P), PRECISIONS[precision],
+                                     ctypes.byref(handle))
         _check(rc, "vqc_plan_create")
         self._h = handle
         self._lib = lib

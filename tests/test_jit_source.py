@@ -76,3 +76,15 @@ def test_unusable_cache_dir_still_compiles(tmp_path, monkeypatch):
     circ, _, _ = _random(np.random.default_rng(5), 13, 20)
     src, secs = _src(circ, ("a", "b", "s"), compile=True)
     assert secs is not None and "vqc_jit_pa0" in src
+
+
+@pytest.mark.parametrize("cfg_id", [2, 4])
+def test_complex64_units_compile_for_sm100a(monkeypatch, cfg_id):
+    """complex64 plans (precision 1) compile their JIT units with VQC_C64:
+    on-chip (cfg2) and HBM passes (cfg4), 8-byte state elements."""
+    monkeypatch.setenv("VQC_JIT_CACHE", "0")
+    monkeypatch.setenv("VQC_JIT_SOURCE_PRECISION", "1")
+    spec = configs.CONFIGS[cfg_id]
+    circ, obs, wrt = configs.build(spec, configs.native_api())
+    src, secs = _src(circ, wrt, compile=True)
+    assert src.count("#define VQC_C64 1") >= 1 and secs is not None

@@ -18,6 +18,24 @@ __global__ void dfma_loop(double* out, int iters) {
   if (a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7 == 12345.0) out[0] = a0;
 }
 
+__global__ void ffma_loop(float* out, int iters) {
+  float a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = threadIdx.x * 1e-6f + k;
+  const float m = 0.9999f, c = 1e-5f;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a[j] = fmaf(a[j], m, c);
+    }
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == 12345.0f) out[0] = s;
+}
+
 __global__ void smem_loop(double* out, int iters) {
   extern __shared__ double2 sm[];
   const int n = 4096;
@@ -69,6 +87,20 @@ int main() {
     }
     double flops = 2.0 * 8 * 16 * (double)iters * threads * blocks;
     printf(", \"fp64_fma_tflops\": %.3f", flops / (best * 1e-3) / 1e12);
+  }
+  // FFMA (complex64 mode's pipe)
+  {
+    int iters = 20000, threads = 512, blocks = sms * 4;
+    float* df = reinterpret_cast<float*>(d);
+    ffma_loop<<<blocks, threads>>>(df, 100);
+    cudaDeviceSynchronize();
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+      cudaEventRecord(e0); ffma_loop<<<blocks, threads>>>(df, iters); cudaEventRecord(e1);
+      cudaEventSynchronize(e1); float ms; cudaEventElapsedTime(&ms, e0, e1); if (ms < best) best = ms;
+    }
+    double flops = 2.0 * 8 * 16 * (double)iters * threads * blocks;
+    printf(", \"fp32_fma_tflops\": %.3f", flops / (best * 1e-3) / 1e12);
   }
   // smem 16B ld+st
   {

@@ -23,7 +23,7 @@ spec = configs.CONFIGS[a.config]
 rows = a.rows or spec.batch
 circ, obs, wrt = configs.build(spec, configs.native_api())
 x, w = configs.inputs_and_weights(spec, batch=rows)
-eng = BatchEngine(device="cuda:0")
+eng = BatchEngine(device="cuda:0", precision=os.environ.get("VQC_PRECISION", "complex128"))
 dev = torch.device("cuda:0")
 plan, layout = eng.plans.get(circ, obs, wrt, dev)
 flat = eng.base_flat(circ, {"w": w})
@@ -47,7 +47,7 @@ prof = native.profile_report()
 ms = t0.elapsed_time(t1) / a.reps
 F = configs.flops_per_sample(spec) * B
 print(json.dumps({"config": a.config, "rows": B, "ms": round(ms, 3), "samples_per_s": round(B / ms * 1e3, 1),
-                  "frac_fp64": round(F / (ms * 1e-3) / 37.1e12, 4),
+                  "frac_fp64": round(F / (ms * 1e-3) / 37.1e12, 4), "precision": eng.precision,
                   "env": {k: os.environ.get(k) for k in ("VQC_REG_SLOTS", "VQC_TILE_QUBITS", "VQC_STATE_BUDGET_MB")},
                   "kernels": {k: [round(v[0] / a.reps, 3), v[1] // a.reps] for k, v in prof.items()},
                   "plan": json.loads(plan.describe())}))
