@@ -115,6 +115,20 @@ constexpr int kHbmAdjointRegs = 3;
 // (few threads per sample would build them through serial global loads)
 constexpr int kSmemTablesMaxN = 10;
 constexpr int kHbmForwardRegs = 4;
+// on-chip JIT plans this small run 3 register slots with both states per
+// thread (measured: cfg2 158 -> 98 us, cfg1 52 -> 31 us per call); n = 11, 12
+// keep 4 slots on thread pairs (cfg3: 5.95 vs 6.40 ms). VQC_SMEM_DUAL=1 / 0
+// forces it on / off for 4 <= n <= 12.
+constexpr int kSmemDualMaxN = 10;
+bool smem_dual(int n) {
+  auto env = [](const char* name) {
+    const char* v = std::getenv(name);
+    return (v && *v) ? std::atoi(v) : -1;
+  };
+  if (n < 4 || n > kSmemMaxQubits || env("VQC_JIT") == 0) return false;
+  const int e = env("VQC_SMEM_DUAL");
+  return e < 0 ? n <= kSmemDualMaxN : e != 0;
+}
 
 // Plans use R = min(4, n) register slots (schedule_circuit), so only these
 // interpreter instantiations exist (each is a large unrolled kernel).
@@ -421,7 +435,9 @@ int smem_samples(const VqcPlan* p, int64_t B, bool dual, size_t* smem_bytes, int
   };
   const int max_threads = P.R >= 5 ? 256 : (split ? 512 : (P.R >= 4 ? 256 : 512));
   int smax = std::max(1, max_threads / TT);
-  const int64_t want = std::max<int64_t>(1, (B + 2 * p->sms - 1) / (2 * p->sms));
+  // samples per CTA: enough CTAs for VQC_SMEM_CTAS_PER_SM (default 2) per SM
+  const int64_t cps = std::max(1, env_int("VQC_SMEM_CTAS_PER_SM", 2)) * (int64_t)p->sms;
+  const int64_t want = std::max<int64_t>(1, (B + cps - 1) / cps);
   int S = 1;
   // JIT kernels of n >= 12 lag their reductions, which assumes one sample per CTA
   if (p->use_jit && P.n >= 12) smax = 1;
@@ -604,8 +620,11 @@ int run_core(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, const
                        (size_t)L.ftable_stride * 8, st, DF, AF)))
         return rc;
     }
-    const dim3 grid((unsigned)L.n_tiles, (unsigned)nb), grid_f((unsigned)tiles_f, (unsigned)nb);
-    const dim3 block_f((unsigned)TPSF), block2((unsigned)(P.adj_dual ? TPS : 2 * TPS));
+    // ping-pong JIT kernels: two tile groups per CTA (half the grid, twice
+    // the block and its shared memory)
+    const int Gb = P.pingpong ? 2 : 1, Gf = PF.pingpong ? 2 : 1;
+    const dim3 grid((unsigned)(L.n_tiles / Gb), (unsigned)nb), grid_f((unsigned)(tiles_f / Gf), (unsigned)nb);
+    const dim3 block_f((unsigned)(Gf * TPSF)), block2((unsigned)(Gb * (P.adj_dual ? TPS : 2 * TPS)));
     auto fwd_pass = [&](int pi, uint32_t flags) {
       AF.pass = pi;
       AF.flags = flags;
@@ -614,12 +633,12 @@ int run_core(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, const
       Kern k;
       if (sep) k.cu = p->fwd->jit.pass_fwd[pi];
       else k = pass_k(p, false, pi);
-      return launch("pass_forward", k, grid_f, block_f, obs ? smF : smF0, st, DF, AF);
+      return launch("pass_forward", k, grid_f, block_f, Gf * (obs ? smF : smF0), st, DF, AF);
     };
     auto adj_pass = [&](int pi, uint32_t flags) {
       A.pass = pi;
       A.flags = flags;
-      return launch("pass_adjoint", pass_k(p, true, pi), grid, block2, smB, st, D, A);
+      return launch("pass_adjoint", pass_k(p, true, pi), grid, block2, Gb * smB, st, D, A);
     };
     const uint32_t stores = F_STORE_PSI | F_STORE_PHI;
     // forward sweep: all but the last forward pass
@@ -718,11 +737,8 @@ int schedule_circuit(const VqcCircuit* c, const int64_t* wrt_col, HostProgram* p
   opt.reg_slots = 4;
   if (c->n_qubits > opt.smem_max_qubits && env_int("VQC_JIT", -1) != 0)
     opt.reg_slots = std::max(3, std::min(4, env_int("VQC_REG_SLOTS", kHbmAdjointRegs)));
-  // on-chip JIT plans large enough for thread pairs: 3 slots, both states
-  // per thread (VQC_SMEM_DUAL)
-  if (c->n_qubits <= opt.smem_max_qubits && c->n_qubits >= 9 && env_int("VQC_JIT", -1) != 0 &&
-      env_int("VQC_SMEM_DUAL", 0) != 0)
-    opt.reg_slots = 3;
+  // small on-chip JIT plans: 3 slots, both states per thread (smem_dual)
+  if (c->n_qubits <= opt.smem_max_qubits && smem_dual(c->n_qubits)) opt.reg_slots = 3;
   if (tile_override > 0) opt.tile_qubits = tile_override;
   if (regs_override > 0) opt.reg_slots = regs_override;
   const int absorbed = prog->absorbed;
@@ -789,9 +805,10 @@ int64_t vqc_jit_source(const VqcCircuit* c, const int64_t* wrt_col, int compile,
   std::vector<uint32_t> zm;  // as for Z-string observables (trailing gates absorbed)
   std::vector<double> zc;
   if (int rc = schedule_circuit(c, wrt_col, &prog, &zm, &zc)) return rc;
-  if ((prog.hbm || env_int("VQC_SMEM_DUAL", 0) != 0) && env_int("VQC_ADJ_DUAL", prog.R <= 3 ? 1 : 0) != 0)
+  if ((prog.hbm || (prog.R <= 3 && smem_dual(prog.n))) && env_int("VQC_ADJ_DUAL", prog.R <= 3 ? 1 : 0) != 0)
     prog.adj_dual = true;
   prog.precision = env_int("VQC_JIT_SOURCE_PRECISION", 0) == 1 ? 1 : 0;  // dump / compile a complex64 plan
+  prog.pingpong = prog.hbm ? std::max(0, std::min(2, env_int("VQC_PINGPONG", 0))) : 0;
   build_thr_table(prog.segs);  // per-segment thread-table offsets, as at plan creation
   const bool split = use_split(prog.n, prog.R) && !prog.adj_dual;
   const std::string src = jit_source(prog, split);
@@ -939,12 +956,19 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
   // circuits are launch-bound and stay on the prebuilt interpreter.
   const int jit_mode = env_int("VQC_JIT", -1);
   // complex64 plans always specialise (the interpreter kernels are complex128)
-  const bool want_jit = precision == 1 || jit_mode > 0 || (jit_mode < 0 && (P.hbm || P.n >= 8));
+  const bool want_jit = precision == 1 || jit_mode > 0 || (jit_mode < 0 && (P.hbm || P.n >= 4));
   if (want_jit && (P.n_fwd_ops + P.n_bwd_ops > 0 || precision == 1)) {
     // HBM adjoint with both states per thread when its register slots allow
     // (VQC_ADJ_DUAL overrides: 0 = thread pairs)
-    if ((P.hbm || (P.R <= 3 && env_int("VQC_SMEM_DUAL", 0) != 0)) && env_int("VQC_ADJ_DUAL", P.R <= 3 ? 1 : 0) != 0)
+    if ((P.hbm || (P.R <= 3 && smem_dual(P.n))) && env_int("VQC_ADJ_DUAL", P.R <= 3 ? 1 : 0) != 0)
       p->prog.adj_dual = true;
+    // HBM passes: ping-pong tile groups (VQC_PINGPONG=0 turns them off)
+    // off by default: both modes measured slower than two free-running CTAs
+    // per SM on cfg4 / cfg5
+    const int pp_mode = std::max(0, std::min(2, env_int("VQC_PINGPONG", 0)));
+    const int pingpong = (P.hbm && P.n - P.k >= 1 && 2 * pass_smem(p, P, true) <= (size_t)kMaxSmemBytes)
+                             ? pp_mode : 0;
+    p->prog.pingpong = pingpong;
     err = jit_build(P, use_split(P.n, P.R) && !P.adj_dual, &p->jit);
     if (!err.empty()) {
       vqc_plan_destroy(p);
@@ -964,6 +988,8 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
         return rc;
       }
       f->prog.precision = precision;
+      f->prog.pingpong = (f->prog.n - f->prog.k >= 1 && 2 * pass_smem(p, f->prog, false) <= (size_t)kMaxSmemBytes)
+                             ? pingpong : 0;
       if (!f->prog.hbm || f->prog.NG != P.NG) {
         vqc_plan_destroy(p);
         return fail(VQC_E_UNSUPPORTED, "forward schedule disagrees with the adjoint schedule");
@@ -1019,14 +1045,14 @@ int64_t vqc_plan_describe(const VqcPlan* p, char* buf, int64_t cap) {
                            "\"passes\": %d, \"segments\": %d, \"rotations\": %d, \"grad_slots\": %d, "
                            "\"fwd_ops\": %d, \"bwd_ops\": %d, \"cols\": %d, \"obs\": %d, \"jit\": %s, "
                            "\"jit_compile_s\": %.3f, \"jit_cubin_bytes\": %zu, \"absorbed_gates\": %d, \"adjoint_dual\": %s, "
-                           "\"fwd_tile_qubits\": %d, \"fwd_reg_slots\": %d, \"fwd_passes\": %d, \"precision\": \"%s\"}",
+                           "\"fwd_tile_qubits\": %d, \"fwd_reg_slots\": %d, \"fwd_passes\": %d, \"precision\": \"%s\", \"pingpong\": %d}",
                            P.n, P.hbm ? "hbm" : "smem", P.k, P.R, (int)P.passes.size(), nseg, P.n_rot,
                            P.NG, P.n_fwd_ops, P.n_bwd_ops, P.n_cols, p->M, p->use_jit ? "true" : "false",
                            p->jit.compile_s + (p->fwd ? p->fwd->jit.compile_s : 0.0),
                            p->jit.cubin_bytes + (p->fwd ? p->fwd->jit.cubin_bytes : 0), P.absorbed,
                            P.adj_dual ? "true" : "false", p->fwd ? p->fwd->prog.k : P.k,
                            p->fwd ? p->fwd->prog.R : P.R, (int)(p->fwd ? p->fwd->prog.passes.size() : P.passes.size()),
-                           P.precision == 1 ? "complex64" : "complex128");
+                           P.precision == 1 ? "complex64" : "complex128", P.pingpong);
   if (buf && cap > 0) {
     const int64_t c = std::min<int64_t>(cap - 1, len);
     memcpy(buf, tmp, (size_t)c);

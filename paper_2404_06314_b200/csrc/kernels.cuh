@@ -41,6 +41,64 @@ typedef double2 cplx_t;
 __device__ __forceinline__ cplx_t mk_c(real_t a, real_t b) { return make_double2(a, b); }
 #endif
 
+// CTA view. Plain kernels treat the CTA as one thread group. HBM pass
+// kernels built with VQC_PINGPONG run two half-CTA groups on two tiles and
+// order their segment phases with named barriers (seg_begin ends in
+// phase_a(), seg_end starts with phase_b()):
+//   VQC_PINGPONG == 1: the register phases (gate arithmetic) alternate
+//     between the groups;
+//   VQC_PINGPONG == 2: the shared-memory phases (register store, reduction,
+//     next register load) alternate, arithmetic may overlap.
+// vtid / vdim / vsync are the group's thread index, size and barrier.
+#ifdef VQC_PINGPONG
+__device__ __forceinline__ unsigned cta_group() { return threadIdx.x >= (blockDim.x >> 1) ? 1u : 0u; }
+__device__ __forceinline__ unsigned vdim() { return blockDim.x >> 1; }
+__device__ __forceinline__ unsigned vtid() { return threadIdx.x - cta_group() * (blockDim.x >> 1); }
+__device__ __forceinline__ void vsync() {
+  asm volatile("bar.sync %0, %1;" ::"r"(1u + cta_group()), "r"(blockDim.x >> 1) : "memory");
+}
+// barrier 3 + g: group g waits there for the other group's hand-over
+__device__ __forceinline__ void turn_wait() {
+  asm volatile("bar.sync %0, %1;" ::"r"(3u + cta_group()), "r"(blockDim.x) : "memory");
+}
+__device__ __forceinline__ void turn_pass() {
+  asm volatile("bar.arrive %0, %1;" ::"r"(4u - cta_group()), "r"(blockDim.x) : "memory");
+}
+#if VQC_PINGPONG == 1
+__device__ __forceinline__ void phase_a() { turn_wait(); }
+__device__ __forceinline__ void phase_b() { turn_pass(); }
+// group 0 takes the first turn; it also consumes group 1's last hand-over
+__device__ __forceinline__ void turn_init() {
+  if (cta_group() == 1u) turn_pass();
+}
+__device__ __forceinline__ void turn_fini() {
+  if (cta_group() == 0u) turn_wait();
+}
+#else
+__device__ __forceinline__ void phase_a() { turn_pass(); }
+__device__ __forceinline__ void phase_b() { turn_wait(); }
+// group 1 starts after group 0's first register load; group 0 hands over
+// once more at the end for group 1's last shared-memory phase
+__device__ __forceinline__ void turn_init() {
+  if (cta_group() == 1u) turn_wait();
+}
+__device__ __forceinline__ void turn_fini() {
+  if (cta_group() == 0u) turn_pass();
+}
+#endif
+constexpr int kCtaGroups = 2;
+#else
+__device__ __forceinline__ unsigned cta_group() { return 0u; }
+__device__ __forceinline__ unsigned vdim() { return blockDim.x; }
+__device__ __forceinline__ unsigned vtid() { return threadIdx.x; }
+__device__ __forceinline__ void vsync() { __syncthreads(); }
+__device__ __forceinline__ void phase_a() {}
+__device__ __forceinline__ void phase_b() {}
+__device__ __forceinline__ void turn_init() {}
+__device__ __forceinline__ void turn_fini() {}
+constexpr int kCtaGroups = 1;
+#endif
+
 struct DevProgram {
   const Op* ops;
   const SegDesc* segs;
@@ -98,7 +156,7 @@ struct RunArgs {
 enum { DBG_PROLOGUE = 0, DBG_FWD = 1, DBG_OBSERVE = 2, DBG_BWD = 3, DBG_STORE = 4, DBG_SEG_LOAD = 5,
        DBG_SEG_OPS = 6, DBG_SEG_STORE = 7, DBG_SEG_FINAL = 8, DBG_CTAS = 9, DBG_N = 10 };
 __device__ __forceinline__ void dbg_add(const RunArgs& A, int slot, long long& t) {
-  if (A.dbg != nullptr && threadIdx.x == 0) {
+  if (A.dbg != nullptr && vtid() == 0) {
     const long long now = clock64();
     atomicAdd(A.dbg + slot, (unsigned long long)(now - t));
     t = now;
@@ -350,7 +408,7 @@ struct Group {
   int role = 0, TT = 0;        // TT = threads per sample
   __device__ __forceinline__ double reduce(double v) const {
     const int width = TT < 32 ? TT : 32;
-    const unsigned mask = blockDim.x >= 32 ? 0xffffffffu : ((1u << blockDim.x) - 1u);
+    const unsigned mask = vdim() >= 32 ? 0xffffffffu : ((1u << vdim()) - 1u);
     for (int off = width >> 1; off > 0; off >>= 1) v += __shfl_xor_sync(mask, v, off);
     return v;
   }
@@ -390,7 +448,7 @@ __device__ __forceinline__ void g_czrun(cplx_t (&a)[1 << R], uint32_t qreg, uint
 // this thread's partial inner product for reduction slot `slot` (reduced over
 // the sample's threads at the end of the segment, in a fixed order)
 __device__ __forceinline__ void put_partial(double* redbuf, int slot, double v) {
-  redbuf[slot * blockDim.x + threadIdx.x] = v;
+  redbuf[slot * vdim() + vtid()] = v;
 }
 // lagged JIT reductions: lanes 2i, 2i+1 add their partials first and one half
 // row (blockDim/2 entries) per slot is written, so two segments' partial
@@ -399,7 +457,7 @@ template <bool PAIR>
 __device__ __forceinline__ void put_part(double* redbuf, int slot, double v) {
   if constexpr (PAIR) {
     v += __shfl_xor_sync(0xffffffffu, v, 1);
-    if (!(threadIdx.x & 1u)) redbuf[slot * (blockDim.x >> 1) + (threadIdx.x >> 1)] = v;
+    if (!(vtid() & 1u)) redbuf[slot * (vdim() >> 1) + (vtid() >> 1)] = v;
   } else {
     put_partial(redbuf, slot, v);
   }
@@ -859,13 +917,14 @@ __device__ __forceinline__ void seg_begin(const SegEnv& E, const SD& sd, SegCtx<
       if constexpr (MODE == MODE_DUAL) f[i] = E.s_phi[ad];
     }
   }
+  phase_a();  // ping-pong hand-over point (see cta_group)
 }
 
 // split adjoint: write this thread's registers back for the partner's inner products
 template <int R, int MODE>
 __device__ __forceinline__ void seg_publish(const SegEnv& E, const SegCtx<R>& C, const Regs<R>& a) {
   if constexpr (MODE == MODE_SPLIT) {
-    __syncthreads();
+    vsync();
     if (E.active) {
       uint32_t base = C.lp0;
       asm volatile("" : "+r"(base));
@@ -878,7 +937,7 @@ __device__ __forceinline__ void seg_publish(const SegEnv& E, const SegCtx<R>& C,
         E.own[ad] = a[i];
       }
     }
-    __syncthreads();
+    vsync();
   }
 }
 
@@ -889,7 +948,8 @@ __device__ __forceinline__ void seg_end(const SegEnv& E, const SD& sd, const Reg
   constexpr int N = 1 << R;
   const Group& grp = E.grp;
   const RunArgs& A = E.A;
-  if (MODE == MODE_SPLIT && sd.ip_count() > 0) __syncthreads();  // partners done reading
+  phase_b();  // ping-pong hand-over point
+  if (MODE == MODE_SPLIT && sd.ip_count() > 0) vsync();  // partners done reading
   asm volatile("" ::: "memory");  // keep the store map's loads and math after the op loop
   if (E.active) {
     uint32_t sp0, sc[R];
@@ -917,7 +977,7 @@ __device__ __forceinline__ void seg_end(const SegEnv& E, const SD& sd, const Reg
       if constexpr (MODE == MODE_DUAL) E.s_phi[ad] = f[i];
     }
   }
-  __syncthreads();
+  vsync();
   if constexpr (MODE != MODE_FWD && REDUCE) {
     const int nout = sd.ip_count();
     if (nout > 0) {
@@ -926,13 +986,13 @@ __device__ __forceinline__ void seg_end(const SegEnv& E, const SD& sd, const Reg
       // (output, sample) applies the block gradient vector. Blocks narrower
       // than a warp (tiny n) reduce serially on thread 0.
       const int nred = sd.red_count();
-      const bool narrow = blockDim.x < 32;
-      const int lane = narrow ? 0 : (threadIdx.x & 31);
-      const int warp = narrow ? (threadIdx.x == 0 ? 0 : 1 << 30) : (threadIdx.x >> 5);
-      const int nwarp = narrow ? 1 : (blockDim.x >> 5);
+      const bool narrow = vdim() < 32;
+      const int lane = narrow ? 0 : (vtid() & 31);
+      const int warp = narrow ? (vtid() == 0 ? 0 : 1 << 30) : (vtid() >> 5);
+      const int nwarp = narrow ? 1 : (vdim() >> 5);
       for (int task = warp; task < nred * grp.S; task += nwarp) {
         const int slot = task / grp.S, s_ = task - slot * grp.S;
-        const double* base = E.s_red + slot * (int)blockDim.x + s_ * grp.TT;
+        const double* base = E.s_red + slot * (int)vdim() + s_ * grp.TT;
         double v = 0.0;
         if (narrow) {
           for (int t = 0; t < grp.TT; ++t) v += base[t];
@@ -942,8 +1002,8 @@ __device__ __forceinline__ void seg_end(const SegEnv& E, const SD& sd, const Reg
         }
         if (lane == 0) E.s_fin[slot * grp.S + s_] = v;
       }
-      __syncthreads();
-      for (int task = threadIdx.x; task < nout * grp.S; task += blockDim.x) {
+      vsync();
+      for (int task = vtid(); task < nout * grp.S; task += vdim()) {
         const int oi = task / grp.S, s_ = task - oi * grp.S;
         const IpOut io = E.D.ipouts[sd.ip_begin() + oi];
         const double* r = E.s_fin + s_;
@@ -968,8 +1028,8 @@ __device__ __forceinline__ void seg_end(const SegEnv& E, const SD& sd, const Reg
 // s_fin alternate between segments and the next post-store barrier orders
 // every reuse, so the reduction needs no barrier of its own.
 __device__ __forceinline__ void jred_phase1(const SegEnv& E, int slot0, int nred, int fin0) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-  const int W = (int)(blockDim.x >> 1);
+  const int lane = vtid() & 31, warp = vtid() >> 5, nwarp = vdim() >> 5;
+  const int W = (int)(vdim() >> 1);
   for (int s = warp; s < nred; s += nwarp) {
     const double* base = E.s_red + (slot0 + s) * W;
     double v = 0.0;
@@ -982,7 +1042,7 @@ __device__ __forceinline__ void jred_phase1(const SegEnv& E, int slot0, int nred
 template <class SD>
 __device__ __forceinline__ void jred_phase2(const SegEnv& E, const SD& sd, int fin0) {
   const RunArgs& A = E.A;
-  for (int oi = threadIdx.x; oi < sd.ip_count(); oi += blockDim.x) {
+  for (int oi = vtid(); oi < sd.ip_count(); oi += vdim()) {
     const IpOut io = E.D.ipouts[sd.ip_begin() + oi];
     const double* r = E.s_fin + fin0;
     double v;
@@ -1042,7 +1102,7 @@ __device__ __forceinline__ void build_tables(const DevProgram& D, const RunArgs&
   const int nrot = pd->rot_end - pd->rot_begin;
   for (int r = lane; r < nrot; r += width)
     cs[r] = valid ? rot_cs(D, A, b, pd->rot_begin + r) : make_double2(1.0, 0.0);
-  __syncthreads();
+  vsync();
   const int nblk = pd->blk_end - pd->blk_begin;
   for (int k = lane; k < nblk; k += width) {
     const BlockDesc bd = D.blocks[pd->blk_begin + k];
@@ -1062,7 +1122,7 @@ __device__ __forceinline__ void build_tables(const DevProgram& D, const RunArgs&
     o[2] = make_double2(U.c.re, U.c.im);
     o[3] = make_double2(U.d.re, U.d.im);
   }
-  __syncthreads();
+  vsync();
 }
 
 // Global indices of the tile elements a thread visits in a strided loop

@@ -18,7 +18,7 @@ struct TermSm {
 };
 
 __device__ __forceinline__ void stage_terms(const DevProgram& D, TermSm* s_terms) {
-  for (int t = threadIdx.x; t < D.T; t += blockDim.x) {
+  for (int t = vtid(); t < D.T; t += vdim()) {
     TermSm ts;
     ts.mask = D.t_smask[t];
     ts.xmask = D.t_xmask[t];
@@ -61,7 +61,7 @@ __device__ __forceinline__ void observe(const DevProgram& D, const RunArgs& A, c
         p2[i] = xr * xr + xi * xi;
       }
     }
-    for (int m = 0; m < D.M; ++m) s_red[m * (int)blockDim.x + threadIdx.x] = 0.0;
+    for (int m = 0; m < D.M; ++m) s_red[m * (int)vdim() + vtid()] = 0.0;
     for (int t = 0; t < D.T; ++t) {
       const TermSm ts = s_terms[t];
       if (ts.xmask != 0u) continue;
@@ -71,7 +71,7 @@ __device__ __forceinline__ void observe(const DevProgram& D, const RunArgs& A, c
 #pragma unroll
       for (int i = 0; i < E; ++i)
         if (i < count) v += ((p0 ^ (uint32_t)__popc((uint32_t)i & h)) & 1u) ? -p2[i] : p2[i];
-      s_red[ts.obs * (int)blockDim.x + threadIdx.x] += ts.coeff * v;
+      s_red[ts.obs * (int)vdim() + vtid()] += ts.coeff * v;
     }
     if (D.has_xy) {
       // X/Y strings (on-chip states only): Re sum_j conj(psi_j) i^k (-1)^{popc((j^x)&s)} psi_{j^x}
@@ -90,15 +90,15 @@ __device__ __forceinline__ void observe(const DevProgram& D, const RunArgs& A, c
           double r = ph == 0 ? re : ph == 1 ? -im : ph == 2 ? -re : im;
           v += (__popc(kx & ts.mask) & 1) ? -r : r;
         }
-        s_red[ts.obs * (int)blockDim.x + threadIdx.x] += ts.coeff * v;
+        s_red[ts.obs * (int)vdim() + vtid()] += ts.coeff * v;
       }
     }
-    __syncthreads();
-    const int warp = threadIdx.x >> 5, lane32 = threadIdx.x & 31, nwarp = (blockDim.x + 31) >> 5;
-    const bool narrow = blockDim.x < 32;
+    vsync();
+    const int warp = vtid() >> 5, lane32 = vtid() & 31, nwarp = (vdim() + 31) >> 5;
+    const bool narrow = vdim() < 32;
     for (int task = warp; task < D.M * grp.S; task += nwarp) {
       const int m = task / grp.S, s_ = task - m * grp.S;
-      const double* base = s_red + m * (int)blockDim.x + s_ * grp.TT;
+      const double* base = s_red + m * (int)vdim() + s_ * grp.TT;
       double v = 0.0;
       if (narrow) {
         if (lane32 == 0)
@@ -110,7 +110,7 @@ __device__ __forceinline__ void observe(const DevProgram& D, const RunArgs& A, c
       const int64_t bl = bl0 + s_;
       if (lane32 == 0 && bl < A.nb) A.expect[(bl * D.M + m) * n_tiles + tile] = v;
     }
-    __syncthreads();
+    vsync();
   }
   if constexpr (DUAL) {
     if (seed_mode != 0) {
@@ -173,7 +173,7 @@ struct SmemLayout {
     fin = o; o += (size_t)2 * red_slots * S * 8;  // two buffers (lagged JIT reductions)
     up = o; o += (size_t)S * M * 8;
     terms = o; o += (size_t)n_terms * sizeof(TermSm);
-    total = o + 16;
+    total = (o + 16 + 127) & ~(size_t)127;  // 128-byte aligned: ping-pong groups sit back to back
   }
 };
 
@@ -184,12 +184,12 @@ enum { KM_FWD = 0, KM_DUAL = 1, KM_SPLIT = 2 };
 template <int R, int KM>
 __device__ __forceinline__ Group make_group(int threads_per_role, int samples) {
   Group g;
-  g.tid = threadIdx.x;
+  g.tid = vtid();
   g.TPS = threads_per_role;
   g.TT = KM == KM_SPLIT ? 2 * threads_per_role : threads_per_role;
   g.S = samples;
-  const int lane = threadIdx.x % g.TT;
-  g.sl = threadIdx.x / g.TT;
+  const int lane = vtid() % g.TT;
+  g.sl = vtid() / g.TT;
   g.role = lane / g.TPS;
   g.gi = lane % g.TPS;
   g.W = g.TT >= 32 ? g.TT >> 5 : 1;
@@ -307,33 +307,36 @@ __device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A)
   const PassDesc* pd = D.passes + A.pass;
   const int k = PM::kConst ? PM::k : pd->k, Nt = 1 << k;
   // threads per tile (the walk stride): compile time for JIT pass maps
-  const int wstride = PM::kConst ? ((KM == KM_SPLIT ? 2 : 1) << (PM::k - R)) : (int)blockDim.x;
+  const int wstride = PM::kConst ? ((KM == KM_SPLIT ? 2 : 1) << (PM::k - R)) : (int)vdim();
   const uint32_t flags = A.flags;
   const Group grp = make_group<R, KM>(1 << (k - R), 1);
-  const int tile = blockIdx.x, n_tiles = gridDim.x;
+  // ping-pong kernels: CTA x holds tiles kCtaGroups * x + group
+  const int tile = (int)(blockIdx.x * kCtaGroups + cta_group()), n_tiles = (int)gridDim.x * kCtaGroups;
   const int64_t bl = blockIdx.y;
   const int64_t b = A.b0 + bl;
   const size_t N = (size_t)1 << D.n;
   const uint32_t tile_base = PM::tile_dep(pd, D.n, (uint32_t)tile);
-  const SmemLayout L(1, Nt, ADJ, D.max_rot_pass, D.max_blk_pass, D.max_av_pass, A.red_slots, (int)blockDim.x,
+  const SmemLayout L(1, Nt, ADJ, D.max_rot_pass, D.max_blk_pass, D.max_av_pass, A.red_slots, (int)vdim(),
                      D.M, D.T, (int)sizeof(cplx_t));
-  cplx_t* s_psi = reinterpret_cast<cplx_t*>(smem_raw + L.psi);
-  cplx_t* s_phi = reinterpret_cast<cplx_t*>(smem_raw + L.phi);
-  double2* s_cs = reinterpret_cast<double2*>(smem_raw + L.cs);
-  double2* s_u = reinterpret_cast<double2*>(smem_raw + L.u);
-  double* s_av = reinterpret_cast<double*>(smem_raw + L.av);
-  double* s_red = reinterpret_cast<double*>(smem_raw + L.red);
-  double* s_fin = reinterpret_cast<double*>(smem_raw + L.fin);
-  double* s_up = reinterpret_cast<double*>(smem_raw + L.up);
-  TermSm* s_terms = reinterpret_cast<TermSm*>(smem_raw + L.terms);
+  unsigned char* const smem_grp = smem_raw + (size_t)cta_group() * L.total;  // this group's carve-up
+  cplx_t* s_psi = reinterpret_cast<cplx_t*>(smem_grp + L.psi);
+  cplx_t* s_phi = reinterpret_cast<cplx_t*>(smem_grp + L.phi);
+  double2* s_cs = reinterpret_cast<double2*>(smem_grp + L.cs);
+  double2* s_u = reinterpret_cast<double2*>(smem_grp + L.u);
+  double* s_av = reinterpret_cast<double*>(smem_grp + L.av);
+  double* s_red = reinterpret_cast<double*>(smem_grp + L.red);
+  double* s_fin = reinterpret_cast<double*>(smem_grp + L.fin);
+  double* s_up = reinterpret_cast<double*>(smem_grp + L.up);
+  TermSm* s_terms = reinterpret_cast<TermSm*>(smem_grp + L.terms);
   if (flags & (F_OBSERVE | F_SEED)) stage_terms(D, s_terms);
 
   long long tdbg = A.dbg ? clock64() : 0;
-  if (A.dbg && threadIdx.x == 0) atomicAdd(A.dbg + DBG_CTAS, 1ull);
+  if (A.dbg && vtid() == 0) atomicAdd(A.dbg + DBG_CTAS, 1ull);
+  turn_init();
   if (ADJ && (flags & F_SEED) && A.bra < 0)
-    for (int m = threadIdx.x; m < D.M; m += blockDim.x) s_up[m] = A.upstream[b * D.M + m];
+    for (int m = vtid(); m < D.M; m += vdim()) s_up[m] = A.upstream[b * D.M + m];
   if (flags & F_INIT) {
-    for (int l = threadIdx.x; l < Nt; l += blockDim.x)
+    for (int l = vtid(); l < Nt; l += vdim())
       s_psi[swz((uint32_t)l)] = mk_c((tile_base == 0 && l == 0) ? 1 : 0, 0);
   } else {
     // asynchronous 16-byte copies straight into the swizzled tile; they land
@@ -341,7 +344,7 @@ __device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A)
     const cplx_t* src = ((flags & F_LOAD_FIN) ? A.psi_fin : A.psi) + (size_t)bl * N;
     const cplx_t* srcf = A.phi + (size_t)bl * N;
     const bool lphi = ADJ && (flags & F_LOAD_PHI);
-    const TileWalk tw = tile_walk<PM>(pd, tile_base, k, threadIdx.x, wstride);
+    const TileWalk tw = tile_walk<PM>(pd, tile_base, k, vtid(), wstride);
     for_tile<OBS_E>(tw, [&](uint32_t sw, uint32_t j) {
       cp_async_elem(s_psi + sw, src + j);
       if (lphi) cp_async_elem(s_phi + sw, srcf + j);
@@ -355,14 +358,14 @@ __device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A)
     const double* tcs = t + 2 * pd->rot_begin;
     const double* tu = t + 2 * (size_t)D.n_rot + 8 * (size_t)pd->blk_begin;
     const double* tav = t + 2 * (size_t)D.n_rot + 8 * (size_t)D.n_blk + 4 * (size_t)pd->av_begin;
-    for (int i = threadIdx.x; i < nrot; i += blockDim.x) cp_async16(s_cs + i, tcs + 2 * i);
-    for (int i = threadIdx.x; i < 4 * nblk; i += blockDim.x) cp_async16(s_u + i, tu + 2 * i);
-    for (int i = threadIdx.x; i < 2 * nav; i += blockDim.x) cp_async16(s_av + 2 * i, tav + 2 * i);
+    for (int i = vtid(); i < nrot; i += vdim()) cp_async16(s_cs + i, tcs + 2 * i);
+    for (int i = vtid(); i < 4 * nblk; i += vdim()) cp_async16(s_u + i, tu + 2 * i);
+    for (int i = vtid(); i < 2 * nav; i += vdim()) cp_async16(s_av + 2 * i, tav + 2 * i);
   } else {
-    build_tables(D, A, pd, b, true, s_cs, s_u, s_av, threadIdx.x, blockDim.x);
+    build_tables(D, A, pd, b, true, s_cs, s_u, s_av, vtid(), vdim());
   }
   cp_async_wait_all();
-  __syncthreads();
+  vsync();
   dbg_add(A, DBG_PROLOGUE, tdbg);
   const SampleTables T{s_cs, s_u, pd->rot_begin, pd->blk_begin};
   if (flags & F_FWD)
@@ -372,14 +375,14 @@ __device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A)
   if (flags & F_STORE_FIN) {
     uint32_t tb = tile_base;
     asm volatile("" : "+r"(tb));
-    const TileWalk tw = tile_walk<PM>(pd, tb, k, threadIdx.x, wstride);
+    const TileWalk tw = tile_walk<PM>(pd, tb, k, vtid(), wstride);
     cplx_t* dst = A.psi_fin + (size_t)bl * N;
     for_tile<OBS_E>(tw, [&](uint32_t sw, uint32_t j) { dst[j] = s_psi[sw]; });
   }
   if (flags & (F_OBSERVE | F_SEED)) {
     observe<ADJ, OBS_E, PM>(D, A, pd, s_psi, s_phi, s_up, s_terms, grp, s_red, s_fin, tile_base, k, bl, (flags & F_OBSERVE) != 0,
                  (flags & F_SEED) ? (A.bra < 0 ? 1 : 2) : 0, A.bra, tile, n_tiles);
-    __syncthreads();
+    vsync();
   }
   dbg_add(A, DBG_OBSERVE, tdbg);
   if constexpr (ADJ) {
@@ -393,7 +396,7 @@ __device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A)
     asm volatile("" ::: "memory");
     uint32_t tb = tile_base;
     asm volatile("" : "+r"(tb));  // rebuild the tile walk here rather than keep it live
-    const TileWalk tw = tile_walk<PM>(pd, tb, k, threadIdx.x, wstride);
+    const TileWalk tw = tile_walk<PM>(pd, tb, k, vtid(), wstride);
     const bool spsi = (flags & F_STORE_PSI) != 0;
     cplx_t* dst = A.psi + (size_t)bl * N;
     cplx_t* dstf = A.phi + (size_t)bl * N;
@@ -403,6 +406,7 @@ __device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A)
     });
   }
   dbg_add(A, DBG_STORE, tdbg);
+  turn_fini();
 }
 
 }  // namespace vqc
