@@ -347,6 +347,7 @@ struct VqcPlan {
   // Separate forward schedule for HBM plans (its own tile size / register
   // slots, VQC_FWD_TILE / VQC_FWD_REG); null = `prog` runs forward and adjoint
   ProgDev* fwd = nullptr;
+  unsigned* d_check = nullptr;  // VQC_CHECKS: device bounds-check failure bits
   // host-call cache
   std::mutex mu;
   cudaStream_t stream = nullptr;
@@ -509,8 +510,27 @@ int run_tile_reduce(const double* in, double* out, int64_t count, int n_tiles, c
 }
 
 // run forward (+ adjoint) for all rows; fills ip (B,K,NG) and d_expect
+int run_core_impl(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, const double* d_up,
+                  double* d_expect, int mode, char* ws, const Layout& L, cudaStream_t st);
+
+// run_core_impl, plus the device bounds checks of VQC_CHECKS plans: the
+// failure bits are cleared before the launches and read back after them
 int run_core(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, const double* d_up,
              double* d_expect, int mode, char* ws, const Layout& L, cudaStream_t st) {
+  if (p->d_check && cudaMemsetAsync(p->d_check, 0, sizeof(unsigned), st) != cudaSuccess)
+    return cuda_fail(cudaGetLastError(), "check reset");
+  const int rc = run_core_impl(p, d_in, d_w, B, d_up, d_expect, mode, ws, L, st);
+  if (rc || !p->d_check) return rc;
+  unsigned bits = 0;
+  cudaError_t e = cudaMemcpyAsync(&bits, p->d_check, sizeof bits, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "check read-back");
+  if (bits) return fail(VQC_E_CUDA, "device bounds check failed (bits " + std::to_string(bits) + ")");
+  return VQC_OK;
+}
+
+int run_core_impl(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, const double* d_up,
+                  double* d_expect, int mode, char* ws, const Layout& L, cudaStream_t st) {
   const HostProgram& P = p->prog;
   const DevProgram& D = p->D;
   RunArgs A{};
@@ -519,6 +539,7 @@ int run_core(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, const
   A.upstream = d_up;
   A.K = L.K;
   A.red_slots = red_slots(p);
+  A.check = p->d_check;
   static unsigned long long* dbg = nullptr;
   const bool dbg_on = env_int("VQC_DEBUG_TIMING", 0) != 0;
   if (dbg_on) {
@@ -931,6 +952,7 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
     return rc;
   }
   p->prog.precision = precision;
+  p->prog.checks = env_int("VQC_CHECKS", 0) != 0;
   std::string err;
   cudaError_t e = cudaGetDevice(&p->device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, p->device);
@@ -944,6 +966,7 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
   if (e == cudaSuccess) e = upload(p->tobs, &p->d_tobs);
   if (e == cudaSuccess) e = upload(P.col_offs, &p->d_col_offs);
   if (e == cudaSuccess) e = upload(P.chain, &p->d_chain);
+  if (e == cudaSuccess && P.checks) e = cudaMalloc(reinterpret_cast<void**>(&p->d_check), sizeof(unsigned));
   if (e != cudaSuccess) {
     vqc_plan_destroy(p);
     return cuda_fail(e, "plan upload");
@@ -956,8 +979,8 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
   // circuits are launch-bound and stay on the prebuilt interpreter.
   const int jit_mode = env_int("VQC_JIT", -1);
   // complex64 plans always specialise (the interpreter kernels are complex128)
-  const bool want_jit = precision == 1 || jit_mode > 0 || (jit_mode < 0 && (P.hbm || P.n >= 4));
-  if (want_jit && (P.n_fwd_ops + P.n_bwd_ops > 0 || precision == 1)) {
+  const bool want_jit = precision == 1 || P.checks || jit_mode > 0 || (jit_mode < 0 && (P.hbm || P.n >= 4));
+  if (want_jit && (P.n_fwd_ops + P.n_bwd_ops > 0 || precision == 1 || P.checks)) {
     // HBM adjoint with both states per thread when its register slots allow
     // (VQC_ADJ_DUAL overrides: 0 = thread pairs)
     if ((P.hbm || (P.R <= 3 && smem_dual(P.n))) && env_int("VQC_ADJ_DUAL", P.R <= 3 ? 1 : 0) != 0)
@@ -988,6 +1011,7 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
         return rc;
       }
       f->prog.precision = precision;
+      f->prog.checks = P.checks;
       f->prog.pingpong = (f->prog.n - f->prog.k >= 1 && 2 * pass_smem(p, f->prog, false) <= (size_t)kMaxSmemBytes)
                              ? pingpong : 0;
       if (!f->prog.hbm || f->prog.NG != P.NG) {
@@ -1025,6 +1049,7 @@ void vqc_plan_destroy(VqcPlan* p) {
   cudaFree(p->d_tobs);
   cudaFree(p->d_col_offs);
   cudaFree(p->d_chain);
+  cudaFree(p->d_check);
   if (p->h_dev) cudaFree(p->h_dev);
   if (p->stream) cudaStreamDestroy(p->stream);
   delete p;

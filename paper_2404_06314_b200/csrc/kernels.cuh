@@ -148,9 +148,30 @@ struct RunArgs {
   int red_slots;           // reduction slots per buffer
   int jacobian;            // smem mode: loop over all M bras in-kernel
   unsigned long long* dbg; // VQC_DEBUG_TIMING: per-phase clock64 totals (thread 0 of each CTA)
+  unsigned int* check;     // VQC_CHECKS: bounds-check failure bits (VQC_DEVICE_CHECKS kernels)
   const double* tables;    // HBM mode: per-sample tables from k_tables (rows relative to b0)
   int64_t table_stride;    // doubles per sample
 };
+
+// Device bounds checks (plans created with VQC_CHECKS=1 compile their JIT
+// units with VQC_DEVICE_CHECKS): every shared-memory tile address of the
+// register loads / stores and the observe step, and every global state index
+// of the tile loads / stores, is range-checked; a failure ORs a bit into
+// A.check and the host call fails. (compute-sanitizer is closed on this
+// pool; these checks plus the bitwise run / chunking invariance tests stand
+// in for memcheck / racecheck.)
+enum { CHK_SEG_LOAD = 1u, CHK_SEG_STORE = 2u, CHK_TILE_GLOBAL = 4u, CHK_TILE_SMEM = 8u, CHK_OBSERVE = 16u,
+       CHK_IP_OUT = 32u };
+#ifdef VQC_DEVICE_CHECKS
+#define VQC_CHECK(A, cond, bit) \
+  do {                          \
+    if (!(cond)) atomicOr((A).check, (unsigned)(bit)); \
+  } while (0)
+#else
+#define VQC_CHECK(A, cond, bit) \
+  do {                          \
+  } while (0)
+#endif
 
 // phase timing (debug only): dbg[slot] += clock64 delta, slots fixed below
 enum { DBG_PROLOGUE = 0, DBG_FWD = 1, DBG_OBSERVE = 2, DBG_BWD = 3, DBG_STORE = 4, DBG_SEG_LOAD = 5,
@@ -913,6 +934,7 @@ __device__ __forceinline__ void seg_begin(const SegEnv& E, const SD& sd, SegCtx<
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       const uint32_t ad = C.addr(i);
+      VQC_CHECK(E.A, ad < (1u << E.D.k), CHK_SEG_LOAD);
       a[i] = E.own[ad];
       if constexpr (MODE == MODE_DUAL) f[i] = E.s_phi[ad];
     }
@@ -973,6 +995,7 @@ __device__ __forceinline__ void seg_end(const SegEnv& E, const SD& sd, const Reg
 #pragma unroll
       for (int s = 0; s < R; ++s)
         if ((i >> s) & 1) ad ^= sc[s];
+      VQC_CHECK(A, ad < (1u << E.D.k), CHK_SEG_STORE);
       E.own[ad] = a[i];
       if constexpr (MODE == MODE_DUAL) E.s_phi[ad] = f[i];
     }
@@ -1015,6 +1038,7 @@ __device__ __forceinline__ void seg_end(const SegEnv& E, const SD& sd, const Reg
           v = av[0] * r[io.red * grp.S] + av[1] * r[(io.red + 1) * grp.S] + av[2] * r[(io.red + 2) * grp.S];
         }
         const int64_t bl = E.bl0 + s_;
+        VQC_CHECK(A, io.gslot >= 0 && io.gslot < E.D.NG && E.tile < E.n_tiles, CHK_IP_OUT);
         if (bl < A.nb) A.ip[(((bl * A.K) + E.bra) * E.D.NG + io.gslot) * E.n_tiles + E.tile] = v;
       }
     }

@@ -52,6 +52,7 @@ struct HostProgram {
   int absorbed = 0;  // trailing gates folded into the observables (absorb_trailing_gates)
   bool adj_dual = false;  // HBM adjoint passes: both states per thread (JIT only) instead of thread pairs
   int precision = 0;      // 0 = complex128 states, 1 = complex64 (JIT kernels compiled with VQC_C64)
+  bool checks = false;    // JIT units with device bounds checks (VQC_CHECKS)
   int pingpong = 0;       // HBM pass kernels: two tiles per CTA; 1 = arithmetic phases alternate,
                           // 2 = shared-memory phases alternate (VQC_PINGPONG, default off)
 };

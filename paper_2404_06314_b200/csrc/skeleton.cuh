@@ -56,6 +56,7 @@ __device__ __forceinline__ void observe(const DevProgram& D, const RunArgs& A, c
     for (int i = 0; i < E; ++i) {
       p2[i] = 0.0;
       if (i < count) {
+        VQC_CHECK(A, swz((uint32_t)lane + (uint32_t)i * (uint32_t)grp.TT) < (1u << k), CHK_OBSERVE);
         const cplx_t x = s_psi[swz((uint32_t)lane + (uint32_t)i * (uint32_t)grp.TT)];
         const double xr = x.x, xi = x.y;   // |psi_j|^2 in float64 for either state type
         p2[i] = xr * xr + xi * xi;
@@ -346,6 +347,8 @@ __device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A)
     const bool lphi = ADJ && (flags & F_LOAD_PHI);
     const TileWalk tw = tile_walk<PM>(pd, tile_base, k, vtid(), wstride);
     for_tile<OBS_E>(tw, [&](uint32_t sw, uint32_t j) {
+      VQC_CHECK(A, j < (uint32_t)N, CHK_TILE_GLOBAL);
+      VQC_CHECK(A, sw < (uint32_t)Nt, CHK_TILE_SMEM);
       cp_async_elem(s_psi + sw, src + j);
       if (lphi) cp_async_elem(s_phi + sw, srcf + j);
     });
@@ -401,6 +404,7 @@ __device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A)
     cplx_t* dst = A.psi + (size_t)bl * N;
     cplx_t* dstf = A.phi + (size_t)bl * N;
     for_tile<OBS_E>(tw, [&](uint32_t sw, uint32_t j) {
+      VQC_CHECK(A, j < (uint32_t)N && sw < (uint32_t)Nt, CHK_TILE_GLOBAL);
       if (spsi) dst[j] = s_psi[sw];
       if (sphi) dstf[j] = s_phi[sw];
     });
