@@ -760,6 +760,11 @@ int schedule_circuit(const VqcCircuit* c, const int64_t* wrt_col, HostProgram* p
     opt.reg_slots = std::max(3, std::min(4, env_int("VQC_REG_SLOTS", kHbmAdjointRegs)));
   // small on-chip JIT plans: 3 slots, both states per thread (smem_dual)
   if (c->n_qubits <= opt.smem_max_qubits && smem_dual(c->n_qubits)) opt.reg_slots = 3;
+  // HBM plans run JIT kernels, whose address maps take CNOT folds onto
+  // thread-bit targets (boundary CNOTs then need no register slot: cfg4 80 ->
+  // 62 adjoint and 62 -> 52 forward segments); VQC_FOLD_THREAD_TARGETS=0 off
+  opt.fold_thread_targets = c->n_qubits > opt.smem_max_qubits && env_int("VQC_JIT", -1) != 0 &&
+                            env_int("VQC_FOLD_THREAD_TARGETS", 1) != 0;
   if (tile_override > 0) opt.tile_qubits = tile_override;
   if (regs_override > 0) opt.reg_slots = regs_override;
   const int absorbed = prog->absorbed;

@@ -903,6 +903,22 @@ struct RtSeg {
   __device__ __forceinline__ int ip_count() const { return sd->ip_count; }
   __device__ __forceinline__ int red_count() const { return sd->red_count; }
   __device__ __forceinline__ int ip_begin() const { return sd->ip_begin; }
+  // translation of the load / store base by the tile's (non-local) bits:
+  // folded CNOTs controlled by tile bits (register targets only here, gen = 0)
+  __device__ __forceinline__ uint32_t tile_ld(uint32_t tb) const {
+    uint32_t t0 = 0u;
+#pragma unroll
+    for (int t = 0; t < kMaxR; ++t)
+      if (__popc(tb & sd->ld_k[t]) & 1) t0 ^= sd->ps[t];
+    return t0;
+  }
+  __device__ __forceinline__ uint32_t tile_st(uint32_t tb) const {
+    uint32_t t0 = 0u;
+#pragma unroll
+    for (int t = 0; t < kMaxR; ++t)
+      if (__popc(tb & sd->st_k[t]) & 1) t0 ^= sd->ps[t];
+    return t0;
+  }
 };
 
 // segment start: address maps and the register load (shared-memory transpose)
@@ -923,11 +939,7 @@ __device__ __forceinline__ void seg_begin(const SegEnv& E, const SD& sd, SegCtx<
     C.lp0 = e01.y;
   }
   // folded CNOT runs controlled by tile (non-local) bits
-  if (E.tile_base != 0) {
-#pragma unroll
-    for (int t = 0; t < R; ++t)
-      if (__popc(E.tile_base & sd.ld_k(t)) & 1) C.lp0 ^= sd.ps(t);
-  }
+  if (E.tile_base != 0) C.lp0 ^= sd.tile_ld(E.tile_base);
 #pragma unroll
   for (int t = 0; t < R; ++t) C.lc[t] = sd.ldc(t);
   if (E.active) {
@@ -981,11 +993,7 @@ __device__ __forceinline__ void seg_end(const SegEnv& E, const SD& sd, const Reg
       const ThrEntry* te = E.D.thr_tab + sd.thr_off() + (grp.gi & ((1 << sd.nthr()) - 1));
       sp0 = te->sp0;
     }
-    if (E.tile_base != 0) {
-#pragma unroll
-      for (int t = 0; t < R; ++t)
-        if (__popc(E.tile_base & sd.st_k(t)) & 1) sp0 ^= sd.ps(t);
-    }
+    if (E.tile_base != 0) sp0 ^= sd.tile_st(E.tile_base);
     asm volatile("" : "+r"(sp0));
 #pragma unroll
     for (int t = 0; t < R; ++t) sc[t] = sd.stc(t);

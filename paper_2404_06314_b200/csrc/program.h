@@ -40,6 +40,7 @@ constexpr int kMaxR = 5;            // register slots per thread (max)
 constexpr int kMaxQubits = 24;      // statevector.py:21
 constexpr int kSmemMaxQubits = 12;  // on-chip (single pass) limit
 constexpr int kMaxFactors = 4;      // factors per angle expression on this path
+constexpr int kMaxTile = 16;        // tile-local positions a segment's address maps cover
 
 // gate codes (_kernels.py:16-22, CZ new)
 enum GateKind : int { G_RX = 0, G_RY = 1, G_RZ = 2, G_CNOT = 3, G_H = 4, G_X = 5, G_CZ = 6 };
@@ -113,6 +114,15 @@ struct SegDesc {
   int8_t reg_g[kMaxR];         // global qubit of each register slot
   int8_t thr_l[kMaxQubits];    // tile-local bit position of thread-index bit i
   int8_t thr_g[kMaxQubits];    // global qubit of thread-index bit i
+  // General form of the folded CNOT maps: output bit of tile-local position p
+  // = parity(index & row[p]) over global bits (identity: 1 << local_q[p]).
+  // The register columns ldc / stc are derived from these rows. Interpreter
+  // plans only fold CNOTs whose target is a register slot (ld_col / ld_k
+  // describe those maps completely, gen = 0); JIT HBM plans may also fold
+  // CNOTs onto thread-bit targets (gen = 1), which the JIT emits from the
+  // rows (thread bases and tile translations).
+  uint32_t ld_row[kMaxTile], st_row[kMaxTile];
+  int8_t gen;
 };
 
 // Per (segment, thread group) precomputed addressing: thread-bit part of

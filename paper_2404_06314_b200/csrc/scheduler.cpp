@@ -112,9 +112,11 @@ std::string analyze(const std::vector<GateIn>& gates, int n, int64_t total_param
 // fold_cnots (register segments): keep each group of the form
 // [CNOTs][body][CNOTs] so both CNOT runs fold into the segment's shared-memory
 // address maps instead of costing register permutations.
+// free_folds: boundary CNOTs fold into the address maps whatever their
+// target (a tile-local qubit), so they take no register slot.
 std::vector<Group> greedy_groups(const std::vector<int>& todo, const std::vector<GateInfo>& info,
                                  int cap, uint32_t forced, std::vector<uint8_t>& status,
-                                 bool fold_cnots = false, int variants = 1) {
+                                 bool fold_cnots = false, int variants = 1, bool free_folds = false) {
   std::vector<Group> groups;
   std::vector<int> remaining = todo;
   // One scan of `remaining`: variant v refuses the first v requests for new
@@ -131,7 +133,9 @@ std::vector<Group> greedy_groups(const std::vector<int>& todo, const std::vector
         if (status[p] != 1 && status[p] != 2) { ok = false; break; }
       if (ok && fold_cnots && phase == 2 && !info[g].cnot) ok = false;
       if (ok) {
-        const uint32_t m = grp.mask | info[g].mix;
+        // in a folded group every CNOT is leading or trailing (body CNOTs end the body)
+        const bool free_cnot = free_folds && fold_cnots && info[g].cnot;
+        const uint32_t m = grp.mask | (free_cnot ? 0u : info[g].mix);
         if (m != grp.mask && refused < v) {
           ++refused;
           ok = false;
@@ -289,7 +293,8 @@ std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total
     {
       std::vector<uint8_t> st2(G, 1);
       for (int g : pg.gates) st2[g] = 0;
-      std::vector<Group> folded = greedy_groups(pg.gates, info, R, 0u, st2, true, opt.variants);
+      std::vector<Group> folded = greedy_groups(pg.gates, info, R, 0u, st2, true, opt.variants,
+                                                opt.fold_thread_targets);
       for (int g : pg.gates) st2[g] = 0;
       std::vector<Group> free_ = greedy_groups(pg.gates, info, R, 0u, st2, false, opt.variants);
       const int seg_cost = opt.segment_cost, cnot_cost = 1;
@@ -381,22 +386,27 @@ std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total
         if (gi.kind == G_CNOT) open_blk[gi.q0] = open_blk[gi.q1] = -1;
         items.push_back({0, {g}});
       }
-      for (const Item& it : items)
-        for (int g : it.gates)
-          if ((info[g].mix & sgp.mask) != info[g].mix) return "internal: mixing qubit not in registers";
-
       // leading / trailing CNOT runs fold into the load / store address maps
       auto is_cnot = [&](const Item& it) { return it.type == 0 && gates[it.gates[0]].kind == G_CNOT; };
       size_t lead = 0;
       while (lead < items.size() && is_cnot(items[lead])) ++lead;
       size_t trail = items.size();
       while (trail > lead && is_cnot(items[trail - 1])) --trail;
+      for (size_t i = 0; i < items.size(); ++i) {
+        const bool folded_cnot = (i < lead || i >= trail) && opt.fold_thread_targets;
+        for (int g : items[i].gates)
+          if (!folded_cnot && (info[g].mix & sgp.mask) != info[g].mix)
+            return "internal: mixing qubit not in registers";
+          else if (folded_cnot && !(pg.mask >> gates[g].q1 & 1u))
+            return "internal: folded CNOT target not in the tile";
+      }
       // affine map of a CNOT sequence, restricted to register bits: register
       // output bit t = XOR of register inputs col-masks + const qubits kmask
-      auto fold = [&](const std::vector<int>& cnots, uint8_t* col, uint32_t* kmask) {
+      auto fold = [&](const std::vector<int>& cnots, uint8_t* col, uint32_t* kmask, uint32_t* lrow) {
         uint32_t row[kMaxQubits];  // row[q]: global-bit mask feeding output bit q
         for (int q = 0; q < n; ++q) row[q] = 1u << q;
         for (int g : cnots) row[gates[g].q1] ^= row[gates[g].q0];
+        for (int p = 0; p < kMaxTile; ++p) lrow[p] = p < k ? row[(int)pd.local_q[p]] : 0u;
         uint32_t regmask = 0;
         for (int s2 = 0; s2 < ns; ++s2) regmask |= 1u << sd.reg_g[s2];
         for (int s2 = 0; s2 < kMaxR; ++s2) { col[s2] = 0; kmask[s2] = 0; }
@@ -413,17 +423,27 @@ std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total
       {
         // loads see C_lead^{-1} (the lead CNOTs in reverse order); stores C_trail
         std::vector<int> inv(lead_g.rbegin(), lead_g.rend());
-        fold(inv, sd.ld_col, sd.ld_k);
-        fold(trail_g, sd.st_col, sd.st_k);
+        fold(inv, sd.ld_col, sd.ld_k, sd.ld_row);
+        fold(trail_g, sd.st_col, sd.st_k, sd.st_row);
+        // register columns: the swizzled address of register bit s under the
+        // map = XOR of swz(e_p) over output positions p whose row reads it
         for (int s2 = 0; s2 < kMaxR; ++s2) {
           uint32_t lcv = 0, scv = 0;
-          for (int t = 0; t < ns; ++t) {
-            if (sd.ld_col[s2] >> t & 1u) lcv ^= sd.ps[t];
-            if (sd.st_col[s2] >> t & 1u) scv ^= sd.ps[t];
-          }
+          if (s2 < ns)
+            for (int p = 0; p < k; ++p) {
+              if (sd.ld_row[p] >> sd.reg_g[s2] & 1u) lcv ^= swz_index(1u << p);
+              if (sd.st_row[p] >> sd.reg_g[s2] & 1u) scv ^= swz_index(1u << p);
+            }
           sd.ldc[s2] = (uint16_t)lcv;
           sd.stc[s2] = (uint16_t)scv;
         }
+        // general maps: some thread-bit output reads other bits
+        sd.gen = 0;
+        for (int p = 0; p < k; ++p)
+          if (!(sgp.mask >> pd.local_q[p] & 1u) &&
+              (sd.ld_row[p] != (1u << pd.local_q[p]) || sd.st_row[p] != (1u << pd.local_q[p])))
+            sd.gen = 1;
+        if (sd.gen && !opt.fold_thread_targets) return "internal: general CNOT fold in an interpreter plan";
       }
       std::vector<Item> body(items.begin() + lead, items.begin() + trail);
       // consecutive fused blocks (distinct slots, commuting) dispatch as one set
@@ -547,6 +567,7 @@ std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total
         std::swap(sd.ld_k[s2], sd.st_k[s2]);
         std::swap(sd.ldc[s2], sd.stc[s2]);
       }
+      for (int p2 = 0; p2 < kMaxTile; ++p2) std::swap(sd.ld_row[p2], sd.st_row[p2]);
       int slot_of[kMaxQubits];
       for (int q = 0; q < kMaxQubits; ++q) slot_of[q] = -1;
       for (int s2 = 0; s2 < sd.nreg; ++s2) slot_of[(int)sd.reg_g[s2]] = s2;

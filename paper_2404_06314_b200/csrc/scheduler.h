@@ -24,6 +24,7 @@ struct ScheduleOptions {
   int smem_max_qubits = kSmemMaxQubits;  // n above this streams tiles through HBM
   int segment_cost = 4;      // price of a segment boundary in interior-CNOT units
   int variants = 1;          // greedy restarts per group (refuse the first v new-qubit requests)
+  bool fold_thread_targets = false;  // boundary CNOTs may target thread bits (JIT HBM plans)
 };
 
 struct HostProgram {

@@ -9,6 +9,7 @@
 // rely on (tile sizes, slot/thread-bit partitions, mixing operands in
 // registers). It does not model the kernels' tiling arithmetic (swizzle,
 // pdep); the GPU parity tests cover that.
+#include <stdexcept>
 #include <array>
 #include <cmath>
 #include <cstdio>
@@ -167,6 +168,10 @@ std::string check_program(const HostProgram& P, const ScheduleOptions& opt) {
 
 }  // namespace
 
+static int sim_exec(const HostProgram& P, int n, int M, const int64_t* term_offs, const std::vector<uint32_t>& zm,
+                    const std::vector<double>& zc, const double* flat, const double* upstream, double* expect_out,
+                    double* grad_out, int64_t* stats);
+
 extern "C" {
 
 // One row: flat (total_params) with the encoding slice already set.
@@ -191,6 +196,12 @@ int sim_run(int n, int64_t G, const int64_t* kinds, const int64_t* q0, const int
   opt.tile_qubits = tile_qubits;
   opt.smem_max_qubits = smem_max_qubits;
   opt.reg_slots = reg_slots;
+  // boundary CNOTs folded onto thread-bit targets, as JIT HBM plans do
+  // (VQC_FOLD_THREAD_TARGETS=0 turns it off, like the engine)
+  {
+    const char* ft = getenv("VQC_FOLD_THREAD_TARGETS");
+    opt.fold_thread_targets = n > smem_max_qubits && !(ft && ft[0] == '0');
+  }
   // as vqc_plan_create: trailing CNOT / CZ / X gates fold into the (Z-string)
   // observables, which the expectation step below then uses
   const int64_t T = M > 0 ? term_offs[M] : 0;
@@ -205,6 +216,19 @@ int sim_run(int n, int64_t G, const int64_t* kinds, const int64_t* q0, const int
     snprintf(err, (size_t)errcap, "%s", e.c_str());
     return -1;
   }
+  try {
+    return sim_exec(P, n, M, term_offs, zm, zc, flat, upstream, expect_out, grad_out, stats);
+  } catch (const std::exception& ex) {
+    snprintf(err, (size_t)errcap, "%s", ex.what());
+    return -2;
+  }
+}
+
+}  // extern "C"
+
+static int sim_exec(const HostProgram& P, int n, int M, const int64_t* term_offs, const std::vector<uint32_t>& zm,
+                    const std::vector<double>& zc, const double* flat, const double* upstream, double* expect_out,
+                    double* grad_out, int64_t* stats) {
   int nseg = 0;
   for (const PassDesc& pd : P.passes) nseg += pd.seg_end - pd.seg_begin;
   stats[0] = (int64_t)P.passes.size();
@@ -238,8 +262,17 @@ int sim_run(int n, int64_t G, const int64_t* kinds, const int64_t* q0, const int
                           [&](int slot, const double* v) { avec[slot] = {v[0], v[1], v[2]}; });
   }
   int cur_blk_base = 0;
-  // folded CNOT runs: register bits of every index are remapped through
-  // (col, k) exactly as the kernels compute their smem addresses
+  // folded CNOT runs: every tile-local output bit p of an index is
+  // parity(index & row[p]) (SegDesc ld_row / st_row), the general form the
+  // JIT kernels compute their smem addresses from; for interpreter plans
+  // (gen = 0) the rows must agree with the register-only (col, k) form
+  const PassDesc* cur_pd = nullptr;
+  auto remap_rows = [&](const uint32_t* row, uint32_t x) {
+    uint32_t out = x & ~cur_pd->local_mask;
+    for (int p = 0; p < P.k; ++p)
+      out |= (uint32_t)(__builtin_popcount(x & row[p]) & 1) << cur_pd->local_q[p];
+    return out;
+  };
   auto remap = [&](const SegDesc& sd, const uint8_t* col, const uint32_t* km, uint32_t x) {
     uint32_t regmask = 0;
     for (int q = 0; q < sd.nreg; ++q) regmask |= 1u << sd.reg_g[q];
@@ -255,15 +288,30 @@ int sim_run(int n, int64_t G, const int64_t* kinds, const int64_t* q0, const int
     for (int q = 0; q < sd.nreg; ++q) out |= ((y >> q) & 1u) << sd.reg_g[q];
     return out;
   };
-  // load: reg content at x = state[remap_ld(x)]; store: state'[remap_st(x)] = reg content at x
+  auto map_ld = [&](const SegDesc& sd, uint32_t x) {
+    const uint32_t r = remap_rows(sd.ld_row, x);
+    if (!sd.gen && r != remap(sd, sd.ld_col, sd.ld_k, x)) {
+      char m[256];
+      snprintf(m, sizeof m, "ld rows disagree: x=%x rows=%x colk=%x nreg=%d reg0=%d row0=%x k0=%x col0=%x", x, r,
+               remap(sd, sd.ld_col, sd.ld_k, x), sd.nreg, sd.reg_g[0], sd.ld_row[0], sd.ld_k[0], sd.ld_col[0]);
+      throw std::runtime_error(m);
+    }
+    return r;
+  };
+  auto map_st = [&](const SegDesc& sd, uint32_t x) {
+    const uint32_t r = remap_rows(sd.st_row, x);
+    if (!sd.gen && r != remap(sd, sd.st_col, sd.st_k, x)) throw std::runtime_error("st rows disagree");
+    return r;
+  };
+  // load: reg content at x = state[map_ld(x)]; store: state'[map_st(x)] = reg content at x
   auto do_load = [&](std::vector<cd>& st, const SegDesc& sd) {
     std::vector<cd> o(st.size());
-    for (size_t x = 0; x < st.size(); ++x) o[x] = st[remap(sd, sd.ld_col, sd.ld_k, (uint32_t)x)];
+    for (size_t x = 0; x < st.size(); ++x) o[x] = st[map_ld(sd, (uint32_t)x)];
     st.swap(o);
   };
   auto do_store = [&](std::vector<cd>& st, const SegDesc& sd) {
     std::vector<cd> o(st.size());
-    for (size_t x = 0; x < st.size(); ++x) o[remap(sd, sd.st_col, sd.st_k, (uint32_t)x)] = st[x];
+    for (size_t x = 0; x < st.size(); ++x) o[map_st(sd, (uint32_t)x)] = st[x];
     st.swap(o);
   };
   auto apply = [&](std::vector<cd>& st, const SegDesc& sd, const Op& op) {
@@ -316,6 +364,7 @@ int sim_run(int n, int64_t G, const int64_t* kinds, const int64_t* q0, const int
   };
   for (const PassDesc& pd : P.passes) {
     cur_blk_base = pd.blk_begin;
+    cur_pd = &pd;
     for (int sg = pd.seg_begin; sg < pd.seg_end; ++sg) {
       const SegDesc& sd = P.segs[sg];
       do_load(S.psi, sd);
@@ -352,6 +401,7 @@ int sim_run(int n, int64_t G, const int64_t* kinds, const int64_t* q0, const int
     for (int pi = (int)P.passes.size() - 1; pi >= 0; --pi) {
       const PassDesc& pd = P.passes[pi];
       cur_blk_base = pd.blk_begin;
+      cur_pd = &pd;
       for (int sg = pd.bseg_begin; sg < pd.bseg_end; ++sg) {
         const SegDesc& sd = P.segs[sg];
         do_load(S.psi, sd);
@@ -383,10 +433,7 @@ int sim_run(int n, int64_t G, const int64_t* kinds, const int64_t* q0, const int
         do_store(S.phi, sd);
         for (int oi = 0; oi < sd.ip_count; ++oi) {
           const IpOut& io = P.ipouts[sd.ip_begin + oi];
-          if (io.red < 0 || io.red >= sd.red_count) {
-            snprintf(err, (size_t)errcap, "IpOut reduction slot out of range");
-            return -1;
-          }
+          if (io.red < 0 || io.red >= sd.red_count) throw std::runtime_error("IpOut reduction slot out of range");
           ipv[io.gslot] = io.avec < 0 ? red[io.red]
                                       : avec[io.avec][0] * red[io.red] + avec[io.avec][1] * red[io.red + 1] +
                                             avec[io.avec][2] * red[io.red + 2];
@@ -407,8 +454,6 @@ int sim_run(int n, int64_t G, const int64_t* kinds, const int64_t* q0, const int
   return 0;
 }
 
-}  // extern "C"
-
 extern "C" {
 // Debug: print the lowered program (op codes per segment) to stdout.
 int sim_dump(int n, int64_t G, const int64_t* kinds, const int64_t* q0, const int64_t* q1,
@@ -428,6 +473,10 @@ int sim_dump(int n, int64_t G, const int64_t* kinds, const int64_t* q0, const in
   opt.tile_qubits = tile_qubits;
   opt.smem_max_qubits = smem_max_qubits;
   opt.reg_slots = reg_slots;
+  {
+    const char* ft = getenv("VQC_FOLD_THREAD_TARGETS");
+    opt.fold_thread_targets = n > smem_max_qubits && !(ft && ft[0] == '0');
+  }
   HostProgram P;
   std::string e = build_program(gates, n, total_params, wc, opt, &P);
   if (!e.empty()) { printf("error: %s\n", e.c_str()); return -1; }

@@ -30,16 +30,22 @@ def test_hbm_plan_has_one_kernel_pair_per_pass():
     assert "exec_op" not in src
 
 
-def test_random_hbm_circuit_compiles_for_sm100a(monkeypatch):
-    """Every gate kind (and so every op the scheduler emits) through NVRTC."""
+@pytest.mark.parametrize("fold", ["0", "1"])
+def test_random_hbm_circuit_compiles_for_sm100a(monkeypatch, fold):
+    """Every gate kind (and so every op the scheduler emits) through NVRTC;
+    with thread-target CNOT folds (default) boundary CNOTs become address
+    maps (tile_ld / thread bases), without them some run in registers."""
     monkeypatch.setenv("VQC_JIT_CACHE", "0")  # really compile (no cubin cache)
+    monkeypatch.setenv("VQC_FOLD_THREAD_TARGETS", fold)
     from test_scheduler_sim import _random
     rng = np.random.default_rng(7)
     circ, _, _ = _random(rng, 13, 60)
     src, secs = _src(circ, ("a", "b", "s"), compile=True)
     assert secs is not None and secs > 0
-    for op in ("jop_cnot", "jop_u2", "jop_ip"):
+    for op in (("jop_cnot",) if fold == "0" else ()) + ("jop_u2", "jop_ip"):
         assert op in src, op
+    if fold == "1":
+        assert "__popc(tb & " in src     # a fold controlled by a tile bit
 
 
 def test_on_chip_plan_shares_code_per_segment_shape(monkeypatch):
