@@ -763,8 +763,11 @@ int schedule_circuit(const VqcCircuit* c, const int64_t* wrt_col, HostProgram* p
   // HBM plans run JIT kernels, whose address maps take CNOT folds onto
   // thread-bit targets (boundary CNOTs then need no register slot: cfg4 80 ->
   // 62 adjoint and 62 -> 52 forward segments); VQC_FOLD_THREAD_TARGETS=0 off
+  // (2 = forward program only, 3 = adjoint / main program only: bisection knobs)
+  const int ftt = env_int("VQC_FOLD_THREAD_TARGETS", 1);
+  const bool fwd_prog = tile_override > 0 || regs_override > 0;
   opt.fold_thread_targets = c->n_qubits > opt.smem_max_qubits && env_int("VQC_JIT", -1) != 0 &&
-                            env_int("VQC_FOLD_THREAD_TARGETS", 1) != 0;
+                            (ftt == 1 || (ftt == 2 && fwd_prog) || (ftt == 3 && !fwd_prog));
   if (tile_override > 0) opt.tile_qubits = tile_override;
   if (regs_override > 0) opt.reg_slots = regs_override;
   const int absorbed = prog->absorbed;

@@ -903,6 +903,9 @@ struct RtSeg {
   __device__ __forceinline__ int ip_count() const { return sd->ip_count; }
   __device__ __forceinline__ int red_count() const { return sd->red_count; }
   __device__ __forceinline__ int ip_begin() const { return sd->ip_begin; }
+  // stores leave the loading threads' cells (CNOT folds onto thread bits):
+  // every thread must finish its loads before any thread stores
+  __device__ __forceinline__ bool st_sync() const { return sd->gen != 0; }
   // translation of the load / store base by the tile's (non-local) bits:
   // folded CNOTs controlled by tile bits (register targets only here, gen = 0)
   __device__ __forceinline__ uint32_t tile_ld(uint32_t tb) const {
@@ -983,7 +986,7 @@ __device__ __forceinline__ void seg_end(const SegEnv& E, const SD& sd, const Reg
   const Group& grp = E.grp;
   const RunArgs& A = E.A;
   phase_b();  // ping-pong hand-over point
-  if (MODE == MODE_SPLIT && sd.ip_count() > 0) vsync();  // partners done reading
+  if ((MODE == MODE_SPLIT && sd.ip_count() > 0) || sd.st_sync()) vsync();  // partners / other cells done reading
   asm volatile("" ::: "memory");  // keep the store map's loads and math after the op loop
   if (E.active) {
     uint32_t sp0, sc[R];

@@ -101,6 +101,41 @@ std::string check_program(const HostProgram& P, const ScheduleOptions& opt) {
         seen |= 1u << sd.thr_g[i];
       }
       if (seen != pd.local_mask) return "slots + thread bits != local set";
+      // the JIT kernels' shared-memory addresses (jit.cpp emit_segment: thread
+      // base from the rows' thread bits, tile translation from their tile
+      // bits, register columns ldc / stc) must equal swz(local part of the
+      // row map) for every thread, register index and tile
+      {
+        const uint32_t nmask = (P.n >= 32) ? 0xffffffffu : ((1u << P.n) - 1u);
+        const uint32_t thr_mask = pd.local_mask & ~[&] { uint32_t r = 0; for (int q = 0; q < sd.nreg; ++q) r |= 1u << sd.reg_g[q]; return r; }();
+        const uint32_t tile_mask = ~pd.local_mask & nmask;
+        auto kernel_addr = [&](const uint32_t* row, const uint16_t* cols, uint32_t j, uint32_t i, uint32_t tb) {
+          uint32_t a = 0;
+          for (int q = 0; q < P.k && q < kMaxTile; ++q) {
+            if (__builtin_popcount(j & row[q] & thr_mask) & 1) a ^= swz_index(1u << q);
+            if (__builtin_popcount(tb & row[q] & tile_mask) & 1) a ^= swz_index(1u << q);
+          }
+          for (int s2 = 0; s2 < sd.nreg; ++s2)
+            if (i >> s2 & 1u) a ^= cols[s2];
+          return a;
+        };
+        auto want_addr = [&](const uint32_t* row, uint32_t x) {
+          uint32_t v = 0;
+          for (int q = 0; q < P.k && q < kMaxTile; ++q) v |= (uint32_t)(__builtin_popcount(x & row[q]) & 1) << q;
+          return swz_index(v);
+        };
+        const uint32_t tiles[3] = {0u, tile_mask, tile_mask & 0x5555u};
+        for (uint32_t g = 0; g < (1u << sd.nthr); ++g)
+          for (uint32_t i = 0; i < (1u << sd.nreg); ++i)
+            for (uint32_t tb : tiles) {
+              uint32_t j = 0, r = 0;
+              for (int b = 0; b < sd.nthr; ++b) j |= ((g >> b) & 1u) << sd.thr_g[b];
+              for (int b = 0; b < sd.nreg; ++b) r |= ((i >> b) & 1u) << sd.reg_g[b];
+              const uint32_t x = j | r | tb;
+              if (kernel_addr(sd.ld_row, sd.ldc, j, i, tb) != want_addr(sd.ld_row, x)) return "JIT load address != row map";
+              if (kernel_addr(sd.st_row, sd.stc, j, i, tb) != want_addr(sd.st_row, x)) return "JIT store address != row map";
+            }
+      }
       for (int o = sd.op_begin; o < sd.op_end; ++o) {
         const Op& op = P.ops[o];
         const uint32_t code = op_code(op.w0), a = op_a(op.w0), b = op_b(op.w0);
