@@ -115,6 +115,11 @@ constexpr int kHbmAdjointRegs = 3;
 // (few threads per sample would build them through serial global loads)
 constexpr int kSmemTablesMaxN = 10;
 constexpr int kHbmForwardRegs = 4;
+// complex64 HBM plans: 4 slots, both states per thread (float2 states need
+// half the registers), 12-qubit tiles; one program for both sweeps
+// (measured on cfg4: 36.4k -> 38.9k samples/s, profiles/r02/knobs_c8_complex64.log)
+constexpr int kHbmTileC64 = 12;
+constexpr int kHbmRegsC64 = 4;
 // on-chip JIT plans this small run 3 register slots with both states per
 // thread (measured: cfg2 158 -> 98 us, cfg1 52 -> 31 us per call); n = 11, 12
 // keep 4 slots on thread pairs (cfg3: 5.95 vs 6.40 ms). VQC_SMEM_DUAL=1 / 0
@@ -727,7 +732,7 @@ int check_common(const VqcPlan* p, const double* d_in, const double* d_w, int64_
 // the CPU-side JIT source dump)
 int schedule_circuit(const VqcCircuit* c, const int64_t* wrt_col, HostProgram* prog,
                      std::vector<uint32_t>* zmask = nullptr, std::vector<double>* zcoeff = nullptr,
-                     int tile_override = 0, int regs_override = 0) {
+                     int tile_override = 0, int regs_override = 0, int precision = 0) {
   std::vector<GateIn> gates((size_t)c->n_gates);
   for (int64_t g = 0; g < c->n_gates; ++g) {
     GateIn& gi = gates[g];
@@ -747,7 +752,9 @@ int schedule_circuit(const VqcCircuit* c, const int64_t* wrt_col, HostProgram* p
   for (int64_t i = 0; i < c->total_params; ++i) wcol[i] = wrt_col[i];
   if (zmask) prog->absorbed = absorb_trailing_gates(&gates, c->n_qubits, zmask, zcoeff);
   ScheduleOptions opt;
-  opt.tile_qubits = env_int("VQC_TILE_QUBITS", 11);
+  // HBM tiles: 2^11 complex128 amplitudes (32 KiB per state); complex64
+  // elements are half the size, so its tiles hold 2^12 (same bytes)
+  opt.tile_qubits = env_int("VQC_TILE_QUBITS", precision == 1 ? kHbmTileC64 : 11);
   opt.segment_cost = env_int("VQC_SEGMENT_COST", 4);
   opt.variants = std::max(1, env_int("VQC_SCHED_VARIANTS", 1));
   opt.forced_low = std::max(0, std::min(3, env_int("VQC_FORCED_LOW", 3)));  // contiguous low qubits per pass
@@ -757,7 +764,7 @@ int schedule_circuit(const VqcCircuit* c, const int64_t* wrt_col, HostProgram* p
   // interpreter kernels exist for R = 4 passes only.
   opt.reg_slots = 4;
   if (c->n_qubits > opt.smem_max_qubits && env_int("VQC_JIT", -1) != 0)
-    opt.reg_slots = std::max(3, std::min(4, env_int("VQC_REG_SLOTS", kHbmAdjointRegs)));
+    opt.reg_slots = std::max(3, std::min(4, env_int("VQC_REG_SLOTS", precision == 1 ? kHbmRegsC64 : kHbmAdjointRegs)));
   // small on-chip JIT plans: 3 slots, both states per thread (smem_dual)
   if (c->n_qubits <= opt.smem_max_qubits && smem_dual(c->n_qubits)) opt.reg_slots = 3;
   // HBM plans run JIT kernels, whose address maps take CNOT folds onto
@@ -833,10 +840,12 @@ int64_t vqc_jit_source(const VqcCircuit* c, const int64_t* wrt_col, int compile,
   HostProgram prog;
   std::vector<uint32_t> zm;  // as for Z-string observables (trailing gates absorbed)
   std::vector<double> zc;
-  if (int rc = schedule_circuit(c, wrt_col, &prog, &zm, &zc)) return rc;
-  if ((prog.hbm || (prog.R <= 3 && smem_dual(prog.n))) && env_int("VQC_ADJ_DUAL", prog.R <= 3 ? 1 : 0) != 0)
+  const int prec = env_int("VQC_JIT_SOURCE_PRECISION", 0) == 1 ? 1 : 0;  // dump / compile a complex64 plan
+  if (int rc = schedule_circuit(c, wrt_col, &prog, &zm, &zc, 0, 0, prec)) return rc;
+  if ((prog.hbm || (prog.R <= 3 && smem_dual(prog.n))) &&
+      env_int("VQC_ADJ_DUAL", (prog.R <= 3 || (prog.hbm && prec == 1)) ? 1 : 0) != 0)
     prog.adj_dual = true;
-  prog.precision = env_int("VQC_JIT_SOURCE_PRECISION", 0) == 1 ? 1 : 0;  // dump / compile a complex64 plan
+  prog.precision = prec;
   prog.pingpong = prog.hbm ? std::max(0, std::min(2, env_int("VQC_PINGPONG", 0))) : 0;
   build_thr_table(prog.segs);  // per-segment thread-table offsets, as at plan creation
   const bool split = use_split(prog.n, prog.R) && !prog.adj_dual;
@@ -955,7 +964,7 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
   // Z-only observables absorb the circuit's trailing CNOT / CZ / X gates
   // (G^dagger O G is again a Z string): fewer state passes, same results
   if (int rc = schedule_circuit(c, wrt_col, &p->prog, p->has_xy ? nullptr : &p->smask,
-                                p->has_xy ? nullptr : &p->tcoeff)) {
+                                p->has_xy ? nullptr : &p->tcoeff, 0, 0, precision)) {
     delete p;
     return rc;
   }
@@ -991,7 +1000,8 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
   if (want_jit && (P.n_fwd_ops + P.n_bwd_ops > 0 || precision == 1 || P.checks)) {
     // HBM adjoint with both states per thread when its register slots allow
     // (VQC_ADJ_DUAL overrides: 0 = thread pairs)
-    if ((P.hbm || (P.R <= 3 && smem_dual(P.n))) && env_int("VQC_ADJ_DUAL", P.R <= 3 ? 1 : 0) != 0)
+    if ((P.hbm || (P.R <= 3 && smem_dual(P.n))) &&
+        env_int("VQC_ADJ_DUAL", (P.R <= 3 || (P.hbm && precision == 1)) ? 1 : 0) != 0)
       p->prog.adj_dual = true;
     // HBM passes: ping-pong tile groups (VQC_PINGPONG=0 turns them off)
     // off by default: both modes measured slower than two free-running CTAs
