@@ -423,7 +423,21 @@ Layout make_layout(const VqcPlan* p, int64_t B, int mode) {
   return L;
 }
 
-int red_slots(const VqcPlan* p) { return std::max(1, std::max(p->M, p->prog.max_red_per_seg)); }
+// reduction slots of the shared-memory partial buffer (slots x threads
+// doubles). Per-warp reductions keep one row of the pass's slots per warp:
+// warps x max_red_per_pass doubles = (max_red_per_pass / 32) slots x threads.
+// JIT HBM adjoint passes with both states per thread reduce their gradient
+// partials per warp when the scheduler planned thread groups and a pass's
+// slots fit a small table (deep passes keep the per-segment CTA reductions)
+bool use_warp_red(const HostProgram& P) {
+  return P.hbm && P.group_sync && P.adj_dual && P.pingpong == 0 && P.max_red_per_pass <= 512;
+}
+
+int red_slots(const VqcPlan* p) {
+  int rs = std::max(1, std::max(p->M, p->prog.max_red_per_seg));
+  if (p->prog.warp_red) rs = std::max(rs, (p->prog.max_red_per_pass + 31) / 32);
+  return rs;
+}
 
 // bytes per state element: complex128 or complex64
 int elem_bytes(const VqcPlan* p) { return p->prog.precision == 1 ? 8 : 16; }
@@ -775,6 +789,10 @@ int schedule_circuit(const VqcCircuit* c, const int64_t* wrt_col, HostProgram* p
   const bool fwd_prog = tile_override > 0 || regs_override > 0;
   opt.fold_thread_targets = c->n_qubits > opt.smem_max_qubits && env_int("VQC_JIT", -1) != 0 &&
                             (ftt == 1 || (ftt == 2 && fwd_prog) || (ftt == 3 && !fwd_prog));
+  // thread-group barriers and per-warp reductions in the JIT HBM pass kernels
+  // (VQC_GROUP_SYNC=0: CTA barriers and per-segment CTA reductions as before)
+  opt.group_sync = c->n_qubits > opt.smem_max_qubits && env_int("VQC_JIT", -1) != 0 &&
+                   env_int("VQC_GROUP_SYNC", 1) != 0 && env_int("VQC_PINGPONG", 0) == 0;
   if (tile_override > 0) opt.tile_qubits = tile_override;
   if (regs_override > 0) opt.reg_slots = regs_override;
   const int absorbed = prog->absorbed;
@@ -847,6 +865,7 @@ int64_t vqc_jit_source(const VqcCircuit* c, const int64_t* wrt_col, int compile,
     prog.adj_dual = true;
   prog.precision = prec;
   prog.pingpong = prog.hbm ? std::max(0, std::min(2, env_int("VQC_PINGPONG", 0))) : 0;
+  prog.warp_red = use_warp_red(prog);
   build_thr_table(prog.segs);  // per-segment thread-table offsets, as at plan creation
   const bool split = use_split(prog.n, prog.R) && !prog.adj_dual;
   const std::string src = jit_source(prog, split);
@@ -1010,6 +1029,7 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
     const int pingpong = (P.hbm && P.n - P.k >= 1 && 2 * pass_smem(p, P, true) <= (size_t)kMaxSmemBytes)
                              ? pp_mode : 0;
     p->prog.pingpong = pingpong;
+    p->prog.warp_red = use_warp_red(p->prog);
     err = jit_build(P, use_split(P.n, P.R) && !P.adj_dual, &p->jit);
     if (!err.empty()) {
       vqc_plan_destroy(p);

@@ -978,6 +978,17 @@ __device__ __forceinline__ void seg_publish(const SegEnv& E, const SegCtx<R>& C,
   }
 }
 
+// timing ablations (wrong results; VQC_JIT_OPTS=-DVQC_ABL_WSYNC / -DVQC_ABL_NORED)
+#ifdef VQC_ABL_ALL
+#define VQC_ABL_WSYNC 1
+#define VQC_ABL_NORED 1
+#endif
+#ifdef VQC_ABL_WSYNC
+#define VQC_ABL_SYNC() __syncwarp()
+#else
+#define VQC_ABL_SYNC() vsync()
+#endif
+
 // segment end: register store (through the folded store map), barrier, and the
 // segment's gradient outputs
 template <int R, int MODE, bool REDUCE = true, class SD>
@@ -986,7 +997,7 @@ __device__ __forceinline__ void seg_end(const SegEnv& E, const SD& sd, const Reg
   const Group& grp = E.grp;
   const RunArgs& A = E.A;
   phase_b();  // ping-pong hand-over point
-  if ((MODE == MODE_SPLIT && sd.ip_count() > 0) || sd.st_sync()) vsync();  // partners / other cells done reading
+  if ((MODE == MODE_SPLIT && sd.ip_count() > 0) || sd.st_sync()) VQC_ABL_SYNC();  // partners / other cells done reading
   asm volatile("" ::: "memory");  // keep the store map's loads and math after the op loop
   if (E.active) {
     uint32_t sp0, sc[R];
@@ -1011,7 +1022,10 @@ __device__ __forceinline__ void seg_end(const SegEnv& E, const SD& sd, const Reg
       if constexpr (MODE == MODE_DUAL) E.s_phi[ad] = f[i];
     }
   }
-  vsync();
+  VQC_ABL_SYNC();
+#ifdef VQC_ABL_NORED
+  return;
+#endif
   if constexpr (MODE != MODE_FWD && REDUCE) {
     const int nout = sd.ip_count();
     if (nout > 0) {
@@ -1053,6 +1067,177 @@ __device__ __forceinline__ void seg_end(const SegEnv& E, const SD& sd, const Reg
         if (bl < A.nb) A.ip[(((bl * A.K) + E.bra) * E.D.NG + io.gslot) * E.n_tiles + E.tile] = v;
       }
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Thread-group barriers and per-warp reductions (JIT HBM pass kernels; the
+// scheduler's assign_thread_groups plans the thread-index bits).
+//
+// group_sync(t): barrier over the blockDim >> t threads that share the top t
+// thread-index bits (t = 0: the CTA; a warp or less: __syncwarp). Named
+// barriers 2^t - 1 + group index (levels 1..3 use ids 1..14).
+__device__ __forceinline__ void group_sync(int t) {
+  const unsigned g = vdim() >> t;
+  if (t <= 0) {
+    vsync();
+  } else if (g <= 32u) {
+    __syncwarp();
+  } else {
+    const unsigned id = (1u << t) - 1u + vtid() / g;
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(g) : "memory");
+  }
+}
+
+// segment end with a group barrier: register store through the folded store
+// map, then the barrier the next segment's loads need (sd.sync_st top bits
+// shared). Gradient partials are reduced per warp (warp_reduce_store), so no
+// reduction phases follow.
+template <int R, int MODE, class SD>
+__device__ __forceinline__ void seg_end_g(const SegEnv& E, const SD& sd, const Regs<R>& a, const Regs<R>& f) {
+  constexpr int N = 1 << R;
+  const Group& grp = E.grp;
+  if (sd.st_sync()) group_sync(sd.sync_self());  // the group's loads are done before its cells are overwritten
+  asm volatile("" ::: "memory");
+  uint32_t sp0, sc[R];
+  sp0 = SD::thr_sp0((uint32_t)grp.gi & ((1u << sd.nthr()) - 1u));
+  if (E.tile_base != 0) sp0 ^= sd.tile_st(E.tile_base);
+  asm volatile("" : "+r"(sp0));
+#pragma unroll
+  for (int t = 0; t < R; ++t) sc[t] = sd.stc(t);
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    uint32_t ad = sp0;
+#pragma unroll
+    for (int s = 0; s < R; ++s)
+      if ((i >> s) & 1) ad ^= sc[s];
+    VQC_CHECK(E.A, ad < (1u << E.D.k), CHK_SEG_STORE);
+    E.own[ad] = a[i];
+    if constexpr (MODE == MODE_DUAL) E.s_phi[ad] = f[i];
+  }
+  group_sync(sd.sync_st());
+}
+
+// Deterministic warp reduction of N per-thread partials by recursive halving:
+// at lane bit B the lanes with the bit clear keep the lower half of the
+// values and send the upper half to their partner (and vice versa), so after
+// the five steps each value's total sits in the lanes of one group; values
+// beyond nv (padding of odd halves) are zero. The representative lane writes
+// dst[index]. 2 * (N/2 + N/4 + ...) + ... shuffles instead of 5 per value.
+template <int N, int BIT>
+__device__ __forceinline__ void warp_reduce_rec(const double (&v)[N], unsigned lane, int base, int nv, double* dst) {
+  if constexpr (BIT < 0) {
+    static_assert(N == 1, "at most 32 values per warp reduction");
+    if (nv > 0) dst[base] = v[0];
+  } else if constexpr (N == 1) {
+    double x[1] = {v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1 << BIT)};
+    // all lanes of the pair hold the same total; the one with the bit clear goes on
+    warp_reduce_rec<1, BIT - 1>(x, lane, base, ((lane >> BIT) & 1u) ? 0 : nv, dst);
+  } else {
+    constexpr int H = (N + 1) / 2;
+    const bool up = ((lane >> BIT) & 1u) != 0u;
+    double w[H];
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      const double lo = v[i], hi = (i + H < N) ? v[i + H] : 0.0;
+      const double send = up ? lo : hi, keep = up ? hi : lo;
+      w[i] = keep + __shfl_xor_sync(0xffffffffu, send, 1 << BIT);
+    }
+    const int nlo = nv < H ? nv : H;
+    warp_reduce_rec<H, BIT - 1>(w, lane, base + (up ? H : 0), up ? nv - nlo : nlo, dst);
+  }
+}
+// The same reduction in stages the JIT weaves between a segment's gate
+// blocks, so each round's shuffle latency hides behind FP64 work instead of
+// stalling the warp five times: wr_split sends this round's halves (base / nv
+// track which value indices the lane still holds), wr_join adds what arrived.
+template <int N, int BIT>
+__device__ __forceinline__ void wr_split(const double (&v)[N], unsigned lane, double (&keep)[(N + 1) / 2],
+                                         double (&recv)[(N + 1) / 2], int& base, int& nv) {
+  const bool up = ((lane >> BIT) & 1u) != 0u;
+  if constexpr (N == 1) {
+    keep[0] = v[0];
+    recv[0] = __shfl_xor_sync(0xffffffffu, v[0], 1 << BIT);
+    if (up) nv = 0;  // both lanes of the pair hold the same total; the lower one goes on
+  } else {
+    constexpr int H = (N + 1) / 2;
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      const double lo = v[i], hi = (i + H < N) ? v[i + H] : 0.0;
+      const double send = up ? lo : hi;
+      keep[i] = up ? hi : lo;
+      recv[i] = __shfl_xor_sync(0xffffffffu, send, 1 << BIT);
+    }
+    const int nlo = nv < H ? nv : H;
+    base += up ? H : 0;
+    nv = up ? nv - nlo : nlo;
+  }
+}
+template <int H>
+__device__ __forceinline__ void wr_join(const double (&keep)[H], const double (&recv)[H], double (&w)[H]) {
+#pragma unroll
+  for (int i = 0; i < H; ++i) w[i] = keep[i] + recv[i];
+}
+
+// dst: this warp's slots [0, N) of the pass-wide partial table
+template <int N>
+__device__ __forceinline__ void warp_reduce_store(const double (&v)[N], double* dst) {
+  const unsigned lane = vtid() & 31u;
+  if constexpr (N <= 16) {
+    warp_reduce_rec<N, 4>(v, lane, 0, N, dst);
+  } else {
+    double a[16], b[N - 16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = v[i];
+#pragma unroll
+    for (int i = 16; i < N; ++i) b[i - 16] = v[i];
+    warp_reduce_rec<16, 4>(a, lane, 0, 16, dst);
+    warp_reduce_store<N - 16>(b, dst + 16);
+  }
+}
+
+// inner products into per-thread partials (both states in registers)
+template <int R, int S>
+__device__ __forceinline__ void jop_ip3w(const Regs<R>& a, const Regs<R>& f, double& ix, double& iy, double& iz) {
+  ix = iy = iz = 0.0;
+  auto ra = [&](int i) { return a[i]; };
+  auto rf = [&](int i) { return f[i]; };
+  ip_xyz<R, S, -1>(ra, rf, ix, iy, iz);
+}
+template <int R, int KIND, int S>
+__device__ __forceinline__ double jop_ipxyw(const Regs<R>& a, const Regs<R>& f) {
+  auto ra = [&](int i) { return a[i]; };
+  auto rf = [&](int i) { return f[i]; };
+  if constexpr (KIND == 0) return ip_x<R, S, -1>(ra, rf);
+  else return ip_y<R, S, -1>(ra, rf);
+}
+template <int R>
+__device__ __forceinline__ double jop_ipzw(const Regs<R>& a, const Regs<R>& f, uint32_t m, bool cb) {
+  auto ra = [&](int i) { return a[i]; };
+  auto rf = [&](int i) { return f[i]; };
+  return ip_z<R, -1>(ra, rf, m, cb);
+}
+
+// End of a pass's adjoint segments: sum each reduction slot over the warps in
+// warp order and write the pass's gradient outputs. tab rows: (gradient slot,
+// pass-relative reduction slot, pass-relative block gradient vector or -1).
+// The caller's last group barrier (the CTA) ordered the partial table.
+__device__ __forceinline__ void wred_outputs(const SegEnv& E, const int (*tab)[3], int count, int wstride) {
+  const RunArgs& A = E.A;
+  const int nw = (int)(vdim() >> 5);
+  for (int oi = (int)vtid(); oi < count; oi += (int)vdim()) {
+    const int gslot = tab[oi][0], red = tab[oi][1], avec = tab[oi][2];
+    const int nr = avec < 0 ? 1 : 3;
+    double r[3] = {0.0, 0.0, 0.0};
+    for (int w = 0; w < nw; ++w)
+      for (int j = 0; j < nr; ++j) r[j] += E.s_red[w * wstride + red + j];
+    double v = r[0];
+    if (avec >= 0) {
+      const double* av = E.s_av_all + 4 * avec;
+      v = av[0] * r[0] + av[1] * r[1] + av[2] * r[2];
+    }
+    VQC_CHECK(A, gslot >= 0 && gslot < E.D.NG && E.tile < E.n_tiles, CHK_IP_OUT);
+    if (E.bl0 < A.nb) A.ip[(((E.bl0 * A.K) + E.bra) * E.D.NG + gslot) * E.n_tiles + E.tile] = v;
   }
 }
 

@@ -123,6 +123,13 @@ struct SegDesc {
   // rows (thread bases and tile translations).
   uint32_t ld_row[kMaxTile], st_row[kMaxTile];
   int8_t gen;
+  // Thread-group synchronisation (scheduler.cpp assign_thread_groups; JIT HBM
+  // plans): the top sync_ld / sync_st thread-index bits sit on the same tile
+  // positions as in the previous / next segment of the sweep and the folded
+  // maps leave them alone, so that boundary only needs a barrier over
+  // blockDim >> t threads; sync_self: top bits untouched by this segment's own
+  // load and store maps (the barrier between its loads and stores).
+  int8_t sync_ld, sync_st, sync_self;
 };
 
 // Per (segment, thread group) precomputed addressing: thread-bit part of

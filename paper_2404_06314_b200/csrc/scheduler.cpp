@@ -12,6 +12,7 @@
 #include "scheduler.h"
 
 #include <algorithm>
+#include <functional>
 #include <cstdio>
 
 namespace vqc {
@@ -185,6 +186,112 @@ std::vector<Group> greedy_groups(const std::vector<int>& todo, const std::vector
   return groups;
 }
 
+// Thread-group synchronisation (JIT HBM plans). A segment boundary is a
+// shared-memory transpose; the threads that exchange data are those that agree
+// on every tile position which is a thread bit on both sides. If the top t
+// thread-index bits of two consecutive segments sit on the same tile positions
+// (same order) and the folded CNOT maps leave those positions alone, a group
+// of blockDim >> t threads stores exactly the cells it loads next: the
+// boundary needs a barrier over that group only (a warp: __syncwarp), and
+// groups drift apart so shared-memory phases of one overlap arithmetic of
+// another. Dynamic programme over the segments of a pass: states are ordered
+// choices of the top T positions, cost per boundary = other warps waited for.
+void assign_thread_groups(std::vector<SegDesc>& segs, const PassDesc& pd, int k) {
+  const int m = (int)segs.size();
+  const int nthr = segs[0].nthr;
+  const int T = std::min(3, std::max(0, nthr - 5));  // thread bits above the lane bits that are planned
+  auto ident = [&](const uint32_t* row, int p) { return row[p] == (1u << pd.local_q[p]); };
+  auto finish = [&](SegDesc& sd, const std::vector<int>& top) {
+    // lane bits: the first three cover distinct residues mod 3 (bank groups
+    // under the mod-3 fold swizzle), then the rest ascending; top bits last
+    std::vector<int> rest;
+    for (int i = 0; i < sd.nthr; ++i)
+      if (std::find(top.begin(), top.end(), (int)sd.thr_l[i]) == top.end()) rest.push_back(sd.thr_l[i]);
+    std::sort(rest.begin(), rest.end());
+    std::vector<int> order;
+    for (int r = 0; r < 3; ++r)
+      for (size_t i = 0; i < rest.size(); ++i)
+        if (rest[i] >= 0 && rest[i] % 3 == r) { order.push_back(rest[i]); rest[i] = -1; break; }
+    for (int p : rest)
+      if (p >= 0) order.push_back(p);
+    for (int i = (int)top.size() - 1; i >= 0; --i) order.push_back(top[i]);  // top[0] = highest bit
+    for (size_t i = 0; i < order.size(); ++i) {
+      sd.thr_l[i] = (int8_t)order[i];
+      sd.thr_g[i] = pd.local_q[order[i]];
+      sd.tsw[i] = (uint16_t)swz_index(1u << order[i]);
+    }
+  };
+  if (T == 0) {
+    for (SegDesc& sd : segs) sd.sync_ld = sd.sync_st = sd.sync_self = 0;
+    return;
+  }
+  // candidate states per segment: ordered T-tuples of its thread positions (top bit first)
+  std::vector<std::vector<std::vector<int>>> states(m);
+  for (int i = 0; i < m; ++i) {
+    std::vector<int> pos;
+    for (int t = 0; t < segs[i].nthr; ++t) pos.push_back(segs[i].thr_l[t]);
+    std::sort(pos.begin(), pos.end());
+    std::vector<int> cur;
+    std::function<void()> rec = [&]() {
+      if ((int)cur.size() == T) {
+        // keep one residue of each class among the lane bits when possible
+        int have = 0, all = 0;
+        for (int p : pos) {
+          all |= 1 << (p % 3);
+          if (std::find(cur.begin(), cur.end(), p) == cur.end()) have |= 1 << (p % 3);
+        }
+        if (have == all) states[i].push_back(cur);
+        return;
+      }
+      for (int p : pos)
+        if (std::find(cur.begin(), cur.end(), p) == cur.end()) {
+          cur.push_back(p);
+          rec();
+          cur.pop_back();
+        }
+    };
+    rec();
+    if (states[i].empty()) {  // no residue-complete choice: take any
+      cur.assign(pos.end() - T, pos.end());
+      states[i].push_back(cur);
+    }
+  }
+  // level of boundary i -> i + 1 for states a, b: common top prefix on identity rows
+  auto level = [&](int i, const std::vector<int>& a, const std::vector<int>& b) {
+    int t = 0;
+    while (t < T && a[t] == b[t] && ident(segs[i].st_row, a[t]) && ident(segs[i + 1].ld_row, a[t])) ++t;
+    return t;
+  };
+  auto cost_of = [&](int t) { return (1 << (T - t)) - 1; };
+  std::vector<std::vector<int>> best(m), from(m);
+  best[0].assign(states[0].size(), 0);
+  from[0].assign(states[0].size(), -1);
+  for (int i = 1; i < m; ++i) {
+    best[i].assign(states[i].size(), 1 << 30);
+    from[i].assign(states[i].size(), 0);
+    for (size_t b = 0; b < states[i].size(); ++b)
+      for (size_t a = 0; a < states[i - 1].size(); ++a) {
+        const int c = best[i - 1][a] + cost_of(level(i - 1, states[i - 1][a], states[i][b]));
+        if (c < best[i][b]) { best[i][b] = c; from[i][b] = (int)a; }
+      }
+  }
+  int cur = (int)(std::min_element(best[m - 1].begin(), best[m - 1].end()) - best[m - 1].begin());
+  std::vector<int> pick(m);
+  for (int i = m - 1; i >= 0; --i) {
+    pick[i] = cur;
+    cur = from[i][cur];
+  }
+  for (int i = 0; i < m; ++i) {
+    const std::vector<int>& top = states[i][pick[i]];
+    finish(segs[i], top);
+    segs[i].sync_ld = i > 0 ? (int8_t)level(i - 1, states[i - 1][pick[i - 1]], top) : 0;
+    segs[i].sync_st = i + 1 < m ? (int8_t)level(i, top, states[i + 1][pick[i + 1]]) : 0;
+    int t = 0;
+    while (t < T && ident(segs[i].ld_row, top[t]) && ident(segs[i].st_row, top[t])) ++t;
+    segs[i].sync_self = (int8_t)t;
+  }
+}
+
 uint32_t enc(uint32_t code, uint32_t a, uint32_t b, uint32_t ipl, bool adj) {
   return code | (a << 5) | (b << 11) | (ipl << 17) | (adj ? (1u << 31) : 0u);
 }
@@ -226,6 +333,7 @@ std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total
   *P = HostProgram();
   P->n = n;
   P->hbm = n > opt.smem_max_qubits;
+  P->group_sync = opt.group_sync && P->hbm;
   P->k = P->hbm ? std::min(opt.tile_qubits, n) : n;
   P->R = std::min(opt.reg_slots, P->k);
   if (P->hbm && P->k < opt.forced_low + 1) return "tile too small";
@@ -550,6 +658,21 @@ std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total
       fwd_items.push_back(std::move(grouped));
     }
     pd.seg_end = (int)P->segs.size();
+    if (P->group_sync && !fwd_descs.empty()) {
+      assign_thread_groups(fwd_descs, pd, k);
+      for (size_t i = 0; i < fwd_descs.size(); ++i) {
+        SegDesc& dst = P->segs[(size_t)pd.seg_begin + i];
+        const SegDesc& src = fwd_descs[i];
+        for (int t = 0; t < kMaxQubits; ++t) {
+          dst.thr_l[t] = src.thr_l[t];
+          dst.thr_g[t] = src.thr_g[t];
+          dst.tsw[t] = src.tsw[t];
+        }
+        dst.sync_ld = src.sync_ld;
+        dst.sync_st = src.sync_st;
+        dst.sync_self = src.sync_self;
+      }
+    }
     pd.rot_end = next_rot;
     pd.blk_end = (int)P->blocks.size();
     pd.av_end = P->n_av;
@@ -568,6 +691,7 @@ std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total
         std::swap(sd.ldc[s2], sd.stc[s2]);
       }
       for (int p2 = 0; p2 < kMaxTile; ++p2) std::swap(sd.ld_row[p2], sd.st_row[p2]);
+      std::swap(sd.sync_ld, sd.sync_st);  // the adjoint sweep meets the boundaries in reverse
       int slot_of[kMaxQubits];
       for (int q = 0; q < kMaxQubits; ++q) slot_of[q] = -1;
       for (int s2 = 0; s2 < sd.nreg; ++s2) slot_of[(int)sd.reg_g[s2]] = s2;
@@ -677,6 +801,11 @@ std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total
       P->segs.push_back(sd);
     }
     pd.bseg_end = (int)P->segs.size();
+    {
+      int pass_red = 0;
+      for (int s2 = pd.bseg_begin; s2 < pd.bseg_end; ++s2) pass_red += P->segs[s2].red_count;
+      P->max_red_per_pass = std::max(P->max_red_per_pass, pass_red);
+    }
     P->passes.push_back(pd);
   }
   P->n_rot = next_rot;

@@ -13,6 +13,7 @@
 #include <array>
 #include <cmath>
 #include <cstdio>
+#include <algorithm>
 #include <complex>
 #include <cstring>
 #include <string>
@@ -189,6 +190,58 @@ std::string check_program(const HostProgram& P, const ScheduleOptions& opt) {
       }
       return "";
     };
+    // Thread-group barriers (scheduler.cpp assign_thread_groups): a boundary
+    // with sync level t is synchronised over the groups of threads sharing
+    // the top t thread-index bits only, so every such group must store
+    // exactly the shared-memory cells it loads in the next segment (and load
+    // / store the same cells inside a segment whose stores leave the loading
+    // threads' cells, level sync_self).
+    if (opt.group_sync) {
+      const uint32_t nmask = (P.n >= 32) ? 0xffffffffu : ((1u << P.n) - 1u);
+      const uint32_t tile_mask = ~pd.local_mask & nmask;
+      auto cells = [&](const SegDesc& sd, const uint32_t* row, int t, uint32_t grp, uint32_t tb) {
+        std::vector<uint32_t> out;
+        const int low = sd.nthr - t;
+        for (uint32_t g = 0; g < (1u << sd.nthr); ++g) {
+          if (t > 0 && (g >> low) != grp) continue;
+          for (uint32_t i = 0; i < (1u << sd.nreg); ++i) {
+            uint32_t x = tb;
+            for (int b = 0; b < sd.nthr; ++b) x |= ((g >> b) & 1u) << sd.thr_g[b];
+            for (int b = 0; b < sd.nreg; ++b) x |= ((i >> b) & 1u) << sd.reg_g[b];
+            uint32_t v = 0;
+            for (int q = 0; q < P.k && q < kMaxTile; ++q) v |= (uint32_t)(__builtin_popcount(x & row[q]) & 1) << q;
+            out.push_back(swz_index(v));
+          }
+        }
+        std::sort(out.begin(), out.end());
+        return out;
+      };
+      const uint32_t tiles[3] = {0u, tile_mask, tile_mask & 0x5555u};
+      auto check_sweep = [&](int sb, int se) -> std::string {
+        for (int s = sb; s < se; ++s) {
+          const SegDesc& a = P.segs[s];
+          if (s == sb && a.sync_ld != 0) return "first segment of a sweep must load behind a CTA barrier";
+          if (s + 1 == se && a.sync_st != 0) return "last segment of a sweep must store before a CTA barrier";
+          for (uint32_t tb : tiles) {
+            if (a.gen && a.sync_self > 0)
+              for (uint32_t grp = 0; grp < (1u << a.sync_self); ++grp)
+                if (cells(a, a.ld_row, a.sync_self, grp, tb) != cells(a, a.st_row, a.sync_self, grp, tb))
+                  return "thread group loads and stores different cells (sync_self)";
+            if (s + 1 < se) {
+              const SegDesc& b = P.segs[s + 1];
+              if (a.sync_st != b.sync_ld) return "sync_st / sync_ld of a boundary disagree";
+              for (uint32_t grp = 0; grp < (1u << a.sync_st); ++grp)
+                if (cells(a, a.st_row, a.sync_st, grp, tb) != cells(b, b.ld_row, b.sync_ld, grp, tb))
+                  return "thread group stores cells another group loads next";
+            }
+          }
+        }
+        return "";
+      };
+      std::string e = check_sweep(pd.seg_begin, pd.seg_end);
+      if (e.empty()) e = check_sweep(pd.bseg_begin, pd.bseg_end);
+      if (!e.empty()) return e;
+    }
     for (int s = pd.seg_begin; s < pd.seg_end; ++s) {
       std::string e = check_seg(P.segs[s]);
       if (!e.empty()) return e;
@@ -236,6 +289,8 @@ int sim_run(int n, int64_t G, const int64_t* kinds, const int64_t* q0, const int
   {
     const char* ft = getenv("VQC_FOLD_THREAD_TARGETS");
     opt.fold_thread_targets = n > smem_max_qubits && !(ft && ft[0] == '0');
+    const char* gs = getenv("VQC_GROUP_SYNC");  // thread-group barriers, as JIT HBM plans
+    opt.group_sync = n > smem_max_qubits && !(gs && gs[0] == '0');
   }
   // as vqc_plan_create: trailing CNOT / CZ / X gates fold into the (Z-string)
   // observables, which the expectation step below then uses
@@ -511,6 +566,8 @@ int sim_dump(int n, int64_t G, const int64_t* kinds, const int64_t* q0, const in
   {
     const char* ft = getenv("VQC_FOLD_THREAD_TARGETS");
     opt.fold_thread_targets = n > smem_max_qubits && !(ft && ft[0] == '0');
+    const char* gs = getenv("VQC_GROUP_SYNC");  // thread-group barriers, as JIT HBM plans
+    opt.group_sync = n > smem_max_qubits && !(gs && gs[0] == '0');
   }
   HostProgram P;
   std::string e = build_program(gates, n, total_params, wc, opt, &P);
