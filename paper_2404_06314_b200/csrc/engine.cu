@@ -866,6 +866,7 @@ int64_t vqc_jit_source(const VqcCircuit* c, const int64_t* wrt_col, int compile,
   prog.precision = prec;
   prog.pingpong = prog.hbm ? std::max(0, std::min(2, env_int("VQC_PINGPONG", 0))) : 0;
   prog.warp_red = use_warp_red(prog);
+  prog.direct_io = prog.hbm && prog.group_sync && prog.pingpong == 0 && env_int("VQC_DIRECT_IO", 0) != 0;
   build_thr_table(prog.segs);  // per-segment thread-table offsets, as at plan creation
   const bool split = use_split(prog.n, prog.R) && !prog.adj_dual;
   const std::string src = jit_source(prog, split);
@@ -1030,6 +1031,7 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
                              ? pp_mode : 0;
     p->prog.pingpong = pingpong;
     p->prog.warp_red = use_warp_red(p->prog);
+    p->prog.direct_io = P.hbm && P.group_sync && pingpong == 0 && env_int("VQC_DIRECT_IO", 0) != 0;
     err = jit_build(P, use_split(P.n, P.R) && !P.adj_dual, &p->jit);
     if (!err.empty()) {
       vqc_plan_destroy(p);
@@ -1052,6 +1054,7 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
       f->prog.checks = P.checks;
       f->prog.pingpong = (f->prog.n - f->prog.k >= 1 && 2 * pass_smem(p, f->prog, false) <= (size_t)kMaxSmemBytes)
                              ? pingpong : 0;
+      f->prog.direct_io = f->prog.hbm && f->prog.group_sync && f->prog.pingpong == 0 && env_int("VQC_DIRECT_IO", 0) != 0;
       if (!f->prog.hbm || f->prog.NG != P.NG) {
         vqc_plan_destroy(p);
         return fail(VQC_E_UNSUPPORTED, "forward schedule disagrees with the adjoint schedule");

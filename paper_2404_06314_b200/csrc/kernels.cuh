@@ -870,7 +870,19 @@ struct SegEnv {
   int bra, tile, n_tiles;
   cplx_t* own;
   const cplx_t* partner;
+  // direct tile I/O of the first / last segment of a sweep (JIT HBM passes)
+  uint32_t io = 0;
+  cplx_t* g_psi = nullptr;  // this row's states in HBM
+  cplx_t* g_phi = nullptr;
 };
+
+// SegEnv::io. The first segment of a pass's sweep can take its registers
+// straight from HBM (IO_LD) or set them to |0...0> (IO_INIT) and the last one
+// can store them straight back (IO_ST) or drop them (IO_NOST: nothing reads
+// the states after the adjoint sweep's last pass): the tile then crosses
+// shared memory only between segments, half the shared-memory traffic of a
+// three-segment pass, and warps start as soon as their own elements arrive.
+enum { IO_LD = 1u, IO_INIT = 2u, IO_ST = 4u, IO_NOST = 8u };
 
 template <int MODE>
 __device__ __forceinline__ SegEnv make_env(const DevProgram& D, const RunArgs& A, cplx_t* s_psi, cplx_t* s_phi,
@@ -1118,6 +1130,79 @@ __device__ __forceinline__ void seg_end_g(const SegEnv& E, const SD& sd, const R
   group_sync(sd.sync_st());
 }
 
+__device__ __forceinline__ void cp_async_wait_all_();
+
+// First segment of a sweep: registers from HBM (IO_LD), the initial state
+// (IO_INIT) or shared memory. The global index of register element i is the
+// folded load map applied to (thread bits | register bits | tile bits),
+// deposited on the pass's local qubits: GF(2)-linear like the shared-memory
+// address, so base ^ XOR of per-register-bit columns (SD::thr_gl, tile_gl,
+// gcol_l). The per-sample tables (cp.async in pass_body) are awaited here,
+// after the loads are in flight; that CTA barrier also orders these loads
+// before any thread's direct stores to the same cells at the end of the pass.
+template <int R, int MODE, class SD>
+__device__ __forceinline__ void seg_begin_io(const SegEnv& E, const SD& sd, SegCtx<R>& C, Regs<R>& a, Regs<R>& f) {
+  constexpr int N = 1 << R;
+  if (!(E.io & (IO_LD | IO_INIT))) {
+    seg_begin<R, MODE>(E, sd, C, a, f);
+    return;
+  }
+  const uint32_t gi = (uint32_t)E.grp.gi & ((1u << sd.nthr()) - 1u);
+  C.own = E.own;
+  C.partner = E.partner;
+  C.J0 = E.tile_base | SD::thr_j0(gi);
+  C.lp0 = 0;
+#pragma unroll
+  for (int t = 0; t < R; ++t) C.lc[t] = 0;
+  if (E.io & IO_INIT) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      a[i] = mk_c((C.J0 == 0u && i == 0) ? 1 : 0, 0);
+      if constexpr (MODE == MODE_DUAL) f[i] = mk_c(0, 0);
+    }
+  } else {
+    uint32_t gb = E.tile_base | SD::thr_gl(gi);
+    if (E.tile_base != 0) gb ^= SD::tile_gl(E.tile_base);
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      uint32_t idx = gb;
+#pragma unroll
+      for (int s2 = 0; s2 < R; ++s2)
+        if ((i >> s2) & 1) idx ^= SD::gcol_l(s2);
+      VQC_CHECK(E.A, idx < (1u << E.D.n), CHK_TILE_GLOBAL);
+      a[i] = E.g_psi[idx];  // through L1: 16-byte pieces of one sector merge there
+      if constexpr (MODE == MODE_DUAL) f[i] = E.g_phi[idx];
+    }
+  }
+  cp_async_wait_all_();
+  vsync();
+}
+
+// Last segment of a sweep: registers straight to HBM (IO_ST), nowhere
+// (IO_NOST) or to shared memory behind a CTA barrier.
+template <int R, int MODE, class SD>
+__device__ __forceinline__ void seg_end_io(const SegEnv& E, const SD& sd, const Regs<R>& a, const Regs<R>& f) {
+  constexpr int N = 1 << R;
+  if (E.io & IO_NOST) return;
+  if (!(E.io & IO_ST)) {
+    seg_end_g<R, MODE>(E, sd, a, f);
+    return;
+  }
+  const uint32_t gi = (uint32_t)E.grp.gi & ((1u << sd.nthr()) - 1u);
+  uint32_t gb = E.tile_base | SD::thr_gs(gi);
+  if (E.tile_base != 0) gb ^= SD::tile_gs(E.tile_base);
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    uint32_t idx = gb;
+#pragma unroll
+    for (int s2 = 0; s2 < R; ++s2)
+      if ((i >> s2) & 1) idx ^= SD::gcol_s(s2);
+    VQC_CHECK(E.A, idx < (1u << E.D.n), CHK_TILE_GLOBAL);
+    __stcg(E.g_psi + idx, a[i]);
+    if constexpr (MODE == MODE_DUAL) __stcg(E.g_phi + idx, f[i]);
+  }
+}
+
 // Deterministic warp reduction of N per-thread partials by recursive halving:
 // at lane bit B the lanes with the bit clear keep the lower half of the
 // values and send the upper half to their partner (and vice versa), so after
@@ -1285,6 +1370,8 @@ __device__ __forceinline__ void jred_phase2(const SegEnv& E, const SD& sd, int f
 struct RtPassMap;  // pass index maps (defined with the tile walk below)
 struct InterpSegs {
   using PM = RtPassMap;
+  // tiles always staged through shared memory
+  static constexpr bool kDioF = false, kDioB = false, kDioFL = false, kDioFS = false, kDioBL = false, kDioBS = false;
   template <int R, int MODE>
   __device__ __forceinline__ static void run(const SegEnv& E, const SampleTables& T, int sb, int se) {
     const DevProgram& D = E.D;

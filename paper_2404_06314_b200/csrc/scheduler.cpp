@@ -208,6 +208,9 @@ void assign_thread_groups(std::vector<SegDesc>& segs, const PassDesc& pd, int k)
     for (int i = 0; i < sd.nthr; ++i)
       if (std::find(top.begin(), top.end(), (int)sd.thr_l[i]) == top.end()) rest.push_back(sd.thr_l[i]);
     std::sort(rest.begin(), rest.end());
+    // (positions 0-2, the tile's contiguous 128 bytes in HBM, have distinct
+    // residues and sort first: as the lowest lane bits they also make the
+    // first / last segment's direct HBM accesses coalesce)
     std::vector<int> order;
     for (int r = 0; r < 3; ++r)
       for (size_t i = 0; i < rest.size(); ++i)
@@ -240,7 +243,12 @@ void assign_thread_groups(std::vector<SegDesc>& segs, const PassDesc& pd, int k)
           all |= 1 << (p % 3);
           if (std::find(cur.begin(), cur.end(), p) == cur.end()) have |= 1 << (p % 3);
         }
-        if (have == all) states[i].push_back(cur);
+        // the segments that open / close a sweep exchange registers with HBM
+        // directly: keep positions 0-2 among their lane bits (coalescing)
+        bool low_top = false;
+        if (i == 0 || i + 1 == m)
+          for (int p : cur) low_top = low_top || p < 3;
+        if (have == all && !low_top) states[i].push_back(cur);
         return;
       }
       for (int p : pos)
@@ -364,6 +372,7 @@ std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total
 
   std::vector<int> rot_id(G, -1), gslot(G, -1);
   int next_rot = 0, next_g = 0;
+  uint32_t touched = 0;  // qubits some scheduled operation has acted on so far
 
   for (size_t pi = 0; pi < passes.size(); ++pi) {
     Group& pg = passes[pi];
@@ -417,6 +426,12 @@ std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total
       std::vector<int> gates;
       int id = -1;            // block id / diag-run id / packed set ids
       std::vector<Item> sub;  // blocks of a set
+      // first operation on its qubit in the whole schedule: the adjoint sweep
+      // needs its inner products but not its un-apply (nothing later in the
+      // reverse sweep acts on that qubit, and operators on the other qubits
+      // commute with it, so leaving U on both psi and phi changes no later
+      // inner product)
+      bool dead = false;
     };
     pd.seg_begin = (int)P->segs.size();
     std::vector<SegDesc> fwd_descs;
@@ -494,6 +509,21 @@ std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total
         if (gi.kind == G_CNOT) open_blk[gi.q0] = open_blk[gi.q1] = -1;
         items.push_back({0, {g}});
       }
+      // items in execution order: flag 1q items that open their qubit
+      if (opt.skip_dead_unapply)
+        for (Item& it : items) {
+          uint32_t qs = 0;
+          bool one_q = true;
+          for (int g : it.gates) {
+            qs |= 1u << gates[g].q0;
+            if (gates[g].kind == G_CNOT || gates[g].kind == G_CZ) {
+              qs |= 1u << gates[g].q1;
+              one_q = false;
+            }
+          }
+          it.dead = one_q && (qs & touched) == 0u;
+          touched |= qs;
+        }
       // leading / trailing CNOT runs fold into the load / store address maps
       auto is_cnot = [&](const Item& it) { return it.type == 0 && gates[it.gates[0]].kind == G_CNOT; };
       size_t lead = 0;
@@ -748,15 +778,27 @@ std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total
             }
             nred += 3 * __builtin_popcount(gmask);
           }
-          uint32_t smask = 0;
-          for (const Item& sub : it.sub) smask |= 1u << slot_of[gates[sub.gates[0]].q0];
-          op.w0 = enc(OP_U2SET, 0, smask, 0, true);
-          op.param = (uint32_t)it.id;
+          uint32_t smask = 0, live = 0;
+          for (const Item& sub : it.sub) {
+            smask |= 1u << slot_of[gates[sub.gates[0]].q0];
+            if (!sub.dead) live |= 1u << slot_of[gates[sub.gates[0]].q0];
+          }
+          if (live == 0u) continue;  // every block of the set opens its qubit: nothing to un-apply
+          int set_id = it.id;
+          if (live != smask) {  // un-apply the live blocks only: its own id row
+            set_id = (int)(P->setids.size() / kMaxR);
+            P->setids.resize(P->setids.size() + kMaxR, (int16_t)-1);
+            for (int sl = 0; sl < kMaxR; ++sl)
+              if (live >> sl & 1u) P->setids[(size_t)set_id * kMaxR + sl] = P->setids[(size_t)it.id * kMaxR + sl];
+          }
+          op.w0 = enc(OP_U2SET, 0, live, 0, true);
+          op.param = (uint32_t)set_id;
           P->ops.push_back(op);
           continue;
         }
         const int g0 = it.gates[0];
         const GateIn& gi0 = gates[g0];
+        const bool one_q_item = it.type == 1 || (it.type == 0 && gi0.kind != G_CNOT && gi0.kind != G_CZ);
         if (it.type == 1 && it.gates.size() > 1) {
           if (block_has_grad(it)) {
             publish_if_dirty();
@@ -790,6 +832,7 @@ std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total
         } else {
           op.w0 = enc(gi0.kind, operand(gi0.q0), operand(gi0.q1), 0, false);
         }
+        if (it.dead && one_q_item) continue;  // inner products only (Item::dead)
         P->ops.push_back(op);
       }
       if (nred > 1023) return "too many gradient rotations in one segment";

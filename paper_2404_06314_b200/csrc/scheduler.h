@@ -25,6 +25,7 @@ struct ScheduleOptions {
   int segment_cost = 4;      // price of a segment boundary in interior-CNOT units
   int variants = 1;          // greedy restarts per group (refuse the first v new-qubit requests)
   bool fold_thread_targets = false;  // boundary CNOTs may target thread bits (JIT HBM plans)
+  bool skip_dead_unapply = true;  // adjoint sweep: no un-apply for the first 1q operation on a qubit
   bool group_sync = false;   // plan thread-index bits for thread-group barriers (JIT HBM plans)
 };
 
@@ -37,6 +38,7 @@ struct HostProgram {
   int max_red_per_seg = 0;    // reduction slots
   int max_red_per_pass = 0;   // reduction slots of a pass's adjoint segments together
   bool group_sync = false;    // thread-index bits planned for thread-group barriers (ScheduleOptions)
+  bool direct_io = false;     // JIT HBM passes: first / last segment of a sweep exchange registers with HBM directly
   bool warp_red = false;      // JIT HBM adjoint: per-warp reductions, gradients written at the end of the pass
   int max_ipout_per_seg = 0;
   int max_rot_per_pass = 0, max_blk_per_pass = 0, max_av_per_pass = 0;

@@ -287,6 +287,7 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src)
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all_() { cp_async_wait_all(); }  // declared in kernels.cuh (seg_begin_io)
 // one state element (16 B complex128 through L2 only; 8 B complex64)
 __device__ __forceinline__ void cp_async_elem(cplx_t* smem_dst, const cplx_t* gmem_src) {
 #ifdef VQC_C64
@@ -336,7 +337,33 @@ __device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A)
   turn_init();
   if (ADJ && (flags & F_SEED) && A.bra < 0)
     for (int m = vtid(); m < D.M; m += vdim()) s_up[m] = A.upstream[b * D.M + m];
-  if (flags & F_INIT) {
+  // direct tile I/O (kernels.cuh IO_*): which sweep's first / last segment
+  // exchanges its registers with HBM instead of the shared-memory tile
+  uint32_t io_f = 0, io_b = 0;
+  // (per sweep end: the JIT allows it where a warp's accesses coalesce)
+  if ((flags & F_FWD) && pd->seg_end > pd->seg_begin) {
+    if constexpr (SEGS::kDioF)
+      if (flags & F_INIT) io_f |= IO_INIT;
+    if constexpr (SEGS::kDioFL)
+      if (!(flags & F_INIT) && (flags & F_LOAD_PSI) && !(flags & F_LOAD_FIN)) io_f |= IO_LD;
+    if constexpr (SEGS::kDioFS)
+      if ((flags & F_STORE_PSI) && !(flags & (F_STORE_FIN | F_OBSERVE | F_SEED | F_BWD))) io_f |= IO_ST;
+  }
+  if constexpr (ADJ) {
+    if ((flags & F_BWD) && pd->bseg_end > pd->bseg_begin) {
+      if constexpr (SEGS::kDioBL)
+        if (!(flags & (F_FWD | F_OBSERVE | F_SEED | F_INIT | F_LOAD_FIN)) && (flags & F_LOAD_PSI) && (flags & F_LOAD_PHI))
+          io_b |= IO_LD;
+      if constexpr (SEGS::kDioBS)
+        if ((flags & F_STORE_PSI) && (flags & F_STORE_PHI)) io_b |= IO_ST;
+      if constexpr (SEGS::kDioB)
+        if (!(flags & (F_STORE_PSI | F_STORE_PHI))) io_b |= IO_NOST;
+    }
+  }
+  const bool direct_first = ((io_f | io_b) & (IO_LD | IO_INIT)) != 0u;
+  if (direct_first) {
+    // the first segment fills its registers itself
+  } else if (flags & F_INIT) {
     for (int l = vtid(); l < Nt; l += vdim())
       s_psi[swz((uint32_t)l)] = mk_c((tile_base == 0 && l == 0) ? 1 : 0, 0);
   } else {
@@ -367,13 +394,19 @@ __device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A)
   } else {
     build_tables(D, A, pd, b, true, s_cs, s_u, s_av, vtid(), vdim());
   }
-  cp_async_wait_all();
-  vsync();
+  if (!direct_first) {  // else awaited by the first segment, behind its own loads (seg_begin_io)
+    cp_async_wait_all();
+    vsync();
+  }
   dbg_add(A, DBG_PROLOGUE, tdbg);
   const SampleTables T{s_cs, s_u, pd->rot_begin, pd->blk_begin};
-  if (flags & F_FWD)
-    SEGS::template run<R, MODE_FWD>(make_env<MODE_FWD>(D, A, s_psi, s_psi, s_av, 0, pd->av_begin, s_red, s_fin,
-                              grp, grp.role == 0, tile_base, bl, 0, tile, n_tiles), T, pd->seg_begin, pd->seg_end);
+  if (flags & F_FWD) {
+    SegEnv env = make_env<MODE_FWD>(D, A, s_psi, s_psi, s_av, 0, pd->av_begin, s_red, s_fin,
+                                    grp, grp.role == 0, tile_base, bl, 0, tile, n_tiles);
+    env.io = io_f;
+    env.g_psi = A.psi + (size_t)bl * N;
+    SEGS::template run<R, MODE_FWD>(env, T, pd->seg_begin, pd->seg_end);
+  }
   dbg_add(A, DBG_FWD, tdbg);
   if (flags & F_STORE_FIN) {
     uint32_t tb = tile_base;
@@ -389,13 +422,18 @@ __device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A)
   }
   dbg_add(A, DBG_OBSERVE, tdbg);
   if constexpr (ADJ) {
-    if (flags & F_BWD)
-      SEGS::template run<R, BMP>(make_env<BMP>(D, A, s_psi, s_phi, s_av, 0, pd->av_begin,
-                                  s_red, s_fin, grp, true, tile_base, bl, A.bra < 0 ? 0 : A.bra, tile, n_tiles), T, pd->bseg_begin, pd->bseg_end);
+    if (flags & F_BWD) {
+      SegEnv env = make_env<BMP>(D, A, s_psi, s_phi, s_av, 0, pd->av_begin,
+                                 s_red, s_fin, grp, true, tile_base, bl, A.bra < 0 ? 0 : A.bra, tile, n_tiles);
+      env.io = io_b;
+      env.g_psi = A.psi + (size_t)bl * N;
+      env.g_phi = A.phi + (size_t)bl * N;
+      SEGS::template run<R, BMP>(env, T, pd->bseg_begin, pd->bseg_end);
+    }
   }
   dbg_add(A, DBG_BWD, tdbg);
   const bool sphi = ADJ && (flags & F_STORE_PHI);
-  if ((flags & F_STORE_PSI) || sphi) {
+  if (((flags & F_STORE_PSI) || sphi) && !((io_f | io_b) & IO_ST)) {
     asm volatile("" ::: "memory");
     uint32_t tb = tile_base;
     asm volatile("" : "+r"(tb));  // rebuild the tile walk here rather than keep it live
