@@ -9,6 +9,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/vqc.h"
@@ -125,6 +126,7 @@ constexpr int kHbmRegsC64 = 4;
 // keep 4 slots on thread pairs (cfg3: 5.95 vs 6.40 ms). VQC_SMEM_DUAL=1 / 0
 // forces it on / off for 4 <= n <= 12.
 constexpr int kSmemDualMaxN = 10;
+constexpr int kPassMinQubits = 11;  // JIT plans from this size up run the pass kernels (schedule_circuit)
 bool smem_dual(int n) {
   auto env = [](const char* name) {
     const char* v = std::getenv(name);
@@ -633,8 +635,11 @@ int run_core_impl(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, 
     A.psi = psi;
     A.phi = phi;
     A.psi_fin = fin;
-    A.expect = epart;
-    A.ip = ipart;
+    // a tile that is the whole state has no per-tile partials to sum: the
+    // kernels write expectations and inner products in their final layout
+    const bool one_tile = L.n_tiles == 1 && tiles_f == 1;
+    A.expect = (one_tile && d_expect) ? d_expect + (size_t)b0 * p->M : epart;
+    A.ip = one_tile ? ip + (size_t)b0 * L.K * P.NG : ipart;
     A.bra = -1;
     int rc;
     // per-sample angle / block tables of each program that runs
@@ -707,9 +712,9 @@ int run_core_impl(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, 
           if ((rc = adj_pass(pi, F_LOAD_PSI | F_LOAD_PHI | F_BWD | (pi > 0 ? stores : 0)))) return rc;
       }
     }
-    if (adj && (rc = run_tile_reduce(ipart, ip + (size_t)b0 * L.K * P.NG, nb * L.K * P.NG, L.n_tiles, st)))
+    if (adj && !one_tile && (rc = run_tile_reduce(ipart, ip + (size_t)b0 * L.K * P.NG, nb * L.K * P.NG, L.n_tiles, st)))
       return rc;
-    if (d_expect && (rc = run_tile_reduce(epart, d_expect + (size_t)b0 * p->M, nb * p->M, exp_tiles, st)))
+    if (d_expect && !one_tile && (rc = run_tile_reduce(epart, d_expect + (size_t)b0 * p->M, nb * p->M, exp_tiles, st)))
       return rc;
   }
   return VQC_OK;
@@ -769,6 +774,16 @@ int schedule_circuit(const VqcCircuit* c, const int64_t* wrt_col, HostProgram* p
   // HBM tiles: 2^11 complex128 amplitudes (32 KiB per state); complex64
   // elements are half the size, so its tiles hold 2^12 (same bytes)
   opt.tile_qubits = env_int("VQC_TILE_QUBITS", precision == 1 ? kHbmTileC64 : 11);
+  // States of more qubits than this run the pass kernels (tile load, register
+  // segments with thread-group barriers and per-warp reductions, tile store).
+  // With JIT kernels that includes n = 11, 12, whose single tile is the whole
+  // state (cfg3: 5.87 -> 4.91 ms against the on-chip thread-pair kernel); the
+  // smaller on-chip plans keep several samples per CTA. VQC_SMEM_MAX_QUBITS
+  // moves the boundary; interpreter-only plans (VQC_JIT=0) stay on chip to 12.
+  opt.smem_max_qubits = env_int("VQC_JIT", -1) != 0
+                            ? std::max(3, std::min(kSmemMaxQubits, env_int("VQC_SMEM_MAX_QUBITS", kPassMinQubits - 1)))
+                            : kSmemMaxQubits;
+  if (c->n_qubits > opt.smem_max_qubits && c->n_qubits <= kSmemMaxQubits) opt.tile_qubits = c->n_qubits;
   opt.segment_cost = env_int("VQC_SEGMENT_COST", 4);
   opt.variants = std::max(1, env_int("VQC_SCHED_VARIANTS", 1));
   opt.forced_low = std::max(0, std::min(3, env_int("VQC_FORCED_LOW", 3)));  // contiguous low qubits per pass
@@ -1032,15 +1047,23 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
     p->prog.pingpong = pingpong;
     p->prog.warp_red = use_warp_red(p->prog);
     p->prog.direct_io = P.hbm && P.group_sync && pingpong == 0 && env_int("VQC_DIRECT_IO", 0) != 0;
-    err = jit_build(P, use_split(P.n, P.R) && !P.adj_dual, &p->jit);
-    if (!err.empty()) {
-      vqc_plan_destroy(p);
-      return fail(VQC_E_CUDA, err);
-    }
-    p->use_jit = true;
-    // separate forward schedule (VQC_FWD_TILE / VQC_FWD_REG) when it differs
+    // separate forward schedule (VQC_FWD_TILE / VQC_FWD_REG) when it differs:
+    // the main program then only needs its adjoint pass kernels and the
+    // forward program its forward ones, and the two builds run side by side
     const int ft = env_int("VQC_FWD_TILE", P.k), fr = std::max(3, std::min(5, env_int("VQC_FWD_REG", kHbmForwardRegs)));
-    if (P.hbm && (ft != P.k || fr != P.R)) {
+    const bool sep = P.hbm && (ft != P.k || fr != P.R);
+    p->prog.jit_kernels = sep ? 2 : 3;
+    std::string main_err;
+    std::thread main_build([&]() {
+      cudaSetDevice(p->device);
+      main_err = jit_build(P, use_split(P.n, P.R) && !P.adj_dual, &p->jit);
+    });
+    struct Joiner {
+      std::thread& t;
+      ~Joiner() { if (t.joinable()) t.join(); }
+    } joiner{main_build};
+    p->use_jit = true;
+    if (sep) {
       ProgDev* f = new ProgDev();
       p->fwd = f;
       std::vector<uint32_t> zm = p->smask;  // the same trailing gates are absorbed; masks already rewritten
@@ -1064,11 +1087,18 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
         return cuda_fail(e, "plan upload");
       }
       fill_dev(p, f->prog, f->tabs, f->D);
+      f->prog.jit_kernels = 1;
       err = jit_build(f->prog, false, &f->jit);
       if (!err.empty()) {
+        main_build.join();
         vqc_plan_destroy(p);
         return fail(VQC_E_CUDA, err);
       }
+    }
+    main_build.join();
+    if (!main_err.empty()) {
+      vqc_plan_destroy(p);
+      return fail(VQC_E_CUDA, main_err);
     }
   }
   *out = p;

@@ -51,16 +51,30 @@ def test_random_hbm_circuit_compiles_for_sm100a(monkeypatch, fold):
 
 
 def test_on_chip_plan_shares_code_per_segment_shape(monkeypatch):
-    """cfg3 (on-chip): 48 segments of two shapes -> one switch case per shape
-    and unit, compiled in seconds (minutes as one copy per segment)."""
+    """cfg3 kept on chip (VQC_SMEM_MAX_QUBITS=12; by default 11- and 12-qubit
+    plans run the pass kernels on one whole-state tile): 48 segments of two
+    shapes -> one switch case per shape and unit, compiled in seconds
+    (minutes as one copy per segment)."""
     monkeypatch.setenv("VQC_JIT_CACHE", "0")
+    monkeypatch.setenv("VQC_SMEM_MAX_QUBITS", "12")
     spec = configs.CONFIGS[3]
     circ, obs, wrt = configs.build(spec, configs.native_api())
     src, secs = _src(circ, wrt, compile=True)
-    # forward-only unit (1 shape) + forward/adjoint unit (2 shapes)
-    assert src.count("case 0:") == 3 and "case 1:" not in src
+    # forward-only unit (1 shape) + forward/adjoint unit (1 + 2 shapes: the
+    # adjoint segments of the first layer keep only their inner products)
+    assert src.count("case 0:") == 3 and src.count("case 1:") == 1 and "case 2:" not in src
     assert "__constant__ int sab0_opnd" in src and "vqc_jit_sa" in src and "vqc_jit_sf" in src
     assert secs < 120
+
+
+def test_whole_state_tile_plan_for_12_qubits(monkeypatch):
+    """cfg3 by default: one pass whose tile is the whole 12-qubit state, pass
+    kernels with thread-group barriers and per-warp reductions."""
+    spec = configs.CONFIGS[3]
+    circ, obs, wrt = configs.build(spec, configs.native_api())
+    src, _ = _src(circ, wrt)
+    assert src.count("vqc_jit_pa") == 1 and "vqc_jit_sa" not in src
+    assert "__launch_bounds__(512, 1) vqc_jit_pa0" in src and "seg_end_g<R, MODE>" in src and "wr_split<" in src
 
 
 def test_cubin_cache_round_trip(tmp_path, monkeypatch):
