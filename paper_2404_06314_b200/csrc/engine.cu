@@ -126,7 +126,13 @@ constexpr int kHbmRegsC64 = 4;
 // keep 4 slots on thread pairs (cfg3: 5.95 vs 6.40 ms). VQC_SMEM_DUAL=1 / 0
 // forces it on / off for 4 <= n <= 12.
 constexpr int kSmemDualMaxN = 10;
-constexpr int kPassMinQubits = 11;  // JIT plans from this size up run the pass kernels (schedule_circuit)
+// JIT plans from this size up run the pass kernels (schedule_circuit): one
+// sample per CTA with 2^(n-3) threads, i.e. at least a full warp per sample.
+// Up to kPassFusedMaxQubits the forward sweep shares the adjoint schedule and
+// kernel (one launch: cfg2 97 -> 39 us per 1024-row call); above, the forward
+// sweep has its own 4-slot schedule.
+constexpr int kPassMinQubits = 8;
+constexpr int kPassFusedMaxQubits = 10;
 bool smem_dual(int n) {
   auto env = [](const char* name) {
     const char* v = std::getenv(name);
@@ -432,7 +438,7 @@ Layout make_layout(const VqcPlan* p, int64_t B, int mode) {
 // partials per warp when the scheduler planned thread groups and a pass's
 // slots fit a small table (deep passes keep the per-segment CTA reductions)
 bool use_warp_red(const HostProgram& P) {
-  return P.hbm && P.group_sync && P.adj_dual && P.pingpong == 0 && P.max_red_per_pass <= 512;
+  return P.hbm && P.group_sync && P.adj_dual && P.pingpong == 0 && P.max_red_per_pass <= 512 && P.k - P.R >= 5;
 }
 
 int red_slots(const VqcPlan* p) {
@@ -776,13 +782,19 @@ int schedule_circuit(const VqcCircuit* c, const int64_t* wrt_col, HostProgram* p
   opt.tile_qubits = env_int("VQC_TILE_QUBITS", precision == 1 ? kHbmTileC64 : 11);
   // States of more qubits than this run the pass kernels (tile load, register
   // segments with thread-group barriers and per-warp reductions, tile store).
-  // With JIT kernels that includes n = 11, 12, whose single tile is the whole
-  // state (cfg3: 5.87 -> 4.91 ms against the on-chip thread-pair kernel); the
-  // smaller on-chip plans keep several samples per CTA. VQC_SMEM_MAX_QUBITS
+  // With JIT kernels that includes n = 8 ... 12, whose single tile is the
+  // whole state (cfg3: 5.87 -> 4.70 ms against the on-chip thread-pair
+  // kernel); smaller plans keep several samples per CTA. VQC_SMEM_MAX_QUBITS
   // moves the boundary; interpreter-only plans (VQC_JIT=0) stay on chip to 12.
   opt.smem_max_qubits = env_int("VQC_JIT", -1) != 0
                             ? std::max(3, std::min(kSmemMaxQubits, env_int("VQC_SMEM_MAX_QUBITS", kPassMinQubits - 1)))
                             : kSmemMaxQubits;
+  // register slots of a pass plan: 3 with both states per thread; complex64
+  // streams 2^12 tiles with 4 (its whole-state tiles of n <= 12 keep 3)
+  const int pass_regs = std::max(3, std::min(4, env_int("VQC_REG_SLOTS", (precision == 1 && c->n_qubits > kSmemMaxQubits)
+                                                                               ? kHbmRegsC64 : kHbmAdjointRegs)));
+  // (the per-warp reductions of the pass kernels need a full warp per tile)
+  if (c->n_qubits <= kSmemMaxQubits && c->n_qubits - pass_regs < 5) opt.smem_max_qubits = kSmemMaxQubits;
   if (c->n_qubits > opt.smem_max_qubits && c->n_qubits <= kSmemMaxQubits) opt.tile_qubits = c->n_qubits;
   opt.segment_cost = env_int("VQC_SEGMENT_COST", 4);
   opt.variants = std::max(1, env_int("VQC_SCHED_VARIANTS", 1));
@@ -793,7 +805,7 @@ int schedule_circuit(const VqcCircuit* c, const int64_t* wrt_col, HostProgram* p
   // interpreter kernels exist for R = 4 passes only.
   opt.reg_slots = 4;
   if (c->n_qubits > opt.smem_max_qubits && env_int("VQC_JIT", -1) != 0)
-    opt.reg_slots = std::max(3, std::min(4, env_int("VQC_REG_SLOTS", precision == 1 ? kHbmRegsC64 : kHbmAdjointRegs)));
+    opt.reg_slots = pass_regs;
   // small on-chip JIT plans: 3 slots, both states per thread (smem_dual)
   if (c->n_qubits <= opt.smem_max_qubits && smem_dual(c->n_qubits)) opt.reg_slots = 3;
   // HBM plans run JIT kernels, whose address maps take CNOT folds onto
@@ -1050,7 +1062,8 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
     // separate forward schedule (VQC_FWD_TILE / VQC_FWD_REG) when it differs:
     // the main program then only needs its adjoint pass kernels and the
     // forward program its forward ones, and the two builds run side by side
-    const int ft = env_int("VQC_FWD_TILE", P.k), fr = std::max(3, std::min(5, env_int("VQC_FWD_REG", kHbmForwardRegs)));
+    const int ft = env_int("VQC_FWD_TILE", P.k),
+              fr = std::max(3, std::min(5, env_int("VQC_FWD_REG", P.n <= kPassFusedMaxQubits ? P.R : kHbmForwardRegs)));
     const bool sep = P.hbm && (ft != P.k || fr != P.R);
     p->prog.jit_kernels = sep ? 2 : 3;
     std::string main_err;
