@@ -483,20 +483,6 @@ size_t pass_smem(const VqcPlan* p, const HostProgram& P, bool dual, int rs = -1)
                     (int)p->smask.size(), elem_bytes(p)).total;
 }
 
-// persistent two-lane pass kernels (skeleton.cuh pass_persist): shared memory
-// of a CTA and whether a program's passes can use them
-size_t persist_smem(const HostProgram& P, bool dual) {
-  const int warps = std::max(1, (1 << (P.k - P.R)) / 32);
-  return PersistLayout(1 << P.k, dual, P.max_rot_per_pass, P.max_blk_per_pass, P.max_av_per_pass,
-                       dual ? warps * P.max_red_per_pass : 0, P.precision == 1 ? 8 : 16).total;
-}
-bool persist_ok(const HostProgram& P, bool dual) {
-  const int64_t st = 2 * (int64_t)P.n_rot + 8 * (int64_t)P.n_blk + 4 * (int64_t)P.n_av;
-  return P.hbm && P.group_sync && P.pingpong == 0 && (!dual || (P.warp_red && P.adj_dual)) && P.passes.size() > 1 &&
-         P.n - P.k >= 1 && P.k - P.R >= 5 && st > 0 && st * 8 <= 160 * 1024 &&
-         persist_smem(P, dual) <= (size_t)kMaxSmemBytes && env_int("VQC_PERSIST", 1) != 0;
-}
-
 int launch(const char* name, Kern k, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
            const DevProgram& D, const RunArgs& A) {
   if (smem > (size_t)kMaxSmemBytes) return fail(VQC_E_UNSUPPORTED, "shared-memory footprint too large");
@@ -599,7 +585,7 @@ int run_core_impl(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, 
       cudaStreamSynchronize(st);
       const double ctas = h[DBG_CTAS] ? (double)h[DBG_CTAS] : 1.0;
       fprintf(stderr, "[vqc timing] per CTA cycles: prologue %.0f fwd %.0f observe %.0f bwd %.0f store %.0f | "
-              "segments: load %.3f ops %.3f store %.3f final %.3f (ctas %.0f)\n",
+              "segments: load %.0f ops %.0f store %.0f final %.0f (ctas %.0f)\n",
               h[0] / ctas, h[1] / ctas, h[2] / ctas, h[3] / ctas, h[4] / ctas, h[5] / ctas, h[6] / ctas,
               h[7] / ctas, h[8] / ctas, ctas);
     }
@@ -690,11 +676,6 @@ int run_core_impl(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, 
     const int Gb = P.pingpong ? 2 : 1, Gf = PF.pingpong ? 2 : 1;
     const dim3 grid((unsigned)(L.n_tiles / Gb), (unsigned)nb), grid_f((unsigned)(tiles_f / Gf), (unsigned)nb);
     const dim3 block_f((unsigned)(Gf * TPSF)), block2((unsigned)(Gb * (P.adj_dual ? TPS : 2 * TPS)));
-    // persistent kernels: one CTA per SM slot, two lanes per CTA walking the
-    // (row, tile) items of this chunk
-    auto persist_grid = [&](int64_t items, int ctas_per_sm) {
-      return dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)p->sms * ctas_per_sm, (items + 1) / 2)));
-    };
     auto fwd_pass = [&](int pi, uint32_t flags) {
       AF.pass = pi;
       AF.flags = flags;
@@ -703,22 +684,11 @@ int run_core_impl(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, 
       Kern k;
       if (sep) k.cu = p->fwd->jit.pass_fwd[pi];
       else k = pass_k(p, false, pi);
-      if (sep && PF.persist && pi < NPF - 1) {
-        const size_t sm = persist_smem(PF, false);
-        const int per_sm = std::max(1, std::min(256 / TPSF, (int)((size_t)kMaxSmemBytes / sm)));
-        return launch("pass_forward", k, persist_grid(nb * tiles_f, per_sm), dim3((unsigned)(2 * TPSF)), sm, st, DF, AF);
-      }
       return launch("pass_forward", k, grid_f, block_f, Gf * (obs ? smF : smF0), st, DF, AF);
     };
     auto adj_pass = [&](int pi, uint32_t flags) {
       A.pass = pi;
       A.flags = flags;
-      if (P.persist && pi < NP - 1) {
-        RunArgs AP = A;
-        AP.red_slots = std::max(1, TPS / 32) * P.max_red_per_pass;  // doubles of a lane's per-warp partial table
-        return launch("pass_adjoint", pass_k(p, true, pi), persist_grid(nb * L.n_tiles, 1), dim3((unsigned)(2 * TPS)),
-                      persist_smem(P, true), st, D, AP);
-      }
       return launch("pass_adjoint", pass_k(p, true, pi), grid, block2, Gb * smB, st, D, A);
     };
     const uint32_t stores = F_STORE_PSI | F_STORE_PHI;
@@ -924,13 +894,6 @@ int64_t vqc_jit_source(const VqcCircuit* c, const int64_t* wrt_col, int compile,
   prog.pingpong = prog.hbm ? std::max(0, std::min(2, env_int("VQC_PINGPONG", 0))) : 0;
   prog.warp_red = use_warp_red(prog);
   prog.direct_io = prog.hbm && prog.group_sync && prog.pingpong == 0 && env_int("VQC_DIRECT_IO", 0) != 0;
-  // VQC_JIT_SOURCE_KERNELS = 1 / 2: the forward / adjoint kernels of a plan with
-  // a separate forward schedule (persistent two-lane kernels where they apply)
-  const int jk = env_int("VQC_JIT_SOURCE_KERNELS", 3);
-  if (jk == 1 || jk == 2) {
-    prog.jit_kernels = jk;
-    prog.persist = persist_ok(prog, jk == 2);
-  }
   build_thr_table(prog.segs);  // per-segment thread-table offsets, as at plan creation
   const bool split = use_split(prog.n, prog.R) && !prog.adj_dual;
   const std::string src = jit_source(prog, split);
@@ -1103,7 +1066,6 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
               fr = std::max(3, std::min(5, env_int("VQC_FWD_REG", P.n <= kPassFusedMaxQubits ? P.R : kHbmForwardRegs)));
     const bool sep = P.hbm && (ft != P.k || fr != P.R);
     p->prog.jit_kernels = sep ? 2 : 3;
-    p->prog.persist = sep && persist_ok(p->prog, true);
     std::string main_err;
     std::thread main_build([&]() {
       cudaSetDevice(p->device);
@@ -1139,7 +1101,6 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
       }
       fill_dev(p, f->prog, f->tabs, f->D);
       f->prog.jit_kernels = 1;
-      f->prog.persist = persist_ok(f->prog, false);
       err = jit_build(f->prog, false, &f->jit);
       if (!err.empty()) {
         main_build.join();

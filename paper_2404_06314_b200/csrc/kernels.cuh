@@ -50,10 +50,7 @@ __device__ __forceinline__ cplx_t mk_c(real_t a, real_t b) { return make_double2
 //   VQC_PINGPONG == 2: the shared-memory phases (register store, reduction,
 //     next register load) alternate, arithmetic may overlap.
 // vtid / vdim / vsync are the group's thread index, size and barrier.
-// VQC_LANES (persistent pass kernels, skeleton.cuh pass_persist): the same
-// two-group view, free running: each half-CTA "lane" walks its own sequence
-// of tiles and the lanes only share a pool of tile buffers.
-#if defined(VQC_PINGPONG) || defined(VQC_LANES)
+#ifdef VQC_PINGPONG
 __device__ __forceinline__ unsigned cta_group() { return threadIdx.x >= (blockDim.x >> 1) ? 1u : 0u; }
 __device__ __forceinline__ unsigned vdim() { return blockDim.x >> 1; }
 __device__ __forceinline__ unsigned vtid() { return threadIdx.x - cta_group() * (blockDim.x >> 1); }
@@ -67,12 +64,7 @@ __device__ __forceinline__ void turn_wait() {
 __device__ __forceinline__ void turn_pass() {
   asm volatile("bar.arrive %0, %1;" ::"r"(4u - cta_group()), "r"(blockDim.x) : "memory");
 }
-#if defined(VQC_LANES)
-__device__ __forceinline__ void phase_a() {}
-__device__ __forceinline__ void phase_b() {}
-__device__ __forceinline__ void turn_init() {}
-__device__ __forceinline__ void turn_fini() {}
-#elif VQC_PINGPONG == 1
+#if VQC_PINGPONG == 1
 __device__ __forceinline__ void phase_a() { turn_wait(); }
 __device__ __forceinline__ void phase_b() { turn_pass(); }
 // group 0 takes the first turn; it also consumes group 1's last hand-over
@@ -862,7 +854,6 @@ __device__ __forceinline__ void exec_op(const DevProgram& D, const Op op, Regs<R
 // ---------------------------------------------------------------------------
 // Segment frame shared by the interpreter and the JIT: everything a segment
 // needs besides its ops (the caller's run_segments arguments).
-struct LanePrefetch;
 struct SegEnv {
   const DevProgram& D;
   const RunArgs& A;
@@ -879,7 +870,6 @@ struct SegEnv {
   int bra, tile, n_tiles;
   cplx_t* own;
   const cplx_t* partner;
-  struct LanePrefetch* pf = nullptr;  // persistent pass kernels: the lane's next tile (lane_poll)
   // direct tile I/O of the first / last segment of a sweep (JIT HBM passes)
   uint32_t io = 0;
   cplx_t* g_psi = nullptr;  // this row's states in HBM
@@ -1106,12 +1096,7 @@ __device__ __forceinline__ void group_sync(int t) {
   } else if (g <= 32u) {
     __syncwarp();
   } else {
-#ifdef VQC_LANES
-    // lanes: ids 1, 2 are the lane barriers; each lane's levels 1, 2 take six more
-    const unsigned id = 3u + 6u * cta_group() + ((1u << t) - 2u) + vtid() / g;
-#else
     const unsigned id = (1u << t) - 1u + vtid() / g;
-#endif
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(g) : "memory");
   }
 }

@@ -40,8 +40,6 @@ struct HostProgram {
   bool group_sync = false;    // thread-index bits planned for thread-group barriers (ScheduleOptions)
   int jit_kernels = 3;        // HBM pass kernels to build: bit 0 forward, bit 1 adjoint (a plan with a
                               // separate forward schedule needs one kind from each program)
-  bool persist = false;       // HBM passes that neither observe nor seed run persistent two-lane kernels
-                              // with prefetched tiles (skeleton.cuh pass_persist)
   bool direct_io = false;     // JIT HBM passes: first / last segment of a sweep exchange registers with HBM directly
   bool warp_red = false;      // JIT HBM adjoint: per-warp reductions, gradients written at the end of the pass
   int max_ipout_per_seg = 0;

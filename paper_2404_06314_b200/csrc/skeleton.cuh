@@ -451,266 +451,4 @@ __device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A)
   turn_fini();
 }
 
-// ---------------------------------------------------------------------------
-// Persistent pass kernels (JIT units built with VQC_LANES). A pass over
-// HBM-resident states costs every tile a load and a store on top of its
-// arithmetic, and with two resident CTAs per SM the SM's FP64 pipe runs half
-// empty whenever one of them waits for its tile: measured per pass, time =
-// a + b * (FP64 instructions) with a ~ 25 % of the total. Here one CTA per
-// SM slot stays resident and its two half-CTA lanes walk their own tile
-// sequences (item i -> row i / tiles, tile i % tiles; lane l of CTA c takes
-// items 2c + l + 2 j gridDim.x). The CTA holds three tile buffers: one per
-// lane plus a spare that the lanes use in turn to prefetch their next tile
-// with cp.async while they compute (lane_poll, called between segments), so
-// a lane's load hides behind its own arithmetic and only the store and the
-// switch remain exposed. The spare is handed over explicitly: a lane that
-// moves into its prefetched buffer releases its old one to the other lane,
-// which holds exactly one buffer at that moment. Lane 1 starts when lane 0
-// is half way through its first tile, so the hand-overs alternate. No lane
-// ever waits for the other: without a prefetched tile it loads into its own
-// buffer as the plain kernel does.
-struct LanePrefetch {
-  volatile int* s_free;   // -1 or (buffer | owner lane << 8)
-  volatile int* s_flag;   // lane 0 reached the middle of its first tile
-  volatile int* s_mail;   // the lane's poll result, broadcast by its thread 0
-  int want;               // the lane has a next item
-  int got;                // buffer holding (or receiving) the next item's tile, -1 none
-  int lane;
-  // what issue() needs
-  const DevProgram* D;
-  const RunArgs* A;
-  const PassDesc* pd;
-  unsigned char* bufs;    // three tile buffers
-  size_t buf_bytes;
-  unsigned char* tab_next;  // the lane's other table set
-  int64_t bl;             // next item's row and tile
-  uint32_t tile_base;
-};
-
-struct PersistLayout {
-  size_t buf, bufs, tab_cs, tab_u, tab_av, tab, red, ctrl, total;
-  // tile buffer = psi [+ phi]; per lane: two table sets and the per-warp partial table
-  __host__ __device__ PersistLayout(int n_amp, bool dual, int nrot, int nblk, int nav, int wred_doubles, int esz) {
-    buf = (size_t)n_amp * esz * (dual ? 2 : 1);
-    bufs = 0;
-    size_t o = 3 * buf;
-    tab_cs = 0;
-    tab_u = (size_t)nrot * 16;
-    tab_av = tab_u + (size_t)nblk * 64;
-    tab = (tab_av + (size_t)nav * 32 + 127) & ~(size_t)127;
-    // lane l: tables at o + l * (2 * tab + red), then its partial table
-    red = ((size_t)wred_doubles * 8 + 127) & ~(size_t)127;
-    ctrl = o + 2 * (2 * tab + red);
-    total = ctrl + 128;
-  }
-  __host__ __device__ size_t lane_base(int l) const { return 3 * buf + (size_t)l * (2 * tab + red); }
-};
-
-// cp.async of one tile (psi and, for adjoint passes, phi) and the row's table
-// slices; completion is awaited by the lane before it computes on them
-template <int R, bool ADJ, class PM>
-__device__ __forceinline__ void lane_issue_load(const DevProgram& D, const RunArgs& A, const PassDesc* pd,
-                                                unsigned char* buf, unsigned char* tab, const PersistLayout& PL,
-                                                int64_t bl, uint32_t tile_base) {
-  constexpr int E = 1 << R;
-  constexpr int k = PM::k, Nt = 1 << k;
-  const size_t N = (size_t)1 << D.n;
-  cplx_t* s_psi = reinterpret_cast<cplx_t*>(buf);
-  cplx_t* s_phi = s_psi + Nt;
-  const cplx_t* src = A.psi + (size_t)bl * N;
-  const cplx_t* srcf = A.phi + (size_t)bl * N;
-  const TileWalk tw = tile_walk<PM>(pd, tile_base, k, vtid(), (int)vdim());
-  for_tile<E>(tw, [&](uint32_t sw, uint32_t j) {
-    VQC_CHECK(A, j < (uint32_t)N && sw < (uint32_t)Nt, CHK_TILE_GLOBAL);
-    cp_async_elem(s_psi + sw, src + j);
-    if constexpr (ADJ) cp_async_elem(s_phi + sw, srcf + j);
-  });
-  const double* t = A.tables + (size_t)bl * A.table_stride;
-  const int nrot = pd->rot_end - pd->rot_begin, nblk = pd->blk_end - pd->blk_begin, nav = pd->av_end - pd->av_begin;
-  const double* tcs = t + 2 * pd->rot_begin;
-  const double* tu = t + 2 * (size_t)D.n_rot + 8 * (size_t)pd->blk_begin;
-  const double* tav = t + 2 * (size_t)D.n_rot + 8 * (size_t)D.n_blk + 4 * (size_t)pd->av_begin;
-  double2* s_cs = reinterpret_cast<double2*>(tab + PL.tab_cs);
-  double2* s_u = reinterpret_cast<double2*>(tab + PL.tab_u);
-  double* s_av = reinterpret_cast<double*>(tab + PL.tab_av);
-  for (int i = vtid(); i < nrot; i += vdim()) cp_async16(s_cs + i, tcs + 2 * i);
-  for (int i = vtid(); i < 4 * nblk; i += vdim()) cp_async16(s_u + i, tu + 2 * i);
-  for (int i = vtid(); i < 2 * nav; i += vdim()) cp_async16(s_av + 2 * i, tav + 2 * i);
-}
-
-// Between two segments of a persistent lane (lane-uniform call): take the
-// spare buffer if it was handed to this lane and start loading the next tile.
-// idx / count: position of the call in the sweep (lane 0 releases lane 1's
-// start at the middle of its first tile).
-template <int R, bool ADJ, class PM>
-__device__ __forceinline__ void lane_poll(const SegEnv& E, int idx, int count) {
-#ifdef VQC_LANES
-  LanePrefetch* pf = E.pf;
-  if (pf == nullptr) return;
-  if (pf->lane == 0 && 2 * (idx + 1) >= count) {
-    if (vtid() == 0) *pf->s_flag = 1;
-  }
-  if (pf->got >= 0 || !pf->want) return;
-  if (pf->A->dbg && vtid() == 0) atomicAdd(pf->A->dbg + DBG_SEG_OPS, 1ull);
-  vsync();
-  if (vtid() == 0) {
-    const int v = *pf->s_free;
-    int b = -1;
-    if (v >= 0 && (v >> 8) == pf->lane) {
-      b = v & 0xff;
-      *pf->s_free = -1;
-    }
-    __threadfence_block();
-    *pf->s_mail = b;
-  }
-  vsync();
-  const int b = *pf->s_mail;
-  if (b >= 0) {
-    if (pf->A->dbg && vtid() == 0) atomicAdd(pf->A->dbg + DBG_SEG_FINAL, 1ull);
-    pf->got = b;
-    const PersistLayout PL(1 << PM::k, ADJ, pf->D->max_rot_pass, pf->D->max_blk_pass, pf->D->max_av_pass, 0,
-                           (int)sizeof(cplx_t));
-    lane_issue_load<R, ADJ, PM>(*pf->D, *pf->A, pf->pd, pf->bufs + (size_t)b * pf->buf_bytes, pf->tab_next, PL, pf->bl,
-                                pf->tile_base);
-  }
-#endif
-}
-
-#ifdef VQC_LANES
-template <int R, int KM, class SEGS>
-__device__ __forceinline__ void pass_persist(const DevProgram& D, const RunArgs& A) {
-  constexpr bool ADJ = KM != KM_FWD;
-  static_assert(KM == KM_FWD || KM == KM_DUAL, "persistent lanes hold both states per thread");
-  constexpr int E = 1 << R;
-  constexpr int BMP = MODE_DUAL;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  using PM = typename SEGS::PM;
-  const PassDesc* pd = D.passes + A.pass;
-  constexpr int k = PM::k, Nt = 1 << k;
-  const uint32_t flags = A.flags;
-  const int lane = (int)cta_group();
-  const Group grp = make_group<R, KM>(1 << (k - R), 1);
-  const size_t N = (size_t)1 << D.n;
-  const int n_tiles = 1 << (D.n - k);
-  const PersistLayout PL(Nt, ADJ, D.max_rot_pass, D.max_blk_pass, D.max_av_pass, A.red_slots, (int)sizeof(cplx_t));
-  unsigned char* const bufs = smem_raw;
-  unsigned char* const lane_mem = smem_raw + PL.lane_base(lane);
-  double* s_red = reinterpret_cast<double*>(lane_mem + 2 * PL.tab);
-  volatile int* s_free = reinterpret_cast<volatile int*>(smem_raw + PL.ctrl);
-  volatile int* s_flag = s_free + 1;
-  const int64_t n_items = A.nb * (int64_t)n_tiles;
-  const int64_t stride = 2 * (int64_t)gridDim.x;
-  int64_t it = 2 * (int64_t)blockIdx.x + lane;
-  if (threadIdx.x == 0) {
-    *s_free = 2 | (0 << 8);  // the spare goes to lane 0 first
-    *s_flag = (2 * (int64_t)blockIdx.x >= n_items) ? 1 : 0;  // lane 0 idle: lane 1 starts at once
-  }
-  __syncthreads();
-  if (lane == 1 && it < n_items) {
-    while (*s_flag == 0) __nanosleep(200);
-  }
-  int cur = lane, tb = 0;
-  bool loaded = false;
-  const bool stores = (flags & F_STORE_PSI) != 0;
-  while (it < n_items) {
-    const int64_t bl = it / n_tiles;
-    const int tile = (int)(it - bl * n_tiles);
-    const uint32_t tile_base = PM::tile_dep(pd, D.n, (uint32_t)tile);
-    unsigned char* const buf = bufs + (size_t)cur * PL.buf;
-    unsigned char* const tab = lane_mem + (size_t)tb * PL.tab;
-    long long tdbg = A.dbg ? clock64() : 0;
-    if (A.dbg && vtid() == 0) {  // VQC_DEBUG_TIMING: items, and how many found their tile prefetched
-      atomicAdd(A.dbg + DBG_CTAS, 1ull);
-      atomicAdd(A.dbg + (loaded ? DBG_SEG_LOAD : DBG_SEG_STORE), 1ull);
-    }
-    cplx_t* s_psi = reinterpret_cast<cplx_t*>(buf);
-    cplx_t* s_phi = s_psi + (ADJ ? Nt : 0);
-    if (!loaded) {
-      if (flags & F_INIT) {
-        for (int l = vtid(); l < Nt; l += vdim()) s_psi[swz((uint32_t)l)] = mk_c((tile_base == 0 && l == 0) ? 1 : 0, 0);
-        // tables only
-        const cplx_t* keep_psi = A.psi;
-        (void)keep_psi;
-        const double* t = A.tables + (size_t)bl * A.table_stride;
-        const int nrot = pd->rot_end - pd->rot_begin, nblk = pd->blk_end - pd->blk_begin, nav = pd->av_end - pd->av_begin;
-        double2* c_cs = reinterpret_cast<double2*>(tab + PL.tab_cs);
-        double2* c_u = reinterpret_cast<double2*>(tab + PL.tab_u);
-        double* c_av = reinterpret_cast<double*>(tab + PL.tab_av);
-        for (int i = vtid(); i < nrot; i += vdim()) cp_async16(c_cs + i, t + 2 * pd->rot_begin + 2 * i);
-        for (int i = vtid(); i < 4 * nblk; i += vdim())
-          cp_async16(c_u + i, t + 2 * (size_t)D.n_rot + 8 * (size_t)pd->blk_begin + 2 * i);
-        for (int i = vtid(); i < 2 * nav; i += vdim())
-          cp_async16(c_av + 2 * i, t + 2 * (size_t)D.n_rot + 8 * (size_t)D.n_blk + 4 * (size_t)pd->av_begin + 2 * i);
-      } else {
-        lane_issue_load<R, ADJ, PM>(D, A, pd, buf, tab, PL, bl, tile_base);
-      }
-    }
-    cp_async_wait_all();
-    vsync();
-    dbg_add(A, DBG_PROLOGUE, tdbg);
-    double2* s_cs = reinterpret_cast<double2*>(tab + PL.tab_cs);
-    double2* s_u = reinterpret_cast<double2*>(tab + PL.tab_u);
-    double* s_av = reinterpret_cast<double*>(tab + PL.tab_av);
-    const SampleTables T{s_cs, s_u, pd->rot_begin, pd->blk_begin};
-    LanePrefetch pf;
-    pf.s_free = s_free;
-    pf.s_flag = s_flag;
-    pf.s_mail = s_free + 2 + lane;
-    pf.lane = lane;
-    pf.got = -1;
-    const int64_t nit = it + stride;
-    pf.want = (nit < n_items && !(flags & F_INIT)) ? 1 : 0;
-    pf.D = &D;
-    pf.A = &A;
-    pf.pd = pd;
-    pf.bufs = bufs;
-    pf.buf_bytes = PL.buf;
-    pf.tab_next = lane_mem + (size_t)(tb ^ 1) * PL.tab;
-    pf.bl = nit / n_tiles;
-    pf.tile_base = PM::tile_dep(pd, D.n, (uint32_t)(nit - pf.bl * n_tiles));
-    if constexpr (!ADJ) {
-      SegEnv env = make_env<MODE_FWD>(D, A, s_psi, s_psi, s_av, 0, pd->av_begin, s_red, s_red, grp, true, tile_base, bl, 0,
-                                      tile, n_tiles);
-      env.pf = &pf;
-      SEGS::template run<R, MODE_FWD>(env, T, pd->seg_begin, pd->seg_end);
-    } else {
-      SegEnv env = make_env<BMP>(D, A, s_psi, s_phi, s_av, 0, pd->av_begin, s_red, s_red, grp, true, tile_base, bl,
-                                 A.bra < 0 ? 0 : A.bra, tile, n_tiles);
-      env.pf = &pf;
-      SEGS::template run<R, BMP>(env, T, pd->bseg_begin, pd->bseg_end);
-    }
-    if (lane == 0 && vtid() == 0) *s_flag = 1;  // (at the latest: sweeps without a poll in their first half)
-    dbg_add(A, ADJ ? DBG_BWD : DBG_FWD, tdbg);
-    if (stores) {
-      asm volatile("" ::: "memory");
-      uint32_t tbx = tile_base;
-      asm volatile("" : "+r"(tbx));
-      const TileWalk tw = tile_walk<PM>(pd, tbx, k, vtid(), (int)vdim());
-      cplx_t* dst = A.psi + (size_t)bl * N;
-      cplx_t* dstf = A.phi + (size_t)bl * N;
-      for_tile<E>(tw, [&](uint32_t sw, uint32_t j) {
-        VQC_CHECK(A, j < (uint32_t)N && sw < (uint32_t)Nt, CHK_TILE_GLOBAL);
-        dst[j] = s_psi[sw];
-        if constexpr (ADJ) dstf[j] = s_phi[sw];
-      });
-    }
-    vsync();  // the lane is done reading this buffer and its tables
-    dbg_add(A, DBG_STORE, tdbg);
-    if (pf.got >= 0) {
-      if (vtid() == 0) {
-        __threadfence_block();
-        *s_free = cur | ((lane ^ 1) << 8);  // hand the old buffer to the other lane
-      }
-      cur = pf.got;
-      tb ^= 1;
-      loaded = true;
-    } else {
-      loaded = false;
-    }
-    it = nit;
-  }
-  if (lane == 0 && vtid() == 0) *s_flag = 1;
-}
-#endif
-
 }  // namespace vqc
