@@ -441,9 +441,12 @@ def roofline_from_profile(spec, prof: dict, steps: int, rows_total: int,
         "peak_source": how,
     }
     # measured DRAM traffic (ncu dram__bytes_read.sum + dram__bytes_write.sum
-    # over every launch of one fwd+adjoint call, profiles/r01/traffic_cfg<id>.json)
+    # over every launch of one fwd+adjoint call, profiles/r0N/traffic_cfg<id>.json:
+    # the latest round that captured this config)
     try:
-        with open(os.path.join(ROOT, "profiles", "r01", f"traffic_cfg{spec.cfg_id}.json")) as fh:
+        rnd = next(r for r in ("r02", "r01")
+                   if os.path.exists(os.path.join(ROOT, "profiles", r, f"traffic_cfg{spec.cfg_id}.json")))
+        with open(os.path.join(ROOT, "profiles", rnd, f"traffic_cfg{spec.cfg_id}.json")) as fh:
             tr = json.load(fh)
         per_sample = sum(v.get("dram_bytes_per_sample", 0.0) for k, v in tr["kernels"].items()
                          if k.startswith("pass_") or k.startswith("smem_"))
@@ -451,8 +454,8 @@ def roofline_from_profile(spec, prof: dict, steps: int, rows_total: int,
             out["traffic"] = per_sample * rows_total / max(evo_launches, 1.0)
             out["traffic_unit"] = "DRAM bytes per state-evolution launch (ncu, scaled to this step's rows)"
             out["traffic_bytes_per_sample"] = per_sample
-            out["traffic_source"] = "profiles/r01/" + f"traffic_cfg{spec.cfg_id}.json"
-    except (OSError, KeyError, ValueError):
+            out["traffic_source"] = f"profiles/{rnd}/traffic_cfg{spec.cfg_id}.json"
+    except (OSError, KeyError, ValueError, StopIteration):
         pass
     hb = configs.hbm_bytes_per_sample(spec, K=1)
     if hb > 0 and evo_ms > 0:

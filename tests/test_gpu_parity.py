@@ -97,7 +97,7 @@ def _vjp_device(torch, eng, circ, obs, wrt, w, x, up):
     plan, layout = eng.plans.get(circ, obs, wrt, eng.device)
     dev = eng.device
     B, M = len(x), len(obs)
-    flat = eng.base_flat(circ, {"w": w})
+    flat = eng.base_flat(circ, w if isinstance(w, dict) else {"w": w})
     d_x, d_w = torch.from_numpy(x).to(dev), torch.from_numpy(flat).to(dev)
     d_up = torch.from_numpy(np.ascontiguousarray(up)).to(dev)
     rows = torch.empty((B, layout.n_cols), dtype=torch.float64, device=dev)
@@ -230,6 +230,59 @@ def test_random_with_cz_vs_oracle(torch_cuda, n):
     circ, trainable = _rand_circuit(rng, n, 30 + 4 * n)
     obs = _z_obs(rng, n, 3)
     x = rng.uniform(-2, 2, (5, 4))
+    wrt = ("a", "b", "s")
+    e_ref, j_ref = oracle_batch(circ, obs, trainable, x, wrt)
+    res = _engine().run_batch(_request(circ, obs, trainable, x, wrt))
+    assert close(res.expectations, e_ref) < TOL
+    for k in wrt:
+        assert close(res.gradients[k], j_ref[k]) < TOL
+
+
+def _pauli_obs(rng, n, m):
+    from paper_2404_06314_b200.observables import Observable
+    out = []
+    for _ in range(m):
+        terms = []
+        for _ in range(int(rng.integers(1, 4))):
+            terms.append((float(rng.uniform(-2, 2)), "".join("IXYZ"[int(rng.integers(4))] for _ in range(n))))
+        out.append(Observable(tuple(terms)))
+    return out
+
+
+@pytest.mark.parametrize("n", [8, 9, 10, 11, 12])
+def test_whole_state_tile_general_observables(torch_cuda, n):
+    """8 <= n <= 12 run the pass kernels on one tile holding the whole state
+    (n <= 10: forward and adjoint in one kernel; 11, 12: separate 4-slot
+    forward kernel, 256 / 512-thread CTAs with thread-group barriers): general
+    X/Y/Z strings, Jacobians and a VJP with a row-dependent upstream."""
+    rng = np.random.default_rng(700 + n)
+    circ, trainable = _rand_circuit(rng, n, 40 + 4 * n)
+    obs = _pauli_obs(rng, n, 3)
+    x = rng.uniform(-2, 2, (6, 4))
+    wrt = ("a", "b", "s")
+    e_ref, j_ref = oracle_batch(circ, obs, trainable, x, wrt)
+    res = _engine().run_batch(_request(circ, obs, trainable, x, wrt))
+    assert close(res.expectations, e_ref) < TOL
+    for k in wrt:
+        assert close(res.gradients[k], j_ref[k]) < TOL
+    up = rng.uniform(-1, 1, (len(x), len(obs)))
+    e, rows, vsum = _vjp_device(torch_cuda, _engine(), circ, obs, wrt, trainable, x, up)
+    ref_rows = np.concatenate([np.einsum("bm,bmp->bp", up, j_ref[k]) for k in wrt], axis=1)
+    assert close(e, e_ref) < TOL
+    assert close(rows, ref_rows) < TOL
+    assert close(vsum, ref_rows.sum(axis=0)) < 1e-10 * max(1.0, np.abs(ref_rows).sum(axis=0).max())
+
+
+@pytest.mark.parametrize("n", [9, 12])
+def test_on_chip_jit_kernels_kept_by_knob(torch_cuda, monkeypatch, n):
+    """VQC_SMEM_MAX_QUBITS=12 keeps 8-12 qubit plans on the on-chip JIT kernels
+    (several samples per CTA / thread pairs), the default before the pass
+    kernels took them over."""
+    monkeypatch.setenv("VQC_SMEM_MAX_QUBITS", "12")
+    rng = np.random.default_rng(800 + n)
+    circ, trainable = _rand_circuit(rng, n, 30 + 4 * n)
+    obs = _pauli_obs(rng, n, 2)
+    x = rng.uniform(-2, 2, (4, 4))
     wrt = ("a", "b", "s")
     e_ref, j_ref = oracle_batch(circ, obs, trainable, x, wrt)
     res = _engine().run_batch(_request(circ, obs, trainable, x, wrt))
