@@ -29,6 +29,40 @@ __device__ __forceinline__ void stage_terms(const DevProgram& D, TermSm* s_terms
   }
 }
 
+// In-place Walsh-Hadamard transform of a thread's E values (natural order):
+// W[h] = sum_i (-1)^{popc(i & h)} v[i]. A Z string's sign over a thread's
+// elements is (-1)^{p0 ^ popc(i & h)} with h the same for every thread of the
+// tile, so its sum over them is +-W[h], and the adjoint seed's weights are the
+// transform of the per-h sums of the term coefficients.
+template <int E>
+__device__ __forceinline__ void wht(double (&v)[E]) {
+#pragma unroll
+  for (int len = 1; len < E; len <<= 1) {
+#pragma unroll
+    for (int i = 0; i < E; ++i)
+      if (!(i & len)) {
+        const double a = v[i], b = v[i | len];
+        v[i] = a + b;
+        v[i | len] = a - b;
+      }
+  }
+}
+// v[h] with a run-time (tile-uniform) h: a uniform branch, no local memory
+template <int E>
+__device__ __forceinline__ double pick(const double (&v)[E], uint32_t h) {
+  double r = v[0];
+#pragma unroll
+  for (int i = 1; i < E; ++i)
+    if (h == (uint32_t)i) r = v[i];
+  return r;
+}
+template <int E>
+__device__ __forceinline__ void add_at(double (&v)[E], uint32_t h, double x) {
+#pragma unroll
+  for (int i = 0; i < E; ++i)
+    if (h == (uint32_t)i) v[i] += x;
+}
+
 // Expectations (observables.py / _kernels.py:182-198, Z strings) and the
 // adjoint seed phi = w(j) psi with w = sum_m u_m O_m(j) (VJP) or O_bra(j)
 // (_kernels.py:209-217). Each thread owns `count` tile elements; a term's
@@ -44,11 +78,12 @@ __device__ __forceinline__ void observe(const DevProgram& D, const RunArgs& A, c
   const int lane = grp.lane_in_sample();
   const TileWalk tw = tile_walk<PM>(pd, tile_base, k, lane, grp.TT);
   const int count = tw.count;
+  constexpr int EB = ctz_const(E);  // element-index bits of a thread
   auto term_bits = [&](uint32_t mask, uint32_t& p0, uint32_t& h) {
     p0 = (uint32_t)__popc(tw.base & mask) & 1u;
     h = 0;
 #pragma unroll
-    for (int b = 0; b < kMaxR; ++b) h |= ((uint32_t)__popc(tw.hi[b] & mask) & 1u) << b;
+    for (int b = 0; b < EB; ++b) h |= ((uint32_t)__popc(tw.hi[b] & mask) & 1u) << b;
   };
   if (do_expect) {
     double p2[E];
@@ -63,16 +98,17 @@ __device__ __forceinline__ void observe(const DevProgram& D, const RunArgs& A, c
       }
     }
     for (int m = 0; m < D.M; ++m) s_red[m * (int)vdim() + vtid()] = 0.0;
+    double wh[E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) wh[i] = p2[i];
+    wht<E>(wh);
     for (int t = 0; t < D.T; ++t) {
       const TermSm ts = s_terms[t];
       if (ts.xmask != 0u) continue;
       uint32_t p0, h;
       term_bits(ts.mask, p0, h);
-      double v = 0.0;
-#pragma unroll
-      for (int i = 0; i < E; ++i)
-        if (i < count) v += ((p0 ^ (uint32_t)__popc((uint32_t)i & h)) & 1u) ? -p2[i] : p2[i];
-      s_red[ts.obs * (int)vdim() + vtid()] += ts.coeff * v;
+      const double v = pick<E>(wh, h);
+      s_red[ts.obs * (int)vdim() + vtid()] += ts.coeff * (p0 ? -v : v);
     }
     if (D.has_xy) {
       // X/Y strings (on-chip states only): Re sum_j conj(psi_j) i^k (-1)^{popc((j^x)&s)} psi_{j^x}
@@ -125,9 +161,9 @@ __device__ __forceinline__ void observe(const DevProgram& D, const RunArgs& A, c
         if (e == 0.0) continue;
         uint32_t p0, h;
         term_bits(ts.mask, p0, h);
-#pragma unroll
-        for (int i = 0; i < E; ++i) w[i] += ((p0 ^ (uint32_t)__popc((uint32_t)i & h)) & 1u) ? -e : e;
+        add_at<E>(w, h, p0 ? -e : e);
       }
+      wht<E>(w);  // w[i] = sum_h (-1)^{popc(i & h)} (per-h sums)
 #pragma unroll
       for (int i = 0; i < E; ++i) {
         if (i >= count) break;
