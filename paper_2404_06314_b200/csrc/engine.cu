@@ -87,16 +87,22 @@ __global__ void k_chain(DevProgram D, RunArgs A, const double* __restrict__ ip, 
 // out[col] = sum_b rows[b, col] in fixed order (model.py:661 einsum over rows)
 __global__ void k_batch_sum(const double* __restrict__ rows, int64_t nb, int ncols,
                             double* __restrict__ out) {
-  __shared__ double part[8][33];
+  __shared__ double part[32][33];
   const int col = blockIdx.x * 32 + threadIdx.x;
-  double v = 0.0;
-  if (col < ncols)
-    for (int64_t b = threadIdx.y; b < nb; b += 8) v += rows[b * ncols + col];
-  part[threadIdx.y][threadIdx.x] = v;
+  double v0 = 0.0, v1 = 0.0;  // 32 row slices per column, two chains each
+  if (col < ncols) {
+    int64_t b = threadIdx.y;
+    for (; b + 32 < nb; b += 64) {
+      v0 += rows[b * ncols + col];
+      v1 += rows[(b + 32) * ncols + col];
+    }
+    if (b < nb) v0 += rows[b * ncols + col];
+  }
+  part[threadIdx.y][threadIdx.x] = v0 + v1;
   __syncthreads();
   if (threadIdx.y == 0 && col < ncols) {
     double s = 0.0;
-    for (int w = 0; w < 8; ++w) s += part[w][threadIdx.x];
+    for (int w = 0; w < 32; ++w) s += part[w][threadIdx.x];
     out[col] = s;
   }
 }
@@ -654,7 +660,10 @@ int run_core_impl(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, 
     A.table_stride = 0;
     AF.tables = nullptr;
     AF.table_stride = 0;
-    if (L.table_stride > 0 && (!sep || mode != VQC_MODE_FORWARD)) {
+    // (a whole-state tile is its sample's only CTA: it builds the tables
+    // itself, build_tables in pass_body, instead of a k_tables launch)
+    if (one_tile) {
+    } else if (L.table_stride > 0 && (!sep || mode != VQC_MODE_FORWARD)) {
       A.tables = reinterpret_cast<double*>(ws + L.tables);
       A.table_stride = L.table_stride;
       if ((rc = launch("tables", Kern{k_tables, nullptr}, dim3((unsigned)nb), dim3(256),
@@ -664,7 +673,7 @@ int run_core_impl(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, 
     if (!sep) {
       AF.tables = A.tables;
       AF.table_stride = A.table_stride;
-    } else if (L.ftable_stride > 0) {
+    } else if (L.ftable_stride > 0 && !one_tile) {
       AF.tables = reinterpret_cast<double*>(ws + L.ftables);
       AF.table_stride = L.ftable_stride;
       if ((rc = launch("tables", Kern{k_tables, nullptr}, dim3((unsigned)nb), dim3(256),
@@ -1230,7 +1239,7 @@ int vqc_adjoint(VqcPlan* p, const double* d_in, const double* d_w, int64_t B, co
   double* rows = d_rows ? d_rows : reinterpret_cast<double*>(w + L.rows);
   if ((rc = run_chain(p, d_in, d_w, ip, B, 1, rows, st))) return rc;
   if (d_sum) {
-    const dim3 block(32, 8), grid((unsigned)((P.n_cols + 31) / 32));
+    const dim3 block(32, 32), grid((unsigned)((P.n_cols + 31) / 32));
     ProfScope ps("batch_sum", st);
     k_batch_sum<<<grid, block, 0, st>>>(rows, B, P.n_cols, d_sum);
     ++g_launches;
