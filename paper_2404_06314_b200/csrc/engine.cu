@@ -767,6 +767,23 @@ int check_common(const VqcPlan* p, const double* d_in, const double* d_w, int64_
 int schedule_circuit(const VqcCircuit* c, const int64_t* wrt_col, HostProgram* prog,
                      std::vector<uint32_t>* zmask = nullptr, std::vector<double>* zcoeff = nullptr,
                      int tile_override = 0, int regs_override = 0, int precision = 0) {
+  // Idle-qubit padding: a circuit of 4-7 qubits is planned on 8, the extra
+  // qubits staying in |0>, so it runs the pass kernels (one warp per sample,
+  // warp-level synchronisation and reductions) instead of the on-chip kernels,
+  // which are latency-bound at a few warps per SM: 16384 rows of 8 layers on
+  // 4 / 5 / 6 / 7 qubits 2.9e6 / 4.0e6 / 5.6e6 / 4.2e6 -> 1.46e7 / 1.24e7 /
+  // 1.14e7 / 9.6e6 samples/s, cfg1 0.072 -> 0.047 ms per call. Amplitudes
+  // with an idle bit set stay exactly zero, so results only move by summation
+  // order. VQC_PAD_QUBITS=0 turns it off (the on-chip JIT kernels).
+  const int n_true = c->n_qubits;
+  const int pad_to = env_int("VQC_JIT", -1) != 0 ? std::min(kSmemMaxQubits, env_int("VQC_PAD_QUBITS", kPassMinQubits)) : 0;
+  const int nq = (n_true >= 4 && n_true < pad_to) ? pad_to : n_true;
+  if (nq != n_true)
+    for (int64_t g = 0; g < c->n_gates; ++g) {
+      const bool two = c->kinds[g] == G_CNOT || c->kinds[g] == G_CZ;
+      if (c->q0[g] < 0 || c->q0[g] >= n_true || (two && (c->q1[g] < 0 || c->q1[g] >= n_true)))
+        return fail(VQC_E_INVALID, "gate " + std::to_string(g) + ": qubit out of range");
+    }
   std::vector<GateIn> gates((size_t)c->n_gates);
   for (int64_t g = 0; g < c->n_gates; ++g) {
     GateIn& gi = gates[g];
@@ -784,7 +801,7 @@ int schedule_circuit(const VqcCircuit* c, const int64_t* wrt_col, HostProgram* p
   }
   std::vector<int64_t> wcol((size_t)c->total_params, -1);
   for (int64_t i = 0; i < c->total_params; ++i) wcol[i] = wrt_col[i];
-  if (zmask) prog->absorbed = absorb_trailing_gates(&gates, c->n_qubits, zmask, zcoeff);
+  if (zmask) prog->absorbed = absorb_trailing_gates(&gates, nq, zmask, zcoeff);
   ScheduleOptions opt;
   // HBM tiles: 2^11 complex128 amplitudes (32 KiB per state); complex64
   // elements are half the size, so its tiles hold 2^12 (same bytes)
@@ -800,11 +817,11 @@ int schedule_circuit(const VqcCircuit* c, const int64_t* wrt_col, HostProgram* p
                             : kSmemMaxQubits;
   // register slots of a pass plan: 3 with both states per thread; complex64
   // streams 2^12 tiles with 4 (its whole-state tiles of n <= 12 keep 3)
-  const int pass_regs = std::max(3, std::min(4, env_int("VQC_REG_SLOTS", (precision == 1 && c->n_qubits > kSmemMaxQubits)
+  const int pass_regs = std::max(3, std::min(4, env_int("VQC_REG_SLOTS", (precision == 1 && nq > kSmemMaxQubits)
                                                                                ? kHbmRegsC64 : kHbmAdjointRegs)));
   // (the per-warp reductions of the pass kernels need a full warp per tile)
-  if (c->n_qubits <= kSmemMaxQubits && c->n_qubits - pass_regs < 5) opt.smem_max_qubits = kSmemMaxQubits;
-  if (c->n_qubits > opt.smem_max_qubits && c->n_qubits <= kSmemMaxQubits) opt.tile_qubits = c->n_qubits;
+  if (nq <= kSmemMaxQubits && nq - pass_regs < 5) opt.smem_max_qubits = kSmemMaxQubits;
+  if (nq > opt.smem_max_qubits && nq <= kSmemMaxQubits) opt.tile_qubits = nq;
   opt.segment_cost = env_int("VQC_SEGMENT_COST", 4);
   opt.variants = std::max(1, env_int("VQC_SCHED_VARIANTS", 1));
   opt.forced_low = std::max(0, std::min(3, env_int("VQC_FORCED_LOW", 3)));  // contiguous low qubits per pass
@@ -813,26 +830,26 @@ int schedule_circuit(const VqcCircuit* c, const int64_t* wrt_col, HostProgram* p
   // values (VQC_REG_SLOTS) only for JIT-compiled HBM plans: the prebuilt
   // interpreter kernels exist for R = 4 passes only.
   opt.reg_slots = 4;
-  if (c->n_qubits > opt.smem_max_qubits && env_int("VQC_JIT", -1) != 0)
+  if (nq > opt.smem_max_qubits && env_int("VQC_JIT", -1) != 0)
     opt.reg_slots = pass_regs;
   // small on-chip JIT plans: 3 slots, both states per thread (smem_dual)
-  if (c->n_qubits <= opt.smem_max_qubits && smem_dual(c->n_qubits)) opt.reg_slots = 3;
+  if (nq <= opt.smem_max_qubits && smem_dual(nq)) opt.reg_slots = 3;
   // HBM plans run JIT kernels, whose address maps take CNOT folds onto
   // thread-bit targets (boundary CNOTs then need no register slot: cfg4 80 ->
   // 62 adjoint and 62 -> 52 forward segments); VQC_FOLD_THREAD_TARGETS=0 off
   // (2 = forward program only, 3 = adjoint / main program only: bisection knobs)
   const int ftt = env_int("VQC_FOLD_THREAD_TARGETS", 1);
   const bool fwd_prog = tile_override > 0 || regs_override > 0;
-  opt.fold_thread_targets = c->n_qubits > opt.smem_max_qubits && env_int("VQC_JIT", -1) != 0 &&
+  opt.fold_thread_targets = nq > opt.smem_max_qubits && env_int("VQC_JIT", -1) != 0 &&
                             (ftt == 1 || (ftt == 2 && fwd_prog) || (ftt == 3 && !fwd_prog));
   // thread-group barriers and per-warp reductions in the JIT HBM pass kernels
   // (VQC_GROUP_SYNC=0: CTA barriers and per-segment CTA reductions as before)
-  opt.group_sync = c->n_qubits > opt.smem_max_qubits && env_int("VQC_JIT", -1) != 0 &&
+  opt.group_sync = nq > opt.smem_max_qubits && env_int("VQC_JIT", -1) != 0 &&
                    env_int("VQC_GROUP_SYNC", 1) != 0 && env_int("VQC_PINGPONG", 0) == 0;
   if (tile_override > 0) opt.tile_qubits = tile_override;
   if (regs_override > 0) opt.reg_slots = regs_override;
   const int absorbed = prog->absorbed;
-  std::string err = build_program(gates, c->n_qubits, c->total_params, wcol, opt, prog);
+  std::string err = build_program(gates, nq, c->total_params, wcol, opt, prog);
   prog->absorbed = absorbed;
   if (!err.empty())
     return fail(err.find("out of range") != std::string::npos || err.find("duplicate") != std::string::npos

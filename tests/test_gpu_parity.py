@@ -273,6 +273,29 @@ def test_whole_state_tile_general_observables(torch_cuda, n):
     assert close(vsum, ref_rows.sum(axis=0)) < 1e-10 * max(1.0, np.abs(ref_rows).sum(axis=0).max())
 
 
+@pytest.mark.parametrize("n", [4, 5, 6, 7])
+@pytest.mark.parametrize("pad", ["8", "0"])
+def test_small_circuits_padded_and_on_chip(torch_cuda, monkeypatch, n, pad):
+    """4-7 qubit circuits are planned on 8 qubits by default (idle qubits stay
+    in |0>, pass kernels); VQC_PAD_QUBITS=0 keeps them on the on-chip JIT
+    kernels. Both against the oracle, general observables."""
+    monkeypatch.setenv("VQC_PAD_QUBITS", pad)
+    rng = np.random.default_rng(900 + n)
+    circ, trainable = _rand_circuit(rng, n, 30 + 4 * n)
+    obs = _pauli_obs(rng, n, 3)
+    x = rng.uniform(-2, 2, (37, 4))
+    wrt = ("a", "b", "s")
+    e_ref, j_ref = oracle_batch(circ, obs, trainable, x, wrt)
+    res = _engine().run_batch(_request(circ, obs, trainable, x, wrt))
+    assert close(res.expectations, e_ref) < TOL
+    for k in wrt:
+        assert close(res.gradients[k], j_ref[k]) < TOL
+    up = rng.uniform(-1, 1, (len(x), len(obs)))
+    e, rows, vsum = _vjp_device(torch_cuda, _engine(), circ, obs, wrt, trainable, x, up)
+    ref_rows = np.concatenate([np.einsum("bm,bmp->bp", up, j_ref[k]) for k in wrt], axis=1)
+    assert close(e, e_ref) < TOL and close(rows, ref_rows) < TOL
+
+
 @pytest.mark.parametrize("n", [9, 12])
 def test_on_chip_jit_kernels_kept_by_knob(torch_cuda, monkeypatch, n):
     """VQC_SMEM_MAX_QUBITS=12 keeps 8-12 qubit plans on the on-chip JIT kernels
