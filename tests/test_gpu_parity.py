@@ -333,10 +333,15 @@ def test_kernel_paths_vs_oracle(torch_cuda, monkeypatch, n, jit):
 
 
 @pytest.mark.parametrize("knobs", [{"VQC_ADJ_DUAL": "0", "VQC_REG_SLOTS": "4"}, {"VQC_SMEM_DUAL": "1"},
-                                   {"VQC_FWD_TILE": "12"}])
+                                   {"VQC_FWD_TILE": "12"}, {"VQC_GROUP_SYNC": "0"}, {"VQC_DIRECT_IO": "1"},
+                                   {"VQC_DIRECT_IO": "1", "VQC_DIO_LINES": "2"}, {"VQC_FORCED_LOW": "2"},
+                                   {"VQC_FOLD_THREAD_TARGETS": "0"}])
 def test_schedule_variants_cfg4_rows(torch_cuda, monkeypatch, knobs):
-    """Alternative schedules (thread-pair 4-slot adjoint, dual on-chip adjoint,
-    12-qubit forward tiles) agree with the reference golden rows."""
+    """Alternative schedules and kernel variants kept behind knobs
+    (thread-pair 4-slot adjoint, dual on-chip adjoint, 12-qubit forward
+    tiles, CTA barriers with per-segment CTA reductions, sweep ends
+    exchanging registers with HBM directly, 64-byte HBM chunks, CNOT folds on
+    register targets only) agree with the reference golden rows."""
     from paper_2404_06314_b200 import configs
     for k, v in knobs.items():
         monkeypatch.setenv(k, v)
