@@ -110,6 +110,18 @@ class BatchInputError(RuntimeError):
         self.index = index
 
 
+def _check_rows(values: np.ndarray, row_offset: int, what: str) -> None:
+    """Per-row failure reporting (batch.py:196-202). The reference wraps
+    whatever a row's worker raises in ``BatchInputError(index)``; a GPU row
+    cannot raise, so a row fails when its inputs or its expectations are not
+    finite, and the first such row is reported by its global index."""
+    rows = values.reshape(values.shape[0], -1)
+    bad = ~np.isfinite(rows).all(axis=1)
+    if bad.any():
+        b = int(np.argmax(bad))
+        raise BatchInputError(row_offset + b, FloatingPointError(f"non-finite {what}"))
+
+
 def encoding_set(circuit: Circuit):
     enc = circuit.sets_with_role("encoding")
     if len(enc) != 1:
@@ -317,6 +329,7 @@ class BatchEngine:
             return BatchResult(np.empty((B, M)),
                                {n: np.ascontiguousarray(grad[:, :, lo:hi])
                                 for n, lo, hi in layout.slices})
+        _check_rows(inputs, request.row_offset, "input")
         if circuit.num_qubits > SMEM_MAX_QUBITS and not all(o.is_z_only for o in observables):
             return self._run_basis_groups(request, observables, layout, B, M, C)
         dev = self.device
@@ -341,6 +354,7 @@ class BatchEngine:
                 plan.adjoint(d_in, d_w, None, expect, jac, None, None, ws, stream.cuda_stream)
             expect_h = expect.cpu().numpy()
             jac_h = jac.cpu().numpy() if jac is not None else np.zeros((B, M, 0))
+        _check_rows(expect_h, request.row_offset, "expectation (non-finite parameters?)")
         return BatchResult(expect_h, {n: np.ascontiguousarray(jac_h[:, :, lo:hi])
                                       for n, lo, hi in layout.slices})
 

@@ -130,11 +130,32 @@ def sharded_run_batch(request, run: Callable, rank: int, world: int, group=None,
 
     from .engine import BatchResult
 
+    from .engine import BatchInputError
+
     inputs = np.asarray(request.inputs, np.float64)
     B = inputs.shape[0]
     lo, hi = shard_rows(B, world, rank)
-    local = run(dataclasses.replace(request, inputs=inputs[lo:hi],
-                                    row_offset=request.row_offset + lo))
+    # a failing row (BatchInputError, batch.py:196-202) must fail every rank:
+    # the lowest failing global index is agreed on before anyone leaves, or
+    # the other ranks would wait in the gather below
+    failed, cause = -1, None
+    local = None
+    try:
+        local = run(dataclasses.replace(request, inputs=inputs[lo:hi],
+                                        row_offset=request.row_offset + lo))
+    except BatchInputError as exc:
+        failed, cause = exc.index, exc.__cause__ or exc
+    if _active(group) and world > 1:
+        import torch
+        import torch.distributed as dist
+        big = np.iinfo(np.int64).max
+        t = torch.tensor([failed if failed >= 0 else big], dtype=torch.int64, device=_comm_device(group))
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+        first = int(t.item())
+        if first != big:
+            raise BatchInputError(first, cause if failed == first else RuntimeError("row failed on another rank"))
+    elif failed >= 0:
+        raise BatchInputError(failed, cause)
     if not gather:
         return local
     expect = gather_rows(local.expectations, B, world, group)

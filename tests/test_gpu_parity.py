@@ -393,6 +393,28 @@ def test_degenerate_shapes(torch_cuda):
     assert r.expectations.shape == (3, 0) and r.gradients["x"].shape == (3, 0, 4)
 
 
+def test_failing_input_reports_index(torch_cuda):
+    """Per-row failure reporting (reference tests/test_batch.py:196-209): the
+    reference wraps a failing row's exception in BatchInputError(index); on
+    the GPU a row fails when its inputs or outputs are not finite."""
+    from paper_2404_06314_b200 import BatchInputError, configs
+    spec = configs.CONFIGS[2]
+    circ, obs, wrt = configs.build(spec, configs.native_api())
+    x, w = configs.inputs_and_weights(spec, batch=6)
+    x = x.copy()
+    x[4, 1] = np.nan
+    with pytest.raises(BatchInputError, match="input 4") as ei:
+        _engine().run_batch(_request(circ, obs, {"w": w}, x, wrt))
+    assert ei.value.index == 4
+    x[4, 1] = 0.5
+    wbad = w.copy()
+    wbad[3] = np.inf          # every row's outputs are NaN: the first one is reported
+    with pytest.raises(BatchInputError, match="input 0"):
+        _engine().run_batch(_request(circ, obs, {"w": wbad}, x, wrt))
+    res = _engine().run_batch(_request(circ, obs, {"w": w}, x, wrt))
+    assert np.isfinite(res.expectations).all()
+
+
 def test_xy_observables_on_chip(torch_cuda):
     """General Pauli strings (observables.py:70-92) on the on-chip path."""
     from paper_2404_06314_b200 import configs, parse_observable

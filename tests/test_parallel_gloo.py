@@ -196,3 +196,44 @@ def test_sharded_run_batch_empty_shards(tmp_path):
             np.testing.assert_array_equal(d["g"], full.gradients["x"])
     for r in range(world):
         np.testing.assert_array_equal(np.load(tmp_path / f"v{r}.npy"), [2.0, 4.0])
+
+
+def _failing_run(req):
+    """Stand-in engine call that fails like BatchEngine.run_batch: the first
+    row whose inputs are not finite, reported by its global index."""
+    from paper_2404_06314_b200.engine import _check_rows
+    _check_rows(np.asarray(req.inputs, np.float64), req.row_offset, "input")
+    return _tiny_run(req)
+
+
+def _failure_worker(rank, world, port, out_dir):
+    import torch.distributed as dist
+
+    from paper_2404_06314_b200 import parallel
+    from paper_2404_06314_b200.engine import BatchInputError, BatchRequest
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        x = np.arange(21.0).reshape(7, 3)
+        x[5, 1] = np.nan                      # row 5 lives on rank 1 only
+        got = -1
+        try:
+            parallel.sharded_run_batch(BatchRequest(None, [], {}, x), _failing_run, rank, world)
+        except BatchInputError as exc:
+            got = exc.index
+        # the group is still usable: nobody was left waiting in a collective
+        v = parallel.allreduce_sum(np.array([1.0]))
+        np.save(os.path.join(out_dir, f"f{rank}.npy"), np.array([got, v[0]]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_sharded_run_batch_row_failure_reaches_every_rank(tmp_path):
+    """A row that fails on one rank raises BatchInputError(global index) on
+    every rank (batch.py:196-202), and no rank hangs in the gather."""
+    world = 2
+    mp.start_processes(_failure_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world,
+                       start_method="spawn")
+    for r in range(world):
+        np.testing.assert_array_equal(np.load(tmp_path / f"f{r}.npy"), [5.0, 2.0])
