@@ -853,6 +853,16 @@ int schedule_circuit(const VqcCircuit* c, const int64_t* wrt_col, HostProgram* p
   if (regs_override > 0) opt.reg_slots = regs_override;
   const int absorbed = prog->absorbed;
   std::string err = build_program(gates, nq, c->total_params, wcol, opt, prog);
+  // Passes keep qubits 0-2 local (128-byte chunks in HBM). Keeping only qubits
+  // 0-1 (64-byte chunks) frees a local qubit: worth it only when it saves a
+  // pass (cfg4 16 -> 15 passes, +1 %; cfg5 keeps 13 and would lose 1.5 %).
+  if (err.empty() && prog->hbm && nq > prog->k && opt.forced_low == 3 && std::getenv("VQC_FORCED_LOW") == nullptr) {
+    ScheduleOptions opt2 = opt;
+    opt2.forced_low = 2;
+    HostProgram alt;
+    if (build_program(gates, nq, c->total_params, wcol, opt2, &alt).empty() && alt.passes.size() < prog->passes.size())
+      *prog = std::move(alt);
+  }
   prog->absorbed = absorbed;
   if (!err.empty())
     return fail(err.find("out of range") != std::string::npos || err.find("duplicate") != std::string::npos
