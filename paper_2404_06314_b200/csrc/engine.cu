@@ -825,6 +825,10 @@ int schedule_circuit(const VqcCircuit* c, const int64_t* wrt_col, HostProgram* p
   // (the per-warp reductions of the pass kernels need a full warp per tile)
   if (nq <= kSmemMaxQubits && nq - pass_regs < 5) opt.smem_max_qubits = kSmemMaxQubits;
   if (nq > opt.smem_max_qubits && nq <= kSmemMaxQubits) opt.tile_qubits = nq;
+  // whole-state tiles (n <= 12 on the pass kernels): passes of at most this
+  // many segments, a bound on the JIT compile time of deep circuits (0: one pass)
+  if (nq > opt.smem_max_qubits && nq <= kSmemMaxQubits)
+    opt.max_pass_segments = std::max(0, env_int("VQC_PASS_SEGMENTS", 48));
   opt.segment_cost = env_int("VQC_SEGMENT_COST", 4);
   opt.variants = std::max(1, env_int("VQC_SCHED_VARIANTS", 1));
   opt.forced_low = std::max(0, std::min(3, env_int("VQC_FORCED_LOW", 3)));  // contiguous low qubits per pass

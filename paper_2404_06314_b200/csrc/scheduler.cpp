@@ -374,6 +374,61 @@ std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total
   int next_rot = 0, next_g = 0;
   uint32_t touched = 0;  // qubits some scheduled operation has acted on so far
 
+  // ---- level 2: register segments inside a tile ----
+  // Two policies, priced per pass: segments shaped [CNOTs][body][CNOTs]
+  // (every CNOT folds into address maps, but more segments), or free
+  // placement (interior CNOTs become register permutations). A segment
+  // boundary costs a shared-memory round trip of the tile; an interior
+  // CNOT a few dozen register moves/selects per thread.
+  auto interior_cnots = [&](const std::vector<Group>& gs) {
+    int cost = 0;
+    for (const Group& gr : gs) {
+      size_t a = 0, b = gr.gates.size();
+      while (a < b && info[gr.gates[a]].cnot) ++a;
+      while (b > a && info[gr.gates[b - 1]].cnot) --b;
+      for (size_t i = a; i < b; ++i) cost += info[gr.gates[i]].cnot ? 1 : 0;
+    }
+    return cost;
+  };
+  auto make_segments = [&](const std::vector<int>& pgates) {
+    std::vector<uint8_t> st2(G, 1);
+    for (int g : pgates) st2[g] = 0;
+    std::vector<Group> folded = greedy_groups(pgates, info, R, 0u, st2, true, opt.variants, opt.fold_thread_targets);
+    for (int g : pgates) st2[g] = 0;
+    std::vector<Group> free_ = greedy_groups(pgates, info, R, 0u, st2, false, opt.variants);
+    const int seg_cost = opt.segment_cost, cnot_cost = 1;
+    const int c_fold = (int)folded.size() * seg_cost + interior_cnots(folded) * cnot_cost;
+    const int c_free = (int)free_.size() * seg_cost + interior_cnots(free_) * cnot_cost;
+    return (c_free < c_fold) ? std::move(free_) : std::move(folded);
+  };
+  // Pass splitting (whole-state tiles): a JIT pass kernel is one straight-line
+  // function, and compile time grows with its segments (cfg3's 32 + 32
+  // segments: ~20 s of NVRTC on one core). Passes of more than
+  // max_pass_segments segments are cut into equal passes over the same local
+  // qubits, whose units compile in parallel; each cut costs a state round
+  // trip (measured: cuts down to 6 / 4 segments cost cfg3 25 % / 40 %, so the
+  // default only bounds the compile time of deep circuits).
+  if (opt.max_pass_segments > 0) {
+    std::vector<Group> cut;
+    for (Group& pg : passes) {
+      const std::vector<Group> sg = make_segments(pg.gates);
+      if ((int)sg.size() <= opt.max_pass_segments) {
+        cut.push_back(pg);
+        continue;
+      }
+      const int parts = ((int)sg.size() + opt.max_pass_segments - 1) / opt.max_pass_segments;
+      const int per = ((int)sg.size() + parts - 1) / parts;
+      for (size_t i = 0; i < sg.size(); i += (size_t)per) {
+        Group sub;
+        sub.mask = pg.mask;
+        for (size_t j = i; j < sg.size() && j < i + (size_t)per; ++j)
+          sub.gates.insert(sub.gates.end(), sg[j].gates.begin(), sg[j].gates.end());
+        cut.push_back(std::move(sub));
+      }
+    }
+    passes.swap(cut);
+  }
+
   for (size_t pi = 0; pi < passes.size(); ++pi) {
     Group& pg = passes[pi];
     // pad the local set to exactly k qubits (lowest unused first)
@@ -390,35 +445,7 @@ std::string build_program(const std::vector<GateIn>& gates, int n, int64_t total
     pd.blk_begin = (int)P->blocks.size();
     pd.av_begin = P->n_av;
 
-    // ---- level 2: register segments inside the tile ----
-    // Two policies, priced per pass: segments shaped [CNOTs][body][CNOTs]
-    // (every CNOT folds into address maps, but more segments), or free
-    // placement (interior CNOTs become register permutations). A segment
-    // boundary costs a shared-memory round trip of the tile; an interior
-    // CNOT a few dozen register moves/selects per thread.
-    auto interior_cnots = [&](const std::vector<Group>& gs) {
-      int cost = 0;
-      for (const Group& gr : gs) {
-        size_t a = 0, b = gr.gates.size();
-        while (a < b && info[gr.gates[a]].cnot) ++a;
-        while (b > a && info[gr.gates[b - 1]].cnot) --b;
-        for (size_t i = a; i < b; ++i) cost += info[gr.gates[i]].cnot ? 1 : 0;
-      }
-      return cost;
-    };
-    std::vector<Group> segs;
-    {
-      std::vector<uint8_t> st2(G, 1);
-      for (int g : pg.gates) st2[g] = 0;
-      std::vector<Group> folded = greedy_groups(pg.gates, info, R, 0u, st2, true, opt.variants,
-                                                opt.fold_thread_targets);
-      for (int g : pg.gates) st2[g] = 0;
-      std::vector<Group> free_ = greedy_groups(pg.gates, info, R, 0u, st2, false, opt.variants);
-      const int seg_cost = opt.segment_cost, cnot_cost = 1;
-      const int c_fold = (int)folded.size() * seg_cost + interior_cnots(folded) * cnot_cost;
-      const int c_free = (int)free_.size() * seg_cost + interior_cnots(free_) * cnot_cost;
-      segs = (c_free < c_fold) ? std::move(free_) : std::move(folded);
-    }
+    std::vector<Group> segs = make_segments(pg.gates);
     if (!pg.gates.empty() && segs.empty()) return "segment scheduling failed";
 
     struct Item {

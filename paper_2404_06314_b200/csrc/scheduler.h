@@ -25,6 +25,7 @@ struct ScheduleOptions {
   int segment_cost = 4;      // price of a segment boundary in interior-CNOT units
   int variants = 1;          // greedy restarts per group (refuse the first v new-qubit requests)
   bool fold_thread_targets = false;  // boundary CNOTs may target thread bits (JIT HBM plans)
+  int max_pass_segments = 0;  // cut passes of more segments into several over the same local qubits (0: never)
   bool skip_dead_unapply = true;  // adjoint sweep: no un-apply for the first 1q operation on a qubit
   bool group_sync = false;   // plan thread-index bits for thread-group barriers (JIT HBM plans)
 };

@@ -289,6 +289,8 @@ int sim_run(int n, int64_t G, const int64_t* kinds, const int64_t* q0, const int
   {
     const char* ft = getenv("VQC_FOLD_THREAD_TARGETS");
     opt.fold_thread_targets = n > smem_max_qubits && !(ft && ft[0] == '0');
+    const char* ps = getenv("VQC_PASS_SEGMENTS");  // pass splitting (whole-state tiles), as the engine
+    if (ps && n <= 12 && n > smem_max_qubits) opt.max_pass_segments = atoi(ps);
     const char* gs = getenv("VQC_GROUP_SYNC");  // thread-group barriers, as JIT HBM plans
     opt.group_sync = n > smem_max_qubits && !(gs && gs[0] == '0');
   }

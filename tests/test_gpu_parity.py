@@ -354,6 +354,27 @@ def test_schedule_variants_cfg4_rows(torch_cuda, monkeypatch, knobs):
     assert close(res.gradients["w"], g["jac_w"]) < TOL
 
 
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_whole_state_tile_cut_into_passes(torch_cuda, monkeypatch, cfg):
+    """VQC_PASS_SEGMENTS cuts a whole-state tile's single pass into several
+    (the compile-time bound for deep circuits, default 48 segments): cfg2
+    (forward and adjoint sweeps in one program, 8 qubits) and cfg3 (separate
+    forward program, 12 qubits) on 3-segment passes against the goldens."""
+    from paper_2404_06314_b200 import configs
+    monkeypatch.setenv("VQC_PASS_SEGMENTS", "3")
+    g = _golden(f"cfg{cfg}.npz")
+    spec = configs.CONFIGS[cfg]
+    circ, obs, wrt = configs.build(spec, configs.native_api())
+    eng = _engine()
+    res = eng.run_batch(_request(circ, obs, {"w": g["w"]}, g["x_rows"], wrt))
+    plan, _ = eng.plans.get(circ, obs, tuple(wrt), eng.device)
+    import json
+    assert json.loads(plan.describe())["passes"] > 2
+    assert close(res.expectations, g["expect"]) < TOL
+    for k in wrt:
+        assert close(res.gradients[k], g["jac_" + k]) < TOL
+
+
 def test_hbm_chunking_is_bitwise_invariant(torch_cuda, monkeypatch):
     """Row chunking (state budget) must not change any per-row result."""
     from paper_2404_06314_b200 import configs

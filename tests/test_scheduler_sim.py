@@ -162,3 +162,22 @@ def test_schedule_is_compact_for_cfg4(sim):
     passes, segments = int(stats[0]), int(stats[1])
     assert passes <= 3 * spec.layers, passes
     assert segments <= 8 * spec.layers * 3, segments
+
+
+def test_pass_splitting_of_whole_state_tiles(sim, monkeypatch):
+    """Whole-state tiles (n <= 12 on the pass kernels) cut passes of more than
+    VQC_PASS_SEGMENTS segments into several passes over the same qubits (a
+    bound on the JIT compile time of deep circuits): same results, more
+    passes, every structural invariant still checked by the simulator."""
+    spec = configs.CONFIGS[3]
+    circ, obs, wrt = configs.build(spec, configs.native_api())
+    x, w = configs.inputs_and_weights(spec, batch=1)
+    e_ref, j_ref = oracle_batch(circ, obs, {"w": w}, x, wrt)
+    flat = _flat_row(circ, {"w": w}, x[0])
+    kw = {"tile_qubits": 12, "smem_max": 7, "reg_slots": 3}
+    _, _, stats_one, _ = run_sim(sim, circ, obs, flat, wrt, **kw)
+    monkeypatch.setenv("VQC_PASS_SEGMENTS", "5")
+    e, jac, stats_cut, layout = run_sim(sim, circ, obs, flat, wrt, **kw)
+    assert stats_one[0] == 1 and stats_cut[0] > 4          # passes
+    full = np.concatenate([j_ref[n][0] for n, _, _ in layout.slices], axis=1)
+    assert close(e, e_ref[0]) < 1e-12 and close(jac, full) < 1e-12
