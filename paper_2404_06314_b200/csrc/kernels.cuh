@@ -1103,7 +1103,7 @@ __device__ __forceinline__ void group_sync(int t) {
 
 // segment end with a group barrier: register store through the folded store
 // map, then the barrier the next segment's loads need (sd.sync_st top bits
-// shared). Gradient partials are reduced per warp (warp_reduce_store), so no
+// shared). Gradient partials are reduced per warp (wr_split / wr_join), so no
 // reduction phases follow.
 template <int R, int MODE, class SD>
 __device__ __forceinline__ void seg_end_g(const SegEnv& E, const SD& sd, const Regs<R>& a, const Regs<R>& f) {
@@ -1207,35 +1207,13 @@ __device__ __forceinline__ void seg_end_io(const SegEnv& E, const SD& sd, const 
 // at lane bit B the lanes with the bit clear keep the lower half of the
 // values and send the upper half to their partner (and vice versa), so after
 // the five steps each value's total sits in the lanes of one group; values
-// beyond nv (padding of odd halves) are zero. The representative lane writes
-// dst[index]. 2 * (N/2 + N/4 + ...) + ... shuffles instead of 5 per value.
-template <int N, int BIT>
-__device__ __forceinline__ void warp_reduce_rec(const double (&v)[N], unsigned lane, int base, int nv, double* dst) {
-  if constexpr (BIT < 0) {
-    static_assert(N == 1, "at most 32 values per warp reduction");
-    if (nv > 0) dst[base] = v[0];
-  } else if constexpr (N == 1) {
-    double x[1] = {v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1 << BIT)};
-    // all lanes of the pair hold the same total; the one with the bit clear goes on
-    warp_reduce_rec<1, BIT - 1>(x, lane, base, ((lane >> BIT) & 1u) ? 0 : nv, dst);
-  } else {
-    constexpr int H = (N + 1) / 2;
-    const bool up = ((lane >> BIT) & 1u) != 0u;
-    double w[H];
-#pragma unroll
-    for (int i = 0; i < H; ++i) {
-      const double lo = v[i], hi = (i + H < N) ? v[i + H] : 0.0;
-      const double send = up ? lo : hi, keep = up ? hi : lo;
-      w[i] = keep + __shfl_xor_sync(0xffffffffu, send, 1 << BIT);
-    }
-    const int nlo = nv < H ? nv : H;
-    warp_reduce_rec<H, BIT - 1>(w, lane, base + (up ? H : 0), up ? nv - nlo : nlo, dst);
-  }
-}
-// The same reduction in stages the JIT weaves between a segment's gate
-// blocks, so each round's shuffle latency hides behind FP64 work instead of
-// stalling the warp five times: wr_split sends this round's halves (base / nv
-// track which value indices the lane still holds), wr_join adds what arrived.
+// beyond nv (padding of odd halves) are zero and the lane whose lower bits
+// are clear writes dst[index]: 2 * (N/2 + N/4 + ...) shuffles instead of 5
+// per value.
+// It runs in stages the JIT weaves between a segment's gate blocks, so each
+// round's shuffle latency hides behind FP64 work instead of stalling the warp
+// five times: wr_split sends this round's halves (base / nv track which value
+// indices the lane still holds), wr_join adds what arrived.
 template <int N, int BIT>
 __device__ __forceinline__ void wr_split(const double (&v)[N], unsigned lane, double (&keep)[(N + 1) / 2],
                                          double (&recv)[(N + 1) / 2], int& base, int& nv) {
@@ -1262,23 +1240,6 @@ template <int H>
 __device__ __forceinline__ void wr_join(const double (&keep)[H], const double (&recv)[H], double (&w)[H]) {
 #pragma unroll
   for (int i = 0; i < H; ++i) w[i] = keep[i] + recv[i];
-}
-
-// dst: this warp's slots [0, N) of the pass-wide partial table
-template <int N>
-__device__ __forceinline__ void warp_reduce_store(const double (&v)[N], double* dst) {
-  const unsigned lane = vtid() & 31u;
-  if constexpr (N <= 16) {
-    warp_reduce_rec<N, 4>(v, lane, 0, N, dst);
-  } else {
-    double a[16], b[N - 16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) a[i] = v[i];
-#pragma unroll
-    for (int i = 16; i < N; ++i) b[i - 16] = v[i];
-    warp_reduce_rec<16, 4>(a, lane, 0, 16, dst);
-    warp_reduce_store<N - 16>(b, dst + 16);
-  }
 }
 
 // inner products into per-thread partials (both states in registers)
