@@ -1250,6 +1250,49 @@ __device__ __forceinline__ void jop_ip3w(const Regs<R>& a, const Regs<R>& f, dou
   auto rf = [&](int i) { return f[i]; };
   ip_xyz<R, S, -1>(ra, rf, ix, iy, iz);
 }
+// Im<phi|X,Y,Z|psi> on every slot of MASK at once (a set of fused blocks):
+// the Z products Im(conj(phi_i) psi_i) are the same for every slot, which
+// only signs them differently, so they are formed once (2 FP64 ops per
+// element) and each slot's Z sum costs adds instead of its own 4 products
+// per pair. pr: 3 values per slot of MASK in slot order.
+template <int R, int MASK>
+__device__ __forceinline__ void jop_ip3w_set(const Regs<R>& a, const Regs<R>& f, double* pr) {
+  constexpr int N = 1 << R;
+  real_t d[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) d[i] = fma(f[i].x, a[i].y, -(f[i].y * a[i].x));
+  int k = 0;
+#pragma unroll
+  for (int s = 0; s < R; ++s) {
+    if (!((MASK >> s) & 1)) continue;
+    real_t ax[2] = {0, 0}, ay[2] = {0, 0}, z0 = 0, z1 = 0;
+    int c = 0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      if ((i >> s) & 1) {
+        z1 += d[i];
+        continue;
+      }
+      z0 += d[i];
+      const int j = i | (1 << s);
+      const cplx_t f0 = f[i], f1 = f[j], p0 = a[i], p1 = a[j];
+      ax[c] = fma(f0.x, p1.y, ax[c]);
+      ax[c] = fma(-f0.y, p1.x, ax[c]);
+      ax[c] = fma(f1.x, p0.y, ax[c]);
+      ax[c] = fma(-f1.y, p0.x, ax[c]);
+      ay[c] = fma(-f0.x, p1.x, ay[c]);
+      ay[c] = fma(-f0.y, p1.y, ay[c]);
+      ay[c] = fma(f1.x, p0.x, ay[c]);
+      ay[c] = fma(f1.y, p0.y, ay[c]);
+      c ^= 1;
+    }
+    pr[3 * k] = (double)(ax[0] + ax[1]);
+    pr[3 * k + 1] = (double)(ay[0] + ay[1]);
+    pr[3 * k + 2] = (double)(z0 - z1);
+    ++k;
+  }
+}
+
 template <int R, int KIND, int S>
 __device__ __forceinline__ double jop_ipxyw(const Regs<R>& a, const Regs<R>& f) {
   auto ra = [&](int i) { return a[i]; };

@@ -26,7 +26,7 @@ def test_hbm_plan_has_one_kernel_pair_per_pass():
     # every fused set of cfg4 is emitted with compile-time slots
     # adjoint schedule: 3 register slots, both states per thread
     # gradient partials per thread, reduced per warp; thread-group barriers
-    assert "jop_u2<R, MODE_FWD, 0, true>(f, f, T, " in src and "jop_ip3w<R, 2>(a, f, pr[6], pr[7], pr[8]);" in src
+    assert "jop_u2<R, MODE_FWD, 0, true>(f, f, T, " in src and "jop_ip3w_set<R, 7>(a, f, pr + 0);" in src
     assert "wr_split<9, 4>(q0_v, wl_, " in src and "seg_end_g<R, MODE>" in src and "wred_outputs(E, jb0_out" in src
     assert "vqc::KM_DUAL" in src
     assert "exec_op" not in src
