@@ -937,6 +937,14 @@ int64_t vqc_jit_source(const VqcCircuit* c, const int64_t* wrt_col, int compile,
   prog.pingpong = prog.hbm ? std::max(0, std::min(2, env_int("VQC_PINGPONG", 0))) : 0;
   prog.warp_red = use_warp_red(prog);
   prog.direct_io = prog.hbm && prog.group_sync && prog.pingpong == 0 && env_int("VQC_DIRECT_IO", 0) != 0;
+  if (env_int("VQC_JIT_SOURCE_TERMS", 0) != 0) {  // per-qubit <Z_i> as compile-time terms (CPU compile checks)
+    for (int q = 0; q < prog.n; ++q) {
+      prog.obs_mask.push_back(1u << q);
+      prog.obs_coeff.push_back(1.0 + 0.125 * q);
+      prog.obs_offs.push_back(q);
+    }
+    prog.obs_offs.push_back(prog.n);
+  }
   build_thr_table(prog.segs);  // per-segment thread-table offsets, as at plan creation
   const bool split = use_split(prog.n, prog.R) && !prog.adj_dual;
   const std::string src = jit_source(prog, split);
@@ -1109,6 +1117,12 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
               fr = std::max(3, std::min(5, env_int("VQC_FWD_REG", P.n <= kPassFusedMaxQubits ? P.R : kHbmForwardRegs)));
     const bool sep = P.hbm && (ft != P.k || fr != P.R);
     p->prog.jit_kernels = sep ? 2 : 3;
+    // Z-string observables become compile-time constants of the observing pass
+    if (!p->has_xy && env_int("VQC_CONST_TERMS", 1) != 0) {
+      p->prog.obs_mask = p->smask;
+      p->prog.obs_coeff = p->tcoeff;
+      p->prog.obs_offs = p->term_offs;
+    }
     std::string main_err;
     std::thread main_build([&]() {
       cudaSetDevice(p->device);
@@ -1144,6 +1158,9 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
       }
       fill_dev(p, f->prog, f->tabs, f->D);
       f->prog.jit_kernels = 1;
+      f->prog.obs_mask = p->prog.obs_mask;
+      f->prog.obs_coeff = p->prog.obs_coeff;
+      f->prog.obs_offs = p->prog.obs_offs;
       err = jit_build(f->prog, false, &f->jit);
       if (!err.empty()) {
         main_build.join();

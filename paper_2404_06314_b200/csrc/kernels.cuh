@@ -1372,8 +1372,10 @@ __device__ __forceinline__ void jred_phase2(const SegEnv& E, const SD& sd, int f
 // outputs go to A.ip (rows relative to A.b0, times n_tiles). Threads with
 // active == false only take part in the barriers.
 struct RtPassMap;  // pass index maps (defined with the tile walk below)
+struct RtTerms;  // observable terms read at run time (skeleton.cuh)
 struct InterpSegs {
   using PM = RtPassMap;
+  using Terms = RtTerms;
   // tiles always staged through shared memory
   static constexpr bool kDioF = false, kDioB = false, kDioFL = false, kDioFS = false, kDioBL = false, kDioBS = false;
   template <int R, int MODE>

@@ -41,6 +41,12 @@ struct HostProgram {
   bool group_sync = false;    // thread-index bits planned for thread-group barriers (ScheduleOptions)
   int jit_kernels = 3;        // HBM pass kernels to build: bit 0 forward, bit 1 adjoint (a plan with a
                               // separate forward schedule needs one kind from each program)
+  // Z-string observables as compile-time constants of the JIT pass kernels
+  // (term masks, coefficients, term_offs): the expectation / seed loops of the
+  // observing pass unroll and their sign bits fold (empty: generic loops)
+  std::vector<uint32_t> obs_mask;
+  std::vector<double> obs_coeff;
+  std::vector<int32_t> obs_offs;  // M + 1
   bool direct_io = false;     // JIT HBM passes: first / last segment of a sweep exchange registers with HBM directly
   bool warp_red = false;      // JIT HBM adjoint: per-warp reductions, gradients written at the end of the pass
   int max_ipout_per_seg = 0;

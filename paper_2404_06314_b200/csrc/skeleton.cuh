@@ -63,13 +63,23 @@ __device__ __forceinline__ void add_at(double (&v)[E], uint32_t h, double x) {
     if (h == (uint32_t)i) v[i] += x;
 }
 
+// Observable terms known at compile time (JIT pass kernels emit a struct with
+// the same members and kConst = true); RtTerms: read from shared memory.
+struct RtTerms {
+  static constexpr bool kConst = false;
+  static constexpr int T = 0, M = 0;
+  __device__ static constexpr uint32_t mask(int) { return 0u; }
+  __device__ static constexpr double coeff(int) { return 0.0; }
+  __device__ static constexpr int off(int) { return 0; }
+};
+
 // Expectations (observables.py / _kernels.py:182-198, Z strings) and the
 // adjoint seed phi = w(j) psi with w = sum_m u_m O_m(j) (VJP) or O_bra(j)
 // (_kernels.py:209-217). Each thread owns `count` tile elements; a term's
 // sign over them is parity(base & s) ^ parity(i & h), h bit b =
 // parity(hi[b] & s), so no per-element index arithmetic is needed.
 // E: elements per thread (compile time; equals the tile walk's count)
-template <bool DUAL, int E, class PM = RtPassMap>
+template <bool DUAL, int E, class PM = RtPassMap, class TMS = RtTerms>
 __device__ __forceinline__ void observe(const DevProgram& D, const RunArgs& A, const PassDesc* pd, cplx_t* s_psi,
                                         cplx_t* s_phi, const double* s_u_row, const TermSm* s_terms,
                                         const Group& grp, double* s_red, double* s_fin, uint32_t tile_base, int k,
@@ -97,11 +107,26 @@ __device__ __forceinline__ void observe(const DevProgram& D, const RunArgs& A, c
         p2[i] = xr * xr + xi * xi;
       }
     }
-    for (int m = 0; m < D.M; ++m) s_red[m * (int)vdim() + vtid()] = 0.0;
     double wh[E];
 #pragma unroll
     for (int i = 0; i < E; ++i) wh[i] = p2[i];
     wht<E>(wh);
+    if constexpr (TMS::kConst) {
+      // constant masks: h and the pick fold, one accumulator and store per observable
+#pragma unroll
+      for (int m = 0; m < TMS::M; ++m) {
+        double acc = 0.0;
+#pragma unroll
+        for (int t = TMS::off(m); t < TMS::off(m + 1); ++t) {
+          uint32_t p0, h;
+          term_bits(TMS::mask(t), p0, h);
+          const double v = pick<E>(wh, h);
+          acc += TMS::coeff(t) * (p0 ? -v : v);
+        }
+        s_red[m * (int)vdim() + vtid()] = acc;
+      }
+    } else {
+    for (int m = 0; m < D.M; ++m) s_red[m * (int)vdim() + vtid()] = 0.0;
     for (int t = 0; t < D.T; ++t) {
       const TermSm ts = s_terms[t];
       if (ts.xmask != 0u) continue;
@@ -109,6 +134,7 @@ __device__ __forceinline__ void observe(const DevProgram& D, const RunArgs& A, c
       term_bits(ts.mask, p0, h);
       const double v = pick<E>(wh, h);
       s_red[ts.obs * (int)vdim() + vtid()] += ts.coeff * (p0 ? -v : v);
+    }
     }
     if (D.has_xy) {
       // X/Y strings (on-chip states only): Re sum_j conj(psi_j) i^k (-1)^{popc((j^x)&s)} psi_{j^x}
@@ -154,6 +180,19 @@ __device__ __forceinline__ void observe(const DevProgram& D, const RunArgs& A, c
       double w[E];
 #pragma unroll
       for (int i = 0; i < E; ++i) w[i] = 0.0;
+      if constexpr (TMS::kConst) {
+#pragma unroll
+        for (int m = 0; m < TMS::M; ++m) {
+          const double um = seed_mode == 1 ? s_u_row[m] : (m == bra ? 1.0 : 0.0);
+#pragma unroll
+          for (int t = TMS::off(m); t < TMS::off(m + 1); ++t) {
+            uint32_t p0, h;
+            term_bits(TMS::mask(t), p0, h);
+            const double e = um * TMS::coeff(t);
+            add_at<E>(w, h, p0 ? -e : e);
+          }
+        }
+      } else {
       for (int t = 0; t < D.T; ++t) {
         const TermSm ts = s_terms[t];
         if (ts.xmask != 0u) continue;
@@ -162,6 +201,7 @@ __device__ __forceinline__ void observe(const DevProgram& D, const RunArgs& A, c
         uint32_t p0, h;
         term_bits(ts.mask, p0, h);
         add_at<E>(w, h, p0 ? -e : e);
+      }
       }
       wht<E>(w);  // w[i] = sum_h (-1)^{popc(i & h)} (per-h sums)
 #pragma unroll
@@ -452,7 +492,7 @@ __device__ __forceinline__ void pass_body(const DevProgram& D, const RunArgs& A)
     for_tile<OBS_E>(tw, [&](uint32_t sw, uint32_t j) { dst[j] = s_psi[sw]; });
   }
   if (flags & (F_OBSERVE | F_SEED)) {
-    observe<ADJ, OBS_E, PM>(D, A, pd, s_psi, s_phi, s_up, s_terms, grp, s_red, s_fin, tile_base, k, bl, (flags & F_OBSERVE) != 0,
+    observe<ADJ, OBS_E, PM, typename SEGS::Terms>(D, A, pd, s_psi, s_phi, s_up, s_terms, grp, s_red, s_fin, tile_base, k, bl, (flags & F_OBSERVE) != 0,
                  (flags & F_SEED) ? (A.bra < 0 ? 1 : 2) : 0, A.bra, tile, n_tiles);
     vsync();
   }

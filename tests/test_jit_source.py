@@ -77,6 +77,18 @@ def test_whole_state_tile_plan_for_12_qubits(monkeypatch):
     assert "__launch_bounds__(512, 1) vqc_jit_pa0" in src and "seg_end_g<R, MODE>" in src and "wr_split<" in src
 
 
+def test_constant_observable_terms_compile(monkeypatch):
+    """Z-string observables as compile-time constants of the observing pass
+    (skeleton.cuh observe<..., TMS>): the unrolled expectation / seed loops
+    compile for sm_100a."""
+    monkeypatch.setenv("VQC_JIT_CACHE", "0")
+    monkeypatch.setenv("VQC_JIT_SOURCE_TERMS", "1")
+    from test_scheduler_sim import _random
+    circ, _, _ = _random(np.random.default_rng(11), 13, 40)
+    src, secs = _src(circ, ("a", "b", "s"), compile=True)
+    assert secs is not None and "static constexpr bool kConst = true" in src and "using Terms = TM" in src
+
+
 def test_cubin_cache_round_trip(tmp_path, monkeypatch):
     """The on-disk cubin cache returns what NVRTC produced (second call reads)."""
     monkeypatch.setenv("VQC_JIT_CACHE", str(tmp_path))
