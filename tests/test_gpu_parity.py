@@ -375,6 +375,32 @@ def test_whole_state_tile_cut_into_passes(torch_cuda, monkeypatch, cfg):
         assert close(res.gradients[k], g["jac_" + k]) < TOL
 
 
+@pytest.mark.parametrize("n", [9, 13])
+@pytest.mark.parametrize("terms", [7, 70])
+def test_many_term_observables(torch_cuda, n, terms):
+    """Z-string observables are compile-time constants of the observing pass
+    up to 64 terms; beyond that (70 here) the kernels read them from shared
+    memory. Both against the oracle, Jacobians and a row-dependent VJP."""
+    from paper_2404_06314_b200.observables import Observable
+    rng = np.random.default_rng(1000 + n + terms)
+    circ, trainable = _rand_circuit(rng, n, 30 + 4 * n)
+    def zterms(k):
+        return tuple((float(rng.uniform(-2, 2)), "".join("Z" if rng.random() < 0.4 else "I" for _ in range(n)))
+                     for _ in range(k))
+    obs = [Observable(zterms(terms)), Observable(zterms(2))]
+    x = rng.uniform(-2, 2, (5, 4))
+    wrt = ("a", "b", "s")
+    e_ref, j_ref = oracle_batch(circ, obs, trainable, x, wrt)
+    res = _engine().run_batch(_request(circ, obs, trainable, x, wrt))
+    assert close(res.expectations, e_ref) < TOL
+    for k in wrt:
+        assert close(res.gradients[k], j_ref[k]) < TOL
+    up = rng.uniform(-1, 1, (len(x), len(obs)))
+    e, rows, _ = _vjp_device(torch_cuda, _engine(), circ, obs, wrt, trainable, x, up)
+    ref_rows = np.concatenate([np.einsum("bm,bmp->bp", up, j_ref[k]) for k in wrt], axis=1)
+    assert close(e, e_ref) < TOL and close(rows, ref_rows) < TOL
+
+
 def test_hbm_chunking_is_bitwise_invariant(torch_cuda, monkeypatch):
     """Row chunking (state budget) must not change any per-row result."""
     from paper_2404_06314_b200 import configs
