@@ -338,6 +338,7 @@ struct ProgDev {
 };
 
 struct VqcPlan {
+  int circuit_qubits = 0;  // the circuit's own qubit count (the plan may hold idle qubits, VQC_PAD_QUBITS)
   int device = 0;
   int sms = 148;
   HostProgram prog;
@@ -1022,6 +1023,7 @@ int vqc_plan_create(const VqcCircuit* c, const VqcObservables* obs, const int64_
   p->enc_off = c->enc_offset;
   p->enc_size = c->enc_size;
   p->M = (int)obs->n_obs;
+  p->circuit_qubits = c->n_qubits;
   p->term_offs.assign((size_t)p->M + 1, 0);
   const uint32_t nmask = c->n_qubits >= 32 ? 0xffffffffu : ((1u << c->n_qubits) - 1u);
   for (int m = 0; m < p->M; ++m) {
@@ -1214,14 +1216,16 @@ int64_t vqc_plan_describe(const VqcPlan* p, char* buf, int64_t cap) {
                            "\"passes\": %d, \"segments\": %d, \"rotations\": %d, \"grad_slots\": %d, "
                            "\"fwd_ops\": %d, \"bwd_ops\": %d, \"cols\": %d, \"obs\": %d, \"jit\": %s, "
                            "\"jit_compile_s\": %.3f, \"jit_cubin_bytes\": %zu, \"absorbed_gates\": %d, \"adjoint_dual\": %s, "
-                           "\"fwd_tile_qubits\": %d, \"fwd_reg_slots\": %d, \"fwd_passes\": %d, \"precision\": \"%s\", \"pingpong\": %d}",
+                           "\"fwd_tile_qubits\": %d, \"fwd_reg_slots\": %d, \"fwd_passes\": %d, \"precision\": \"%s\", \"pingpong\": %d, "
+                           "\"circuit_qubits\": %d, \"thread_group_barriers\": %s, \"warp_reductions\": %s}",
                            P.n, P.hbm ? "hbm" : "smem", P.k, P.R, (int)P.passes.size(), nseg, P.n_rot,
                            P.NG, P.n_fwd_ops, P.n_bwd_ops, P.n_cols, p->M, p->use_jit ? "true" : "false",
                            p->jit.compile_s + (p->fwd ? p->fwd->jit.compile_s : 0.0),
                            p->jit.cubin_bytes + (p->fwd ? p->fwd->jit.cubin_bytes : 0), P.absorbed,
                            P.adj_dual ? "true" : "false", p->fwd ? p->fwd->prog.k : P.k,
                            p->fwd ? p->fwd->prog.R : P.R, (int)(p->fwd ? p->fwd->prog.passes.size() : P.passes.size()),
-                           P.precision == 1 ? "complex64" : "complex128", P.pingpong);
+                           P.precision == 1 ? "complex64" : "complex128", P.pingpong, p->circuit_qubits,
+                           P.group_sync ? "true" : "false", P.warp_red ? "true" : "false");
   if (buf && cap > 0) {
     const int64_t c = std::min<int64_t>(cap - 1, len);
     memcpy(buf, tmp, (size_t)c);
