@@ -1086,18 +1086,34 @@ __device__ __forceinline__ void seg_end(const SegEnv& E, const SD& sd, const Reg
 // Thread-group barriers and per-warp reductions (JIT HBM pass kernels; the
 // scheduler's assign_thread_groups plans the thread-index bits).
 //
-// group_sync(t): barrier over the blockDim >> t threads that share the top t
-// thread-index bits (t = 0: the CTA; a warp or less: __syncwarp). Named
-// barriers 2^t - 1 + group index (levels 1..3 use ids 1..14).
-__device__ __forceinline__ void group_sync(int t) {
-  const unsigned g = vdim() >> t;
-  if (t <= 0) {
+// group_sync_t<T, NTHR>: barrier over the 2^NTHR >> T threads that share the top T
+// thread-index bits (T = 0: the CTA; a warp or less: __syncwarp). Named
+// barriers 2^T - 1 + group index (levels 1..3 use ids 1..14).
+template <int T, int NTHR>
+__device__ __forceinline__ void group_sync_t() {
+  // T: compile-time level (the JIT's segment descriptors). Immediate barrier
+  // ids, and only those of this level: a register id makes ptxas reserve all
+  // 16 named barriers, which caps the resident CTAs per SM at 4.
+  if constexpr (T <= 0) {
     vsync();
-  } else if (g <= 32u) {
-    __syncwarp();
   } else {
-    const unsigned id = (1u << t) - 1u + vtid() / g;
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(g) : "memory");
+    constexpr unsigned g = (1u << NTHR) >> T;  // NTHR thread-index bits: the tile's threads
+    if constexpr (g <= 32u) {
+      __syncwarp();
+    } else if constexpr ((1 << T) > 4) {
+      // eight groups (512-thread tiles, one CTA per SM anyway): a register id
+      const unsigned id = (1u << T) - 1u + vtid() / g;
+      asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(g) : "memory");
+    } else {
+      const unsigned grp = vtid() / g;
+#define VQC_BAR_CASE(I)                                                       \
+  if constexpr ((I) < (1 << T)) {                                             \
+    if (grp == (I)) asm volatile("bar.sync %0, %1;" ::"n"((1 << T) - 1 + (I)), "r"(g) : "memory"); \
+  }
+      VQC_BAR_CASE(0) VQC_BAR_CASE(1) VQC_BAR_CASE(2) VQC_BAR_CASE(3) VQC_BAR_CASE(4) VQC_BAR_CASE(5) VQC_BAR_CASE(6)
+      VQC_BAR_CASE(7)
+#undef VQC_BAR_CASE
+    }
   }
 }
 
@@ -1109,7 +1125,7 @@ template <int R, int MODE, class SD>
 __device__ __forceinline__ void seg_end_g(const SegEnv& E, const SD& sd, const Regs<R>& a, const Regs<R>& f) {
   constexpr int N = 1 << R;
   const Group& grp = E.grp;
-  if (sd.st_sync()) group_sync(sd.sync_self());  // the group's loads are done before its cells are overwritten
+  if (sd.st_sync()) group_sync_t<SD::sync_self(), SD::nthr()>();  // the group's loads are done before its cells are overwritten
   asm volatile("" ::: "memory");
   uint32_t sp0, sc[R];
   sp0 = SD::thr_sp0((uint32_t)grp.gi & ((1u << sd.nthr()) - 1u));
@@ -1127,7 +1143,7 @@ __device__ __forceinline__ void seg_end_g(const SegEnv& E, const SD& sd, const R
     E.own[ad] = a[i];
     if constexpr (MODE == MODE_DUAL) E.s_phi[ad] = f[i];
   }
-  group_sync(sd.sync_st());
+  group_sync_t<SD::sync_st(), SD::nthr()>();
 }
 
 __device__ __forceinline__ void cp_async_wait_all_();
