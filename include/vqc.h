@@ -142,6 +142,15 @@ int64_t vqc_jit_source(const VqcCircuit* circuit, const int64_t* wrt_col, int co
 
 int64_t vqc_last_launch_count(void);
 
+/* SPSA direction draws for rows row0 .. row0 + rows - 1 of a batch (host
+ * arithmetic, no GPU): out (rows, samples, cols) receives +1 / -1, bit for
+ * bit the reference's 2 * rng.integers(0, 2, size=cols) - 1 per sample
+ * (gradients.py:180-201) with rng = numpy default_rng(mix_seed(seed, row))
+ * per row (batch.py:75-81, 197); per_row_seed == 0 draws every row from
+ * default_rng(seed) itself, the single-binding form (gradients.py:243-266). */
+int vqc_spsa_signs(uint64_t seed, int64_t row0, int64_t rows, int64_t samples, int64_t cols,
+                   int per_row_seed, int8_t* out);
+
 /* Per-kernel CUDA-event timing of this thread's launches (bench/profiling):
  * enable resets the totals; report synchronises pending events and writes
  * {"kernel": [total_ms, launches], ...} into buf, returning the JSON length. */

@@ -418,7 +418,8 @@ Layout make_layout(const VqcPlan* p, int64_t B, int mode) {
     const size_t per = (size_t)nstates * N * esz + (size_t)L.K * P.NG * L.n_tiles * 8 +
                        (size_t)M * L.n_tiles * 8;
     int64_t chunk = (int64_t)(p->state_budget / std::max<size_t>(per, 1));
-    chunk = std::max<int64_t>(1, std::min<int64_t>(chunk, B));
+    // rows are the grid's y dimension (at most 65535 per launch)
+    chunk = std::max<int64_t>(1, std::min<int64_t>({chunk, B, (int64_t)65535}));
     L.chunk = chunk;
     L.psi = take((size_t)chunk * N * esz);
     L.phi = take(adj ? (size_t)chunk * N * esz : 0);

@@ -377,7 +377,8 @@ class BatchEngine:
                 grads[n] += res.gradients[n]
         return BatchResult(expect, grads)
 
-    def forward_angle_rows(self, circuit: Circuit, observables, angles: np.ndarray) -> np.ndarray:
+    def forward_angle_rows(self, circuit: Circuit, observables, angles: np.ndarray,
+                           as_tensor: bool = False) -> np.ndarray:
         """Expectations (rows, M) of ``circuit`` with per-row rotation angles
         (rows, R): one GPU forward launch sequence over ``angle_circuit``.
         X/Y strings on HBM plans (n > 12) run one Z-basis launch per basis
@@ -390,12 +391,12 @@ class BatchEngine:
             for pattern, group_obs in basis_groups(observables, circuit.num_qubits):
                 if pattern not in cache:
                     cache[pattern] = basis_circuit(ac, pattern)
-                e = self._forward_rows(cache[pattern], group_obs, angles)
+                e = self._forward_rows(cache[pattern], group_obs, angles, as_tensor)
                 total = e if total is None else total + e
             return total
-        return self._forward_rows(ac, observables, angles)
+        return self._forward_rows(ac, observables, angles, as_tensor)
 
-    def _forward_rows(self, ac: Circuit, observables, angles) -> np.ndarray:
+    def _forward_rows(self, ac: Circuit, observables, angles, as_tensor: bool = False):
         import torch
         dev = self.device
         plan, _ = self.plans.get(ac, observables, (), dev)
@@ -408,17 +409,19 @@ class BatchEngine:
             expect = torch.empty((rows, M), dtype=torch.float64, device=dev)
             ws = self.workspace.get(plan.workspace_bytes(rows, native.VQC_MODE_FORWARD), dev)
             plan.forward(d_in, d_w, expect, ws, stream.cuda_stream)
-            return expect.cpu().numpy()
+            return expect if as_tensor else expect.cpu().numpy()
 
     def _run_shifted(self, request, circuit, observables, layout, flat, inputs,
-                     rng_for_row=None):
+                     rng_for_row=None, single_seed=None):
         """param-shift (gradients.py:137-160) and SPSA (gradients.py:180-201)
         as batched GPU forward evaluations. Each row's shifted / perturbed
         evaluations become extra rows of per-gate angles (computed on the host
         in the reference's arithmetic order), so a chunk of B rows is one
-        forward call over B*(1+2S) angle rows; the finite differences and the
-        chain rule through the angle expressions are host arithmetic in the
-        reference's accumulation order."""
+        forward call over B*(1+2S) angle rows. SPSA draws its directions
+        natively (vqc_spsa_signs, bit for bit numpy's per-row generators) and
+        forms its estimate on the device; param-shift's finite differences and
+        chain rule through the angle expressions are host arithmetic, both in
+        the reference's accumulation order."""
         import torch
         compiled = circuit.compiled()
         enc = encoding_set(circuit)
@@ -475,31 +478,43 @@ class BatchEngine:
                         grad[lo:hi, :, col] += occ * partial[:, None]
             else:
                 K, c, idx = request.spsa_samples, request.spsa_c, layout.flat_of_col
-                deltas = np.empty((n, K, C))
-                for i in range(n):
-                    rng = (rng_for_row(lo + i) if rng_for_row is not None
-                           else np.random.default_rng(
-                               mix_seed(request.seed, request.row_offset + lo + i)))
-                    for k in range(K):
-                        d = rng.integers(0, 2, size=C).astype(np.float64)
-                        deltas[i, k] = 2.0 * d - 1.0
+                if single_seed is not None:
+                    # single-binding form: default_rng(seed) itself for every row
+                    deltas = native.spsa_signs(single_seed, 0, n, K, C, per_row_seed=False
+                                               ).astype(np.float64)
+                elif rng_for_row is None:
+                    # the reference's per-row generators (default_rng(mix_seed(seed,
+                    # global row)), batch.py:197) and draws, natively on the host
+                    deltas = native.spsa_signs(request.seed, request.row_offset + lo, n, K, C
+                                               ).astype(np.float64)
+                else:
+                    deltas = np.empty((n, K, C))
+                    for i in range(n):
+                        rng = rng_for_row(lo + i)
+                        for k in range(K):
+                            d = rng.integers(0, 2, size=C).astype(np.float64)
+                            deltas[i, k] = 2.0 * d - 1.0
                 # perturbed flats and their angles on the device (same IEEE
                 # ops as the reference: base +/- (c * delta), then coeff * f1 * f2 ...)
                 d_flats = torch.from_numpy(flats).to(self.device)
                 d_idx = torch.from_numpy(idx).to(self.device)
-                d_cd = c * torch.from_numpy(deltas).to(self.device)     # (n, K, C)
+                d_delta = torch.from_numpy(deltas).to(self.device)      # (n, K, C)
+                d_cd = c * d_delta
                 pf = d_flats[:, None, :].repeat(1, per_row, 1)          # (n, 1+2K, P)
                 base = d_flats[:, None, d_idx]
                 pf[:, 1::2][:, :, d_idx] = base + d_cd
                 pf[:, 2::2][:, :, d_idx] = base - d_cd
                 ang = device_row_angles(compiled, pf.view(n * per_row, -1), rot)
-                e = self.forward_angle_rows(circuit, observables, ang).reshape(n, per_row, M)
-                expect[lo:hi] = e[:, 0]
-                g_acc = np.zeros((n, M, C))
+                e = self.forward_angle_rows(circuit, observables, ang, as_tensor=True).view(n, per_row, M)
+                # the estimate on the device: the reference's elementwise IEEE
+                # operations in its accumulation order (no fused multiply-add)
+                d_inv = 1.0 / ((2.0 * c) * d_delta)
+                g_acc = torch.zeros((n, M, C), dtype=torch.float64, device=self.device)
                 for k in range(K):
                     diff = e[:, 1 + 2 * k] - e[:, 2 + 2 * k]                # (n, M)
-                    g_acc += diff[:, :, None] * (1.0 / (2.0 * c * deltas[:, k]))[:, None, :]
-                grad[lo:hi] = g_acc / K
+                    g_acc += diff[:, :, None] * d_inv[:, k][:, None, :]
+                expect[lo:hi] = e[:, 0].cpu().numpy()
+                grad[lo:hi] = (g_acc / K).cpu().numpy()
         return expect, grad
 
 

@@ -102,8 +102,11 @@ def spsa_gradients(circuit: Circuit, binding, observables, wrt, c: float = DEFAU
     flat = eng.base_flat(req.circuit, req.trainable_values)
     if layout.n_cols == 0:
         return _batch_result(eng.run_batch(req), layout)
-    e, g = eng._run_shifted(req, req.circuit, req.observables, layout, flat, req.inputs,
-                            rng_for_row=lambda b: np.random.default_rng(seed))
+    if isinstance(seed, (int, np.integer)) and 0 <= int(seed) < 2 ** 64:
+        draws = {"single_seed": int(seed)}       # native draws (vqc_spsa_signs)
+    else:                                        # anything else default_rng accepts
+        draws = {"rng_for_row": lambda b: np.random.default_rng(seed)}
+    e, g = eng._run_shifted(req, req.circuit, req.observables, layout, flat, req.inputs, **draws)
     return _result(e[0], g[0], layout)
 
 

@@ -31,7 +31,7 @@ EXPORTED_SYMBOLS = (
     "vqc_plan_create", "vqc_plan_destroy", "vqc_plan_num_cols", "vqc_plan_num_obs",
     "vqc_plan_mode", "vqc_plan_describe", "vqc_workspace_bytes", "vqc_forward", "vqc_adjoint",
     "vqc_run_batch_host", "vqc_last_launch_count", "vqc_profile_enable", "vqc_profile_report",
-    "vqc_last_error", "vqc_abi_version", "vqc_jit_source",
+    "vqc_last_error", "vqc_abi_version", "vqc_jit_source", "vqc_spsa_signs",
 )
 
 
@@ -87,6 +87,9 @@ def load_library(path: str | None = None):
         lib.vqc_jit_source.restype = ctypes.c_int64
         lib.vqc_jit_source.argtypes = [ctypes.POINTER(VqcCircuit), _I64P, ctypes.c_int, ctypes.c_char_p,
                                        ctypes.c_int64, ctypes.POINTER(ctypes.c_double)]
+        lib.vqc_spsa_signs.restype = ctypes.c_int
+        lib.vqc_spsa_signs.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                       ctypes.c_int64, ctypes.c_int, _VP]
         lib.vqc_last_launch_count.restype = ctypes.c_int64
         lib.vqc_last_launch_count.argtypes = []
         lib.vqc_profile_enable.restype = None
@@ -244,6 +247,18 @@ def jit_source(compiled, wrt_col, enc_offset: int, enc_size: int, compile: bool 
     buf = ctypes.create_string_buffer(int(n) + 1)
     lib.vqc_jit_source(ctypes.byref(circ), keep[6].ctypes.data_as(_I64P), 0, buf, int(n) + 1, None)
     return buf.value.decode(), (secs.value if compile else None)
+
+
+def spsa_signs(seed: int, row0: int, rows: int, samples: int, cols: int,
+               per_row_seed: bool = True) -> np.ndarray:
+    """(rows, samples, cols) int8 of +-1: the reference's per-row SPSA draws
+    (numpy default_rng(mix_seed(seed, row)).integers(0, 2, size=cols) per
+    sample), generated natively on the host."""
+    out = np.empty((rows, samples, cols), np.int8)
+    _check(load_library().vqc_spsa_signs(int(seed) & 0xFFFFFFFFFFFFFFFF, int(row0), int(rows), int(samples),
+                                         int(cols), 1 if per_row_seed else 0, out.ctypes.data),
+           "vqc_spsa_signs")
+    return out
 
 
 def last_launch_count() -> int:

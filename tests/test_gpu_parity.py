@@ -440,6 +440,26 @@ def test_degenerate_shapes(torch_cuda):
     assert r.expectations.shape == (3, 0) and r.gradients["x"].shape == (3, 0, 4)
 
 
+def test_more_rows_than_one_grid_holds(torch_cuda):
+    """Pass kernels index rows with the grid's y dimension: a call of more
+    than 65535 rows runs in row chunks. Rows on both sides of the chunk
+    boundary equal the same inputs evaluated in a small batch (batch
+    invariance, reference tests/test_batch.py:107-132)."""
+    from paper_2404_06314_b200 import configs
+    spec = configs.CONFIGS[2]
+    circ, obs, wrt = configs.build(spec, configs.native_api())
+    x, w = configs.inputs_and_weights(spec, batch=64)
+    eng = _engine()
+    small = eng.run_batch(_request(circ, obs, {"w": w}, x, ("x",)))
+    B = 65535 + 700
+    big = eng.run_batch(_request(circ, obs, {"w": w}, np.tile(x, (B // 64 + 1, 1))[:B], ("x",)))
+    assert big.expectations.shape == (B, len(obs))
+    for lo in (0, 65535 - 31, B - 64):
+        idx = np.arange(lo, lo + 64) % 64
+        assert np.array_equal(big.expectations[lo:lo + 64], small.expectations[idx])
+        assert np.array_equal(big.gradients["x"][lo:lo + 64], small.gradients["x"][idx])
+
+
 def test_failing_input_reports_index(torch_cuda):
     """Per-row failure reporting (reference tests/test_batch.py:196-209): the
     reference wraps a failing row's exception in BatchInputError(index); on

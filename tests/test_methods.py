@@ -106,6 +106,34 @@ def test_spsa_is_a_directional_derivative():
         assert np.abs(spsa[b] - est / k).max() < 2e-3
 
 
+def test_native_spsa_signs_match_numpy():
+    """vqc_spsa_signs (host C++: SeedSequence + PCG64 + bounded draws) is bit
+    for bit numpy's default_rng(mix_seed(seed, row)).integers(0, 2, size=C)
+    per sample (batch.py:197, gradients.py:180-201), for one- and two-word
+    entropies, odd draw counts (the 32-bit half-word buffer carries over
+    between samples) and negative / oversized seeds (mix_seed wraps mod 2^64)."""
+    from paper_2404_06314_b200 import native
+    from paper_2404_06314_b200.engine import mix_seed
+    for seed in (0, 1, 20240406, 2**32 - 1, 2**32, 2**40 + 3, 2**64 - 1, -5, 2**70 + 9):
+        for row0 in (0, 7, 100000):
+            for K, C in ((1, 1), (1, 7), (3, 5), (2, 64)):
+                got = native.spsa_signs(seed, row0, 5, K, C)
+                assert got.shape == (5, K, C) and got.dtype == np.int8
+                for r in range(5):
+                    rng = np.random.default_rng(mix_seed(seed, row0 + r))
+                    for k in range(K):
+                        want = 2.0 * rng.integers(0, 2, size=C).astype(np.float64) - 1.0
+                        assert np.array_equal(got[r, k].astype(np.float64), want), (seed, row0, r, k)
+    # single-binding form: every row from default_rng(seed) itself
+    for seed in (0, 3, 2**33 + 1):
+        got = native.spsa_signs(seed, 0, 2, 3, 9, per_row_seed=False)
+        rng = np.random.default_rng(seed)
+        want = np.stack([2.0 * rng.integers(0, 2, size=9).astype(np.float64) - 1.0 for _ in range(3)])
+        assert np.array_equal(got[0].astype(np.float64), want)
+        assert np.array_equal(got[1], got[0])
+    assert native.spsa_signs(1, 0, 0, 1, 4).shape == (0, 1, 4)
+
+
 def test_angle_circuit_host_helpers(oracle_mod):
     """angle_circuit keeps gates and makes rotation r read angles[r]; row_angles
     equals the reference's compute_angles (oracle restatement)."""

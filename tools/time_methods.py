@@ -13,7 +13,8 @@ import torch  # noqa: E402
 from paper_2404_06314_b200 import configs  # noqa: E402
 from paper_2404_06314_b200.engine import BatchEngine, BatchRequest  # noqa: E402
 
-CASES = [(2, "param-shift", 1024), (2, "spsa", 1024), (3, "param-shift", 256), (4, "param-shift", 64)]
+CASES = [(2, "param-shift", 1024), (2, "spsa", 1024), (3, "param-shift", 256), (3, "spsa", 4096),
+         (4, "param-shift", 64), (4, "spsa", 1024)]
 
 eng = BatchEngine(device="cuda:0")
 for cfg_id, method, rows in CASES:
