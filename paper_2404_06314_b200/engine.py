@@ -419,9 +419,10 @@ class BatchEngine:
         in the reference's arithmetic order), so a chunk of B rows is one
         forward call over B*(1+2S) angle rows. SPSA draws its directions
         natively (vqc_spsa_signs, bit for bit numpy's per-row generators) and
-        forms its estimate on the device; param-shift's finite differences and
-        chain rule through the angle expressions are host arithmetic, both in
-        the reference's accumulation order."""
+        forms its estimate on the device in the reference's accumulation
+        order; param-shift's differences and chain rule through the angle
+        expressions run on the device too (one FP64 matrix product sums the
+        terms of a column)."""
         import torch
         compiled = circuit.compiled()
         enc = encoding_set(circuit)
@@ -446,6 +447,15 @@ class BatchEngine:
                     shifted.append(r)
                     partials.append((g, terms))
             per_row = 1 + 2 * len(shifted)
+            # flattened (slot, column, coefficient, other factors) terms for the
+            # device-side chain rule: other-factor lists padded with an index
+            # one past the flat vector (a column of ones)
+            t_slot = [s for s, (_, terms) in enumerate(partials) for _ in terms]
+            t_col = [col for _, terms in partials for col, _ in terms]
+            t_coeff = [float(compiled.coeff[g]) for g, terms in partials for _ in terms]
+            t_others = [others for _, terms in partials for _, others in terms]
+            width = max([len(o) for o in t_others], default=0)
+            t_pad = [list(o) + [flat.shape[0]] * (width - len(o)) for o in t_others]
         else:
             if request.spsa_samples < 1:
                 raise ValueError(f"spsa_samples must be >= 1, got {request.spsa_samples}")
@@ -466,16 +476,28 @@ class BatchEngine:
                     r = torch.as_tensor(shifted, device=base.device)
                     rows[:, j, r] = base[:, r] + 0.5 * np.pi
                     rows[:, j + 1, r] = base[:, r] - 0.5 * np.pi
-                e = self.forward_angle_rows(circuit, observables,
-                                            rows.view(n * per_row, -1)).reshape(n, per_row, M)
-                expect[lo:hi] = e[:, 0]
-                for s, (g, terms) in enumerate(partials):
-                    occ = 0.5 * (e[:, 1 + 2 * s] - e[:, 2 + 2 * s])    # (n, M)
-                    for col, others in terms:
-                        partial = np.full(n, compiled.coeff[g])
-                        for p in others:
-                            partial = partial * flats[:, p]
-                        grad[lo:hi, :, col] += occ * partial[:, None]
+                e = self.forward_angle_rows(circuit, observables, rows.view(n * per_row, -1),
+                                            as_tensor=True).view(n, per_row, M)
+                expect[lo:hi] = e[:, 0].cpu().numpy()
+                if t_slot:
+                    # occurrence values 0.5 (f+ - f-) per shifted slot, the
+                    # partial of each term's angle expression w.r.t. its
+                    # requested factor (coefficient times the other factors),
+                    # and the sum over the terms of a column as one FP64
+                    # matrix product with the 0/1 term-to-column matrix
+                    dev = e.device
+                    occ = 0.5 * (e[:, 1::2] - e[:, 2::2])                           # (n, S, M)
+                    partial = torch.tensor(t_coeff, dtype=torch.float64, device=dev).repeat(n, 1)
+                    if width:
+                        ext = torch.cat([torch.from_numpy(flats).to(dev),
+                                         torch.ones((n, 1), dtype=torch.float64, device=dev)], 1)
+                        pad = torch.tensor(t_pad, dtype=torch.int64, device=dev)    # (T, width)
+                        for u in range(width):
+                            partial = partial * ext[:, pad[:, u]]
+                    contrib = occ[:, torch.tensor(t_slot, device=dev)] * partial[:, :, None]   # (n, T, M)
+                    onehot = torch.zeros((len(t_col), C), dtype=torch.float64, device=dev)
+                    onehot[torch.arange(len(t_col), device=dev), torch.tensor(t_col, device=dev)] = 1.0
+                    grad[lo:hi] = torch.matmul(contrib.transpose(1, 2), onehot).cpu().numpy()  # (n, M, C)
             else:
                 K, c, idx = request.spsa_samples, request.spsa_c, layout.flat_of_col
                 if single_seed is not None:
