@@ -460,6 +460,24 @@ def test_more_rows_than_one_grid_holds(torch_cuda):
         assert np.array_equal(big.gradients["x"][lo:lo + 64], small.gradients["x"][idx])
 
 
+def test_more_rows_than_one_grid_holds_hbm_plan(torch_cuda):
+    """The same on an HBM plan: a forward-only call of a 13-qubit circuit
+    keeps one 128 KiB state per row, so the 16 GiB state budget alone would
+    allow 131072 rows per launch; rows beyond the grid limit go to the next
+    chunk."""
+    rng = np.random.default_rng(77)
+    circ, tr = _rand_circuit(rng, 13, 30)
+    obs = _z_obs(rng, 13, 2)
+    x = rng.uniform(-2, 2, (64, 4))
+    eng = _engine()
+    small = eng.run_batch(_request(circ, obs, tr, x, ()))
+    B = 65535 + 200
+    big = eng.run_batch(_request(circ, obs, tr, np.tile(x, (B // 64 + 1, 1))[:B], ()))
+    assert big.expectations.shape == (B, 2)
+    for lo in (0, 65535 - 31, B - 64):
+        assert np.array_equal(big.expectations[lo:lo + 64], small.expectations[np.arange(lo, lo + 64) % 64])
+
+
 def test_failing_input_reports_index(torch_cuda):
     """Per-row failure reporting (reference tests/test_batch.py:196-209): the
     reference wraps a failing row's exception in BatchInputError(index); on
